@@ -1,0 +1,313 @@
+"""CPU oracle for arXiv 2010.03817 -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  It
+shares no code with ``paper_2010_03817_b200`` (the CUDA product path) and
+neither imports the other; both consume inputs from ``specgen``.
+
+The arithmetic lives in ``oracle.c`` (plain C99, fp64, no BLAS, built with
+``-O2 -ffp-contract=off -fno-fast-math``); this module is the ctypes binding
+plus the estimator drivers that follow PAPER.md step by step:
+
+* ``chord`` / ``normal`` / ``reflect`` -- Alg. 2, Lemma 3
+  (P:587-651), Alg. 3, lemma:gradient,
+  eq:reflection, with the Schur deflation of DESIGN.md R6 for
+  segments that start on the boundary.
+* ``walk`` / ``trace`` -- Billiard walk (Alg. 5) and HMC-r
+  (Alg. 6, eq:boltz_ode P:1440-1446).
+* ``volume`` -- ball-phase MMC (eq:mmc_vol P:1291-1306, telescoping product
+  P:1246-1259) with the schedule reading R11-R14.
+* ``expectation`` -- Monte-Carlo mean.
+
+Parity pins for every function are in ``tests/test_oracle_*.py``; see
+DESIGN.md "Oracle pins".  Functions without an independent pin say
+"parity unpinned" in their docstring.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liborc.so")
+
+INF = float("inf")
+BILLIARD, HMC = 0, 1
+TAG_WALK = 0 << 28
+TAG_VOLUME = 1 << 28
+TAG_PILOT = 3 << 28
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liborc.so (plain gcc, no fast-math, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
+    ):
+        cmd = [
+            "gcc", "-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+            "-D_POSIX_C_SOURCE=200809L", "-pthread", "-o", _LIB + ".tmp", _SRC, "-lm",
+        ]
+        subprocess.check_call(cmd, cwd=_HERE)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+_lib = None
+_dp = C.POINTER(C.c_double)
+
+
+class _ChordRes(C.Structure):
+    _fields_ = [
+        ("t_plus", C.c_double), ("t_minus", C.c_double), ("binding", C.c_int),
+        ("degenerate", C.c_int), ("outward", C.c_int), ("theta_max", C.c_double),
+        ("theta_2", C.c_double), ("ylen", C.c_int), ("y", C.c_double * (1024 + 8)),
+    ]
+
+
+class _Stats(C.Structure):
+    _fields_ = [(k, C.c_int64) for k in ("calls", "reflections", "rejects", "degenerates", "steps", "failures")]
+
+
+class _WalkParams(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("seed", C.c_uint64), ("tag", C.c_uint32), ("steps", C.c_int64),
+        ("L", C.c_double), ("rho", C.c_int64), ("T", C.c_double), ("c", _dp),
+    ]
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        l = C.CDLL(build())
+        l.orc_lmi_create.restype = C.c_void_p
+        l.orc_lmi_create.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_double, C.c_int]
+        l.orc_lmi_destroy.argtypes = [C.c_void_p]
+        l.orc_lmi_nblocks.argtypes = [C.c_void_p]
+        l.orc_lmi_block_size.argtypes = [C.c_void_p, C.c_int]
+        l.orc_eval_block.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        l.orc_dir_block.argtypes = [C.c_void_p, C.c_int, _dp, _dp]
+        l.orc_cholesky.argtypes = [C.c_int, _dp, _dp]
+        l.orc_jacobi.argtypes = [C.c_int, _dp, _dp, _dp]
+        l.orc_philox4x32_10.argtypes = [C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+        l.orc_u01.restype = C.c_double
+        l.orc_u01.argtypes = [C.c_uint32, C.c_uint32]
+        l.orc_step_draws.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _dp, _dp]
+        l.orc_chord.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_int, _dp, C.POINTER(_ChordRes)]
+        l.orc_normal.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, _dp]
+        l.orc_reflect.argtypes = [C.c_int, _dp, _dp, _dp]
+        l.orc_membership.argtypes = [C.c_void_p, _dp]
+        l.orc_walk.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, C.c_int64, _dp, C.c_int, _dp,
+                               C.POINTER(_Stats), C.c_int]
+        l.orc_trace.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp, _dp, _dp,
+                                _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        l.orc_qep_root.argtypes = [C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]
+        l.orc_hmc_chord.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp,
+                                    C.POINTER(_ChordRes)]
+        _lib = l
+    return _lib
+
+
+def _p(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_dp)
+
+
+def _arr(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+class Lmi:
+    """F(x) = blockdiag(dense F_0(x), cube blocks, ball arrow block) (eq:lmi P:70-75)."""
+
+    def __init__(self, inst, ball_c=None, ball_r: float = 0.0, literal: bool = False, cube: bool = True):
+        self.inst = inst
+        self.n, self.m = inst.n, inst.m
+        self._A = _arr(inst.A)
+        lo = _arr(inst.lo) if (cube and inst.lo is not None) else None
+        hi = _arr(inst.hi) if (cube and inst.hi is not None) else None
+        bc = _arr(ball_c) if ball_c is not None else None
+        self.has_cube = lo is not None
+        self.has_ball = bc is not None
+        self.ball_c, self.ball_r = bc, float(ball_r)
+        self._h = lib().orc_lmi_create(self.n, self.m, _p(self._A), _p(lo), _p(hi), _p(bc), float(ball_r),
+                                       1 if literal else 0)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.orc_lmi_destroy(self._h)
+            self._h = None
+
+    @property
+    def nblocks(self) -> int:
+        return lib().orc_lmi_nblocks(self._h)
+
+    def block_size(self, b: int) -> int:
+        return lib().orc_lmi_block_size(self._h, b)
+
+    def eval_block(self, b: int, x) -> np.ndarray:
+        s = self.block_size(b)
+        out = np.zeros((s, s))
+        lib().orc_eval_block(self._h, b, _p(_arr(x)), _p(out))
+        return out
+
+    def dir_block(self, b: int, v) -> np.ndarray:
+        s = self.block_size(b)
+        out = np.zeros((s, s))
+        lib().orc_dir_block(self._h, b, _p(_arr(v)), _p(out))
+        return out
+
+    def binding_code(self, b: int) -> int:
+        """ABI binding id: 0 dense, 1+2i cube upper, 2+2i cube lower, -1 ball."""
+        if self.has_ball and b == self.nblocks - 1:
+            return -1
+        return b
+
+
+def cholesky(A) -> Optional[np.ndarray]:
+    A = _arr(A)
+    m = A.shape[0]
+    L = np.zeros_like(A)
+    return None if lib().orc_cholesky(m, _p(A), _p(L)) else L
+
+
+def jacobi(A):
+    A = _arr(A)
+    m = A.shape[0]
+    ev = np.zeros(m)
+    V = np.zeros((m, m))
+    lib().orc_jacobi(m, _p(A), _p(ev), _p(V))
+    return ev, V
+
+
+def philox(ctr, key) -> np.ndarray:
+    c = (C.c_uint32 * 4)(*[int(x) & 0xFFFFFFFF for x in ctr])
+    k = (C.c_uint32 * 2)(*[int(x) & 0xFFFFFFFF for x in key])
+    o = (C.c_uint32 * 4)()
+    lib().orc_philox4x32_10(c, k, o)
+    return np.array(list(o), dtype=np.uint32)
+
+
+def u01(a: int, b: int) -> float:
+    return lib().orc_u01(a, b)
+
+
+def step_draws(seed: int, tag: int, chain: int, step: int, n: int):
+    g = np.zeros(n)
+    eta = C.c_double()
+    lib().orc_step_draws(seed, tag, chain, step, n, _p(g), C.byref(eta))
+    return g, eta.value
+
+
+def chord(lmi: Lmi, x, v, F0=None, bound: int = -1, u=None) -> dict:
+    """Boundary oracle on the line x + t v (Alg. 2 + Lemma 3; deflation R6)."""
+    r = _ChordRes()
+    x, v = _arr(x), _arr(v)
+    F0a = _arr(F0) if F0 is not None else None
+    ua = _arr(u) if u is not None else None
+    rc = lib().orc_chord(lmi._h, _p(x), _p(F0a), None, _p(v), int(bound), _p(ua), C.byref(r))
+    if rc:
+        raise ValueError(f"orc_chord failed rc={rc} (x not interior?)")
+    return dict(t_plus=r.t_plus, t_minus=r.t_minus, block=r.binding, binding=lmi.binding_code(r.binding)
+                if r.binding >= 0 else None, degenerate=bool(r.degenerate), outward=bool(r.outward),
+                theta_max=r.theta_max, theta_2=r.theta_2, y=np.array(r.y[: r.ylen]))
+
+
+def normal(lmi: Lmi, block: int, y) -> Optional[np.ndarray]:
+    y = _arr(y)
+    w = np.zeros(lmi.n)
+    rc = lib().orc_normal(lmi._h, block, _p(y), len(y), _p(w))
+    return None if rc else w
+
+
+def reflect(u, w) -> np.ndarray:
+    u, w = _arr(u), _arr(w)
+    s = np.zeros_like(u)
+    lib().orc_reflect(len(u), _p(u), _p(w), _p(s))
+    return s
+
+
+def membership(lmi: Lmi, x) -> bool:
+    return bool(lib().orc_membership(lmi._h, _p(_arr(x))))
+
+
+def qep_root(B0, B1, B2, u=None):
+    """First positive root of det(B0 + t B1 + t^2 B2) (companion + Francis QR)."""
+    B0, B1, B2 = _arr(B0), _arr(B1), _arr(B2)
+    mb = B0.shape[0]
+    tp = C.c_double()
+    y = np.zeros(mb)
+    ua = _arr(u) if u is not None else None
+    rc = lib().orc_qep_root(mb, _p(B0), _p(B1), _p(B2), 1 if u is not None else 0, _p(ua), C.byref(tp), _p(y))
+    if rc:
+        raise ValueError(f"qep_root rc={rc}")
+    return tp.value, y
+
+
+def hmc_chord(lmi: Lmi, x, v, c, T, F0=None, bound=-1, u=None) -> dict:
+    r = _ChordRes()
+    x, v, c = _arr(x), _arr(v), _arr(c)
+    F0a = _arr(F0) if F0 is not None else None
+    ua = _arr(u) if u is not None else None
+    rc = lib().orc_hmc_chord(lmi._h, _p(x), _p(F0a), _p(v), _p(c), float(T), int(bound), _p(ua), C.byref(r))
+    if rc:
+        raise ValueError(f"hmc_chord rc={rc}")
+    return dict(t_plus=r.t_plus, block=r.binding, outward=bool(r.outward), y=np.array(r.y[: r.ylen]))
+
+
+def _params(kind, seed, tag, steps, L, rho, T=1.0, c=None):
+    p = _WalkParams()
+    p.kind, p.seed, p.tag, p.steps, p.L, p.rho, p.T = kind, seed, tag, steps, float(L), rho, float(T)
+    keep = _arr(c) if c is not None else None
+    p.c = _p(keep)
+    return p, keep
+
+
+def walk(lmi: Lmi, kind: int, seed: int, chain_begin: int, chain_end: int, steps: int, L: float, rho: int,
+         x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, nthreads: int = 0):
+    """Run chains [chain_begin, chain_end) (global ids key the RNG). Returns (final_x, stats)."""
+    n = lmi.n
+    if x0 is None:
+        x0 = np.zeros(n)
+    x0 = _arr(x0)
+    stride = 0 if x0.ndim == 1 else n
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    out = np.zeros((chain_end - chain_begin, n))
+    st = _Stats()
+    if nthreads <= 0:
+        nthreads = os.cpu_count() or 1
+    rc = lib().orc_walk(lmi._h, C.byref(p), chain_begin, chain_end, _p(x0), stride, _p(out), C.byref(st),
+                        nthreads)
+    if rc:
+        raise ValueError(f"orc_walk rc={rc}")
+    return out, {k: getattr(st, k) for k, _ in _Stats._fields_}
+
+
+def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_refl: int,
+          x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK) -> dict:
+    n = lmi.n
+    x0 = _arr(np.zeros(n) if x0 is None else x0)
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    hit = np.zeros((max_refl, n))
+    t = np.zeros(max_refl)
+    w = np.zeros((max_refl, n))
+    va = np.zeros((max_refl, n))
+    bind = np.zeros(max_refl, dtype=np.int32)
+    nrec = C.c_int64()
+    rc = lib().orc_trace(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
+                         bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec))
+    if rc:
+        raise ValueError(f"orc_trace rc={rc}")
+    k = nrec.value
+    return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k])
+
+
+def ball_volume(n: int, r: float = 1.0) -> float:
+    """omega_n r^n = pi^(n/2) / Gamma(n/2+1) r^n."""
+    return math.exp(0.5 * n * math.log(math.pi) - math.lgamma(0.5 * n + 1) + n * math.log(r))

@@ -1,0 +1,164 @@
+"""Pins for the oracle's walks and QEP (-m "not gpu"): closed-form moments of
+uniform / Boltzmann distributions on bodies with known laws (P1-P3), HMC
+energy conservation (P11), QEP root vs brute-force scanning (P12), and
+sharding determinism (P15)."""
+import numpy as np
+import pytest
+
+import oracle
+import specgen
+
+
+def _lmi_full(inst, x):
+    return inst.A[0] + np.tensordot(x, inst.A[1:], axes=1)
+
+
+def _brute_first_root(B0, B1, B2, t0=0.0, dt=1e-3, tmax=50.0):
+    """Scan lambda_min(B0 + t B1 + t^2 B2) (LAPACK) for the first sign change after t0, then bisect."""
+    f = lambda t: np.linalg.eigvalsh(B0 + t * B1 + t * t * B2)[0]
+    t = t0 + dt
+    while t < tmax and f(t) > 0:
+        t += dt
+    if t >= tmax:
+        return np.inf
+    lo, hi = t - dt, t
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        if mid in (lo, hi):
+            break
+        if f(mid) > 0:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+# ---------------------------------------------------------------- P12 QEP
+def test_qep_interior_vs_brute_force():
+    rng = np.random.default_rng(11)
+    for m in (1, 3, 6, 10):
+        for _ in range(4):
+            Z = rng.standard_normal((m, m))
+            B0 = Z @ Z.T + np.eye(m)
+            B1 = rng.standard_normal((m, m)); B1 = B1 + B1.T
+            B2 = rng.standard_normal((m, m)); B2 = -(B2 @ B2.T) / 4 + 0.3 * (B2 + B2.T)
+            tp, y = oracle.qep_root(B0, B1, B2)
+            tb = _brute_first_root(B0, B1, B2)
+            if np.isinf(tb):
+                assert np.isinf(tp) or tp > 49
+                continue
+            assert abs(tp - tb) <= 1e-11 * max(1, tb), (m, tp, tb)
+            G = B0 + tp * B1 + tp * tp * B2
+            yn = y / np.linalg.norm(y)
+            scale = max(np.abs(B0).max(), tp * np.abs(B1).max(), tp * tp * np.abs(B2).max())
+            assert np.linalg.norm(G @ yn) <= 1e-12 * scale
+
+
+def test_qep_boundary_start_vs_brute_force():
+    rng = np.random.default_rng(12)
+    for m in (1, 4, 8):
+        for _ in range(4):
+            Z = rng.standard_normal((m, m))
+            B0 = Z @ Z.T + np.eye(m)
+            B1 = rng.standard_normal((m, m)); B1 = B1 + B1.T
+            B2 = -np.eye(m) * 0.5
+            t1, y = oracle.qep_root(B0, B1, B2)
+            assert np.isfinite(t1)
+            # move to the hit; the new pencil in s = t - t1 starts on the boundary
+            C0 = B0 + t1 * B1 + t1 * t1 * B2
+            C1 = -(B1 + 2 * t1 * B2)  # reverse direction -> inward start
+            u = y / np.linalg.norm(y)
+            if u @ C1 @ u <= 0:
+                continue
+            t2, _ = oracle.qep_root(C0, C1, B2, u=u)
+            tb = _brute_first_root(C0, C1, B2, t0=1e-7, dt=1e-3)
+            assert abs(t2 - tb) <= 1e-9 * max(1, tb), (m, t2, tb)
+
+
+# ---------------------------------------------------------------- P11 HMC energy
+def test_hmc_energy_conserved_across_reflections():
+    inst = specgen.rand_cube(5, 6, 13)
+    L = oracle.Lmi(inst)
+    c = specgen.objective(5, 13)
+    T = 0.7
+    for chain in range(4):
+        tr = oracle.trace(L, oracle.HMC, seed=3, chain=chain, steps=1, L=6.0, rho=200, max_refl=50, T=T, c=c)
+        g, _ = oracle.step_draws(3, 0, chain, 0, 5)
+        E0 = 0.5 * g @ g  # x0 = 0
+        for k in range(len(tr["t"])):
+            E = c @ tr["hit_x"][k] / T + 0.5 * tr["v_after"][k] @ tr["v_after"][k]
+            assert abs(E - E0) <= 1e-12 * max(1.0, abs(E0))
+
+
+# ---------------------------------------------------------------- billiard trace invariants
+def test_billiard_trace_invariants():
+    inst = specgen.rand_cube(8, 8, 14)
+    L = oracle.Lmi(inst)
+    tr = oracle.trace(L, oracle.BILLIARD, seed=0, chain=3, steps=20, L=2 * np.sqrt(8), rho=80, max_refl=20)
+    assert len(tr["t"]) == 20
+    for k in range(20):
+        assert abs(np.linalg.norm(tr["v_after"][k]) - 1) < 1e-14
+        x = tr["hit_x"][k]
+        if tr["binding"][k] == 0:
+            F = _lmi_full(inst, x)
+            assert abs(np.linalg.eigvalsh(F)[0]) <= 1e-12 * np.abs(F).max()
+        else:
+            i = (tr["binding"][k] - 1) // 2
+            assert abs(abs(x[i]) - 1) < 1e-14
+        # specular law: w . v_after = -(w . v_before) and v_after tangential part matches
+        assert tr["w"][k] @ tr["v_after"][k] < 0
+
+
+# ---------------------------------------------------------------- P15 sharding determinism
+def test_walk_sharding_bit_identical():
+    inst = specgen.rand_cube(6, 6, 15)
+    L = oracle.Lmi(inst)
+    a, sa = oracle.walk(L, oracle.BILLIARD, 5, 0, 12, 10, 2 * np.sqrt(6), 60, nthreads=3)
+    b1, _ = oracle.walk(L, oracle.BILLIARD, 5, 0, 5, 10, 2 * np.sqrt(6), 60, nthreads=1)
+    b2, _ = oracle.walk(L, oracle.BILLIARD, 5, 5, 12, 10, 2 * np.sqrt(6), 60, nthreads=2)
+    assert np.array_equal(a, np.vstack([b1, b2]))
+    assert sa["steps"] == 120 and sa["calls"] >= 120
+
+
+# ---------------------------------------------------------------- P1-P3 uniform moments
+def _check_moment(vals, expect, nsig=4.5):
+    se = vals.std(ddof=1) / np.sqrt(len(vals))
+    assert abs(vals.mean() - expect) <= nsig * se + 1e-12, (vals.mean(), expect, se)
+
+
+@pytest.mark.parametrize("body", ["cube", "cube_dense", "ball", "elliptope3"])
+def test_billiard_uniform_moments(body):
+    if body == "cube":
+        inst, ex2 = specgen.cube_only(3), 1 / 3
+    elif body == "cube_dense":
+        inst, ex2 = specgen.cube_dense(3), 1 / 3
+    elif body == "ball":
+        inst, ex2 = specgen.ball(4), 1 / 6  # E[x_i^2] = 1/(n+2)
+    else:
+        inst, ex2 = specgen.elliptope(3), 1 / 4  # E[x^2] = 1/(k+1)
+    L = oracle.Lmi(inst)
+    n = inst.n
+    X, st = oracle.walk(L, oracle.BILLIARD, 21, 0, 600, 25, 2 * np.sqrt(n), 10 * n)
+    # coordinates are exchangeable: average per chain to get iid samples
+    _check_moment((X ** 2).mean(axis=1), ex2)
+    _check_moment(X.mean(axis=1), 0.0)
+    assert st["failures"] == 0
+
+
+def test_hmc_boltzmann_cube_moments():
+    """pi(x) ~ exp(-c.x/T) on [-1,1]^n: independent truncated exponentials (P1, V7)."""
+    n = 3
+    inst = specgen.cube_only(n)
+    L = oracle.Lmi(inst)
+    c = np.array([1.0, -0.6, 2.5])
+    T = 1.0
+    X, st = oracle.walk(L, oracle.HMC, 4, 0, 800, 20, 2.0, 100, T=T, c=c)
+    grid = np.linspace(-1, 1, 200001)
+    for i in range(n):
+        dens = np.exp(-c[i] * grid / T)
+        Z = np.trapezoid(dens, grid)
+        e1 = np.trapezoid(grid * dens, grid) / Z
+        e2 = np.trapezoid(grid ** 2 * dens, grid) / Z
+        _check_moment(X[:, i], e1)
+        _check_moment(X[:, i] ** 2, e2)
+    assert st["failures"] == 0
