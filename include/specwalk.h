@@ -1,0 +1,178 @@
+/*
+ * specwalk.h -- C-ABI of the B200-native spectrahedron boundary oracle and the
+ * walks / estimators above it (arXiv 2010.03817, /root/reference/PAPER.md).
+ *
+ * "P:123" = PAPER.md line 123.  All floating point is IEEE fp64.
+ *
+ * Conventions for every call
+ * --------------------------
+ * - Return value: SPEC_OK (0) or one of the SPEC_E* codes below; the message of
+ *   the last failure on the calling thread is spec_last_error().
+ * - Host pointers ("host") are read/written synchronously: the call returns
+ *   after the device work and the copies finished.  "_dev" variants take
+ *   DEVICE pointers on the context's GPU and are asynchronous with respect to
+ *   the host only where stated.
+ * - The library never falls back to the CPU: without a usable CUDA device
+ *   spec_create fails with SPEC_ECUDA.
+ * - Calls on one context are not re-entrant; distinct contexts are independent.
+ * - Layouts are row-major.  n = ambient dimension, m = matrix size of the LMI.
+ * - A "boundary-oracle call" (the unit of BASELINE.json's metric) is one chord
+ *   solve (Alg. 2) plus, if the segment ends on a dense-block hit,
+ *   the normal (lemma:gradient), for one chain on one segment.
+ */
+#ifndef SPECWALK_H
+#define SPECWALK_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SPEC_OK = 0,
+    SPEC_EINVAL = 1,     /* bad argument (sizes, NaN, asymmetry, unknown kind) */
+    SPEC_EPRECOND = 2,   /* a precondition of the paper fails (start not interior) */
+    SPEC_ERUNTIME = 3,   /* numerical failure that is not a counted walk event */
+    SPEC_ECUDA = 4,      /* CUDA / NCCL error or no device */
+    SPEC_ENOMEM = 5,     /* device allocation failed */
+    SPEC_EUNBOUNDED = 6  /* t+ = +inf: S is unbounded along a direction */
+};
+
+/* binding ids returned per hit */
+#define SPEC_BIND_DENSE 0   /* the dense LMI block A(x) */
+#define SPEC_BIND_BALL (-1) /* the ball constraint of a volume phase */
+/* cube: 1+2i = upper face x_i = hi_i, 2+2i = lower face x_i = lo_i */
+#define SPEC_BIND_NONE (-2)
+
+typedef struct spec_ctx spec_ctx;
+
+const char* spec_last_error(void);
+
+/* spec_create -- upload an LMI F(x) = A0 + sum_i x_i A_i (eq:lmi).
+ *  n, m     : ambient dimension (>=1) and matrix size (1..SPEC_MAX_M).
+ *  A        : host, (n+1)*m*m doubles, A[0] = A0, A[i] = A_i, each m x m
+ *             row-major; symmetrised as (A+A^T)/2 on load.  Copied: the
+ *             caller keeps ownership.
+ *  cube_lo, cube_hi : host, n doubles each, or both NULL (no cube block).  The
+ *             cube is the diagonal part of the LMI (hi_i - x_i >= 0,
+ *             x_i - lo_i >= 0) handled in closed form.
+ *  device   : CUDA device ordinal (-1 = current device).
+ *  out      : receives the context (owns all device memory).
+ * Errors: EINVAL for n<1, m<1, m>SPEC_MAX_M, NaN/Inf, |A-A^T| > 1e-12 max(1,|A|),
+ *         lo>=hi; ECUDA / ENOMEM. */
+#define SPEC_MAX_M 256
+int spec_create(int n, int m, const double* A, const double* cube_lo, const double* cube_hi, int device,
+                spec_ctx** out);
+int spec_destroy(spec_ctx* ctx);
+
+/* Objective c (n doubles, host) for the Boltzmann density exp(-c^T x / T) of
+ * HMC-r (eq:boltz_ode).  EINVAL if |c| = 0. */
+int spec_set_objective(spec_ctx* ctx, const double* c);
+
+/* Ball constraint |x - center| <= radius added to S (a volume phase S_i of
+ * eq:mmc_vol).  radius <= 0 removes it.  center: host n doubles. */
+int spec_set_ball(spec_ctx* ctx, const double* center, double radius);
+
+/* boundary_oracle -- the batched INTERSECTION + REFLECTION normal
+ * (Alg. 2, Alg. 3) on lines x_b + t v_b.
+ *  batch    : number of lines (>=0; 0 is a no-op).
+ *  x, v     : host, batch x n.  v need not be unit (t scales with 1/|v|).
+ *  u        : host, batch x m, or NULL.  If given, x_b is ON the boundary of
+ *             the dense block with unit kernel vector u_b (F(x_b) u_b = 0) and
+ *             the chord is solved by Schur deflation (R6); t_minus
+ *             is then 0 for that block.
+ *  t_minus, t_plus : host, batch doubles (Lemma 3: max negative / min
+ *             positive root of det F(x + t v)).  +-inf if unbounded.
+ *  normal   : host, batch x n: outward unit normal at x + t_plus v
+ *             (-grad det F / |grad det F|, lemma:gradient P:752-764; cube faces
+ *             +-e_i; ball (x_hit - c)/r), or NaN if the hit is degenerate.
+ *  kernel   : host, batch x m or NULL: unit kernel vector of F(x + t_plus v)
+ *             for dense hits (the PEP eigenvector), else zeros.
+ *  binding  : host, batch int32: SPEC_BIND_* id of the first strict minimum
+ *             (tie order dense, cube i = 0..n-1, ball).
+ * Errors: EPRECOND if some x_b is not interior (Cholesky of F(x_b) fails) and
+ *         u == NULL; the outputs of the other lines are still written. */
+int boundary_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
+                    double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding);
+/* same, all pointers on the device (asynchronous on the context stream until
+ * spec_sync; u / kernel may be NULL). */
+int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
+                        double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding);
+
+/* ---- walks ---- */
+enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1 };
+
+typedef struct spec_walk_params {
+    int kind;            /* SPEC_WALK_BILLIARD (Alg. 5) or SPEC_WALK_HMC (Alg. 6, Boltzmann) */
+    int64_t chain_begin; /* global id of this rank's first chain (keys the RNG) */
+    int64_t chains;      /* number of chains run by this call */
+    int64_t steps;       /* walk steps per chain (each ends in accept or reject) */
+    double L;            /* tau: billiard l = -tau ln eta; HMC l = tau eta */
+    int64_t rho;         /* reflection bound (reject the step when #refl > rho) */
+    uint64_t seed;       /* Philox4x32-10 key */
+    uint32_t tag;        /* counter word 3 (purpose << 28 | phase), 0 for plain walks */
+    double T;            /* HMC temperature (>0); ignored for billiard */
+} spec_walk_params;
+
+typedef struct spec_walk_stats {
+    int64_t calls;       /* boundary-oracle calls (device-counted) */
+    int64_t reflections;
+    int64_t rejects;     /* steps rejected because #refl > rho */
+    int64_t degenerates; /* steps rejected at a rank <= m-2 / corner hit */
+    int64_t failures;    /* chains whose start was not interior */
+    int64_t steps;
+    int64_t rounds;      /* scheduler rounds (one oracle call per active chain) */
+    double device_ms;    /* CUDA-event time of the walk on the context stream */
+} spec_walk_stats;
+
+/* walk_sample -- run p->chains independent chains for p->steps steps each
+ * from x0 (host: n doubles shared by all chains, or chains x n if
+ * x0_per_chain, or NULL = origin).  Outputs (host, may be NULL):
+ *  sum_x   : n doubles, sum over chains of the end points;
+ *  sum_xx  : n(n+1)/2 doubles, packed lower sum of x x^T over end points;
+ *  final_x : chains x n end points.
+ * Sums are accumulated in fixed chain order (deterministic). */
+int walk_sample(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain, double* sum_x,
+                double* sum_xx, double* final_x, spec_walk_stats* st);
+/* device variant: x0 and outputs are device pointers (x0 may be NULL). */
+int walk_sample_dev(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain, double* sum_x,
+                    double* sum_xx, double* final_x, spec_walk_stats* st);
+
+/* walk_trace -- the first max_refl reflections of each chain in chain_ids
+ * (global ids), for parity.  Outputs host, nchains x max_refl x {n,1,n,n,1};
+ * nrec[k] = number recorded for chain k. */
+int walk_trace(spec_ctx* ctx, const spec_walk_params* p, const int64_t* chain_ids, int64_t nchains,
+               int64_t max_refl, double* hit_x, double* t, double* w, double* v_after, int32_t* binding,
+               int64_t* nrec);
+
+/* ---- resumable walk (the scheduler behind walk_sample) ----
+ * walk_begin  : set up p->chains chains at x0_dev (DEVICE pointer, n or chains x n
+ *               doubles, or NULL = origin), draw step 0.
+ * walk_rounds : run up to max_rounds scheduler rounds (<= 0: until all chains
+ *               finished); one round = one boundary-oracle call per active
+ *               chain.  *active receives the number of unfinished chains.
+ * walk_end    : statistics and DEVICE outputs (any may be NULL), as walk_sample.
+ * spec_walk_stats_now : statistics of the walk in progress (device counters). */
+int walk_begin(spec_ctx* ctx, const spec_walk_params* p, const double* x0_dev, int x0_per_chain);
+int walk_rounds(spec_ctx* ctx, int64_t max_rounds, int64_t* active);
+int walk_end(spec_ctx* ctx, double* sum_x_dev, double* sum_xx_dev, double* final_x_dev, spec_walk_stats* st);
+int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st);
+
+/* Per-kernel CUDA-event timing of the walk scheduler (off by default; adds a
+ * host sync per round).  spec_kernel_times returns accumulated ms and launch
+ * counts for K1 (A(v) GEMM), K2 (chord), K3 (normal GEMM), K4 (reflect), and the
+ * number of chain slots K2 processed (including finished ones not yet compacted). */
+int spec_kernel_timing(spec_ctx* ctx, int enable);
+int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items);
+
+/* Make the host wait for all work queued on the context stream. */
+int spec_sync(spec_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for callers timing with events. */
+void* spec_stream(spec_ctx* ctx);
+/* Number of kernels this context launched since creation (evidence counter). */
+int64_t spec_kernel_launches(spec_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

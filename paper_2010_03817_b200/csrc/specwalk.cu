@@ -1,0 +1,828 @@
+// specwalk.cu -- host side of the C-ABI (include/specwalk.h): context, device
+// memory layout, the round scheduler that drives the kernels, and the
+// boundary_oracle / walk_sample / walk_trace entry points.
+//
+// Device layout (per context / GPU):
+//   Ahat   : np x mtp   row i = packed lower(A_{i+1}), zero padded
+//   a0     : mtp        packed lower(A0)
+//   chains : X, Xs, V (C x np); AX, AXs, AV, Yh (C x mtp); U (C x m); Gn (C x np)
+//            scalar SoA: ell, steps_done, refl, bound, flags, counters
+// np = roundup(n, 64), mt = m(m+1)/2, mtp = roundup(mt, 64).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/specwalk.h"
+#include "gemm.cuh"
+#include "walk.cuh"
+
+using namespace sw;
+
+static thread_local std::string g_err;
+
+extern "C" const char* spec_last_error(void) { return g_err.c_str(); }
+
+static int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) return fail(SPEC_ECUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+static int roundup(int a, int b) { return (a + b - 1) / b * b; }
+
+struct ChainBuf {
+    long long cap = 0;
+    double *X = nullptr, *Xs = nullptr, *V = nullptr, *AX = nullptr, *AXs = nullptr, *AV = nullptr, *Yh = nullptr,
+           *U = nullptr, *Gn = nullptr, *ell = nullptr;
+    int *steps_done = nullptr, *refl = nullptr, *bound = nullptr, *flags = nullptr, *nrej = nullptr, *ndeg = nullptr;
+    long long *calls = nullptr, *nrefl = nullptr;
+    int *list = nullptr, *list2 = nullptr, *nlist = nullptr;
+    int* counters = nullptr;  // [0] count, [1] count2, [2] ncount
+    long long* gid = nullptr;
+};
+
+struct spec_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    int n = 0, m = 0, np = 0, mt = 0, mtp = 0, ld = 0;
+    double* Ahat = nullptr;
+    double* a0 = nullptr;
+    double *lo = nullptr, *hi = nullptr;
+    int has_cube = 0;
+    double* c = nullptr;
+    int has_obj = 0;
+    double* ball_c = nullptr;
+    double ball_r = 0.0;
+    int has_ball = 0;
+    double amax = 0.0;
+    ChainBuf cb;
+    double* scratch = nullptr;
+    long long scratch_stride = 0;
+    int scratch_ctas = 0;
+    bool smem_path = true;
+    size_t smem_bytes = 0;
+    int chord_threads = 256;
+    int chord_grid_max = 0;
+    int num_sms = 0;
+    long long* dstats = nullptr;
+    unsigned long long* prof = nullptr;
+    long long launches = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    void* walk = nullptr;  // WalkRun*
+};
+
+static void free_chains(ChainBuf& b) {
+    void* ps[] = {b.X, b.Xs, b.V, b.AX, b.AXs, b.AV, b.Yh, b.U, b.Gn, b.ell, b.steps_done, b.refl, b.bound,
+                  b.flags, b.nrej, b.ndeg, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    b = ChainBuf();
+}
+
+template <typename T>
+static cudaError_t zalloc(T** p, size_t count) {
+    cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
+    if (e == cudaSuccess) e = cudaMemset(*p, 0, sizeof(T) * (count ? count : 1));
+    return e;
+}
+
+static int ensure_chains(spec_ctx* ctx, long long C) {
+    ChainBuf& b = ctx->cb;
+    if (C <= b.cap) return SPEC_OK;
+    free_chains(b);
+    long long cap = C;
+    size_t np = ctx->np, mtp = ctx->mtp, m = ctx->m;
+    cudaError_t e = cudaSuccess;
+#define ZA(ptr, cnt) \
+    if (e == cudaSuccess) e = zalloc(&b.ptr, (size_t)(cnt));
+    ZA(X, cap * np) ZA(Xs, cap * np) ZA(V, cap * np) ZA(Gn, cap * np) ZA(AX, cap * mtp) ZA(AXs, cap * mtp)
+    ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(steps_done, cap) ZA(refl, cap)
+    ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
+    ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap)
+#undef ZA
+    if (e != cudaSuccess) {
+        free_chains(b);
+        cudaGetLastError();
+        return fail(SPEC_ENOMEM, std::string("chain buffers: ") + cudaGetErrorString(e));
+    }
+    b.cap = cap;
+    return SPEC_OK;
+}
+
+extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo, const double* cube_hi,
+                           int device, spec_ctx** out) {
+    if (!out) return fail(SPEC_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || m < 1 || m > SPEC_MAX_M || !A) return fail(SPEC_EINVAL, "bad n/m/A");
+    if ((cube_lo == nullptr) != (cube_hi == nullptr)) return fail(SPEC_EINVAL, "cube_lo/cube_hi: both or neither");
+    const size_t mm = (size_t)m * m;
+    for (size_t e = 0; e < (size_t)(n + 1) * mm; ++e)
+        if (!std::isfinite(A[e])) return fail(SPEC_EINVAL, "A has NaN/Inf");
+    for (int k = 0; k <= n; ++k)
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < i; ++j) {
+                double a = A[k * mm + (size_t)i * m + j], b = A[k * mm + (size_t)j * m + i];
+                if (std::fabs(a - b) > 1e-12 * std::fmax(1.0, std::fabs(a)))
+                    return fail(SPEC_EINVAL, "A_" + std::to_string(k) + " is not symmetric");
+            }
+    if (cube_lo)
+        for (int i = 0; i < n; ++i)
+            if (!(cube_lo[i] < cube_hi[i])) return fail(SPEC_EINVAL, "cube_lo >= cube_hi");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(SPEC_ECUDA, "no CUDA device (the library has no CPU fallback)");
+    }
+    spec_ctx* ctx = new spec_ctx();
+    if (device < 0) cudaGetDevice(&device);
+    ctx->dev = device;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&ctx->e0));
+    CK(cudaEventCreate(&ctx->e1));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    ctx->num_sms = prop.multiProcessorCount;
+    ctx->n = n;
+    ctx->m = m;
+    ctx->np = roundup(n, 64);
+    ctx->mt = m * (m + 1) / 2;
+    ctx->mtp = roundup(ctx->mt, 64);
+    ctx->ld = m | 1;
+    // packed, symmetrised, padded coefficient matrix
+    std::vector<double> Ah((size_t)ctx->np * ctx->mtp, 0.0), a0((size_t)ctx->mtp, 0.0);
+    double amax = 0.0;
+    for (int k = 0; k <= n; ++k)
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j <= i; ++j) {
+                double v = 0.5 * (A[k * mm + (size_t)i * m + j] + A[k * mm + (size_t)j * m + i]);
+                if (k == 0) a0[pk(i, j)] = v;
+                else {
+                    Ah[(size_t)(k - 1) * ctx->mtp + pk(i, j)] = v;
+                    amax = std::fmax(amax, std::fabs(v));
+                }
+            }
+    ctx->amax = amax;
+    CK(zalloc(&ctx->Ahat, Ah.size()));
+    CK(zalloc(&ctx->a0, a0.size()));
+    CK(cudaMemcpy(ctx->Ahat, Ah.data(), sizeof(double) * Ah.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->a0, a0.data(), sizeof(double) * a0.size(), cudaMemcpyHostToDevice));
+    if (cube_lo) {
+        CK(zalloc(&ctx->lo, n));
+        CK(zalloc(&ctx->hi, n));
+        CK(cudaMemcpy(ctx->lo, cube_lo, sizeof(double) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->hi, cube_hi, sizeof(double) * n, cudaMemcpyHostToDevice));
+        ctx->has_cube = 1;
+    }
+    CK(zalloc(&ctx->c, ctx->np));
+    CK(zalloc(&ctx->ball_c, ctx->np));
+    CK(zalloc(&ctx->dstats, 8));
+    if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 16));
+    // K2 placement: shared memory if it fits, else a global scratch slice per CTA
+    size_t per_cta = (size_t)2 * m * ctx->ld + (size_t)NVEC * m + 64;
+    ctx->smem_bytes = per_cta * sizeof(double);
+    ctx->chord_threads = (m <= 32) ? 64 : (m <= 64 ? 128 : 256);
+    if (ctx->smem_bytes <= 200 * 1024) {
+        ctx->smem_path = true;
+        CK(cudaFuncSetAttribute(chord_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ctx->smem_bytes));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel<true>, ctx->chord_threads,
+                                                         ctx->smem_bytes));
+        if (occ < 1) occ = 1;
+        ctx->chord_grid_max = occ * ctx->num_sms;
+    } else {
+        ctx->smem_path = false;
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel<false>, ctx->chord_threads, 0));
+        if (occ < 1) occ = 1;
+        if (occ > 2) occ = 2;
+        ctx->chord_grid_max = occ * ctx->num_sms;
+        ctx->scratch_stride = (long long)roundup((int)per_cta, 32);
+        ctx->scratch_ctas = ctx->chord_grid_max;
+        CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
+        ctx->smem_bytes = 0;
+    }
+    *out = ctx;
+    return SPEC_OK;
+}
+
+static void free_walk(spec_ctx* ctx);
+extern "C" int spec_destroy(spec_ctx* ctx) {
+    if (!ctx) return SPEC_OK;
+    free_walk(ctx);
+    cudaSetDevice(ctx->dev);
+    free_chains(ctx->cb);
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    if (ctx->e0) cudaEventDestroy(ctx->e0);
+    if (ctx->e1) cudaEventDestroy(ctx->e1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return SPEC_OK;
+}
+
+extern "C" int spec_sync(spec_ctx* ctx) {
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPEC_OK;
+}
+extern "C" void* spec_stream(spec_ctx* ctx) { return (void*)ctx->stream; }
+extern "C" int64_t spec_kernel_launches(spec_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
+    if (!ctx || !c) return fail(SPEC_EINVAL, "null argument");
+    double s = 0.0;
+    for (int i = 0; i < ctx->n; ++i) s += c[i] * c[i];
+    if (!(s > 0.0) || !std::isfinite(s)) return fail(SPEC_EINVAL, "|c| must be finite and > 0");
+    CK(cudaSetDevice(ctx->dev));
+    CK(cudaMemcpy(ctx->c, c, sizeof(double) * ctx->n, cudaMemcpyHostToDevice));
+    ctx->has_obj = 1;
+    return SPEC_OK;
+}
+
+extern "C" int spec_set_ball(spec_ctx* ctx, const double* center, double radius) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    CK(cudaSetDevice(ctx->dev));
+    if (!(radius > 0.0)) {
+        ctx->has_ball = 0;
+        return SPEC_OK;
+    }
+    if (!center) return fail(SPEC_EINVAL, "center is NULL");
+    CK(cudaMemcpy(ctx->ball_c, center, sizeof(double) * ctx->n, cudaMemcpyHostToDevice));
+    ctx->ball_r = radius;
+    ctx->has_ball = 1;
+    return SPEC_OK;
+}
+
+// ---------------------------------------------------------------- kernel launch helpers
+static void launch_gemm_av(spec_ctx* ctx, const double* Arows, const int* list, const int* count_dev,
+                           int count_host, double* out, const double* bias) {
+    dim3 grid(ctx->mtp / GB_N, (count_host + GB_M - 1) / GB_M);
+    gemm_f64_dmma<false><<<grid, 128, 0, ctx->stream>>>(Arows, ctx->np, list, count_dev, count_host, ctx->Ahat,
+                                                        ctx->mtp, out, ctx->mtp, bias, ctx->np);
+    ctx->launches++;
+}
+static void launch_gemm_normal(spec_ctx* ctx, const int* list, const int* count_dev, int count_host) {
+    dim3 grid(ctx->np / GB_N, (count_host + GB_M - 1) / GB_M);
+    gemm_f64_dmma<true><<<grid, 128, 0, ctx->stream>>>(ctx->cb.Yh, ctx->mtp, list, count_dev, count_host,
+                                                       ctx->Ahat, ctx->mtp, ctx->cb.Gn, ctx->np, nullptr, ctx->mtp);
+    ctx->launches++;
+}
+
+static ChordParams chord_params(spec_ctx* ctx, int mode) {
+    ChordParams P;
+    memset(&P, 0, sizeof(P));
+    ChainBuf& b = ctx->cb;
+    P.n = ctx->n; P.np = ctx->np; P.m = ctx->m; P.mt = ctx->mt; P.mtp = ctx->mtp; P.ld = ctx->ld;
+    P.mode = mode;
+    P.AV = b.AV; P.AX = b.AX; P.AXs = b.AXs; P.Yh = b.Yh; P.X = b.X; P.Xs = b.Xs; P.V = b.V; P.U = b.U;
+    P.ell = b.ell; P.steps_done = b.steps_done; P.refl = b.refl; P.bound = b.bound; P.flags = b.flags;
+    P.calls = b.calls; P.nrefl = b.nrefl; P.nrej = b.nrej; P.ndeg = b.ndeg;
+    P.lo = ctx->has_cube ? ctx->lo : nullptr;
+    P.hi = ctx->has_cube ? ctx->hi : nullptr;
+    P.ball_c = ctx->ball_c; P.ball_r = ctx->ball_r; P.has_ball = ctx->has_ball;
+    P.scratch = ctx->scratch; P.scratch_stride = ctx->scratch_stride;
+    P.nlist = b.nlist; P.ncount = b.counters + 2;
+    P.prof = ctx->prof;
+    return P;
+}
+
+static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
+    int grid = count_host < ctx->chord_grid_max ? count_host : ctx->chord_grid_max;
+    if (grid < 1) grid = 1;
+    if (ctx->smem_path)
+        chord_kernel<true><<<grid, ctx->chord_threads, ctx->smem_bytes, ctx->stream>>>(P);
+    else
+        chord_kernel<false><<<grid, ctx->chord_threads, 0, ctx->stream>>>(P);
+    ctx->launches++;
+}
+
+static NormalParams normal_params(spec_ctx* ctx, int mode) {
+    NormalParams Q;
+    memset(&Q, 0, sizeof(Q));
+    ChainBuf& b = ctx->cb;
+    Q.n = ctx->n; Q.np = ctx->np; Q.m = ctx->m; Q.mt = ctx->mt; Q.mtp = ctx->mtp; Q.mode = mode;
+    Q.Gn = b.Gn; Q.V = b.V; Q.X = b.X; Q.Xs = b.Xs; Q.AX = b.AX; Q.AXs = b.AXs; Q.ell = b.ell;
+    Q.steps_done = b.steps_done; Q.refl = b.refl; Q.bound = b.bound; Q.flags = b.flags; Q.ndeg = b.ndeg;
+    Q.amax = ctx->amax;
+    Q.ball_c = ctx->ball_c; Q.ball_r = ctx->ball_r;
+    return Q;
+}
+
+// ---------------------------------------------------------------- boundary_oracle
+static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const double* dv, const double* du,
+                       double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
+                       bool host_out, int* status_out) {
+    ChainBuf& b = ctx->cb;
+    const int B = (int)batch;
+    const int n = ctx->n, np = ctx->np, m = ctx->m;
+    // pad x, v into the chain layout
+    int thr = 256, blocks = (int)std::min<long long>(((long long)B * np + thr - 1) / thr, 65535);
+    pad_rows_kernel<<<blocks, thr, 0, ctx->stream>>>(dx, n, B, n, b.X, np);
+    pad_rows_kernel<<<blocks, thr, 0, ctx->stream>>>(dv, n, B, n, b.V, np);
+    ctx->launches += 2;
+    std::vector<int> bound_h(B, du ? 0 : SW_BIND_NONE_DEV);
+    CK(cudaMemcpyAsync(b.bound, bound_h.data(), sizeof(int) * B, cudaMemcpyHostToDevice, ctx->stream));
+    if (du) CK(cudaMemcpyAsync(b.U, du, sizeof(double) * (size_t)B * m, cudaMemcpyDeviceToDevice, ctx->stream));
+    // A(x) = a0 + X Ahat ; A(v) = V Ahat  (K0, K1)
+    launch_gemm_av(ctx, b.X, nullptr, nullptr, B, b.AX, ctx->a0);
+    launch_gemm_av(ctx, b.V, nullptr, nullptr, B, b.AV, nullptr);
+    // K2 in oracle mode
+    double *o_tm, *o_tp, *o_nrm, *o_ker = nullptr;
+    int *o_bind, *o_stat;
+    CK(cudaMalloc(&o_tm, sizeof(double) * B));
+    CK(cudaMalloc(&o_tp, sizeof(double) * B));
+    CK(cudaMalloc(&o_nrm, sizeof(double) * (size_t)B * n));
+    if (kernel) CK(cudaMalloc(&o_ker, sizeof(double) * (size_t)B * m));
+    CK(cudaMalloc(&o_bind, sizeof(int) * B));
+    CK(cudaMalloc(&o_stat, sizeof(int) * B));
+    ChordParams P = chord_params(ctx, 1);
+    P.count_host = B;
+    P.o_tminus = o_tm; P.o_tplus = o_tp; P.o_kernel = o_ker; P.o_binding = o_bind; P.o_status = o_stat;
+    launch_chord(ctx, P, B);
+    // K3 normal contraction for every line (non-dense rows are ignored by K4)
+    launch_gemm_normal(ctx, nullptr, nullptr, B);
+    NormalParams Q = normal_params(ctx, 1);
+    Q.count_host = B;
+    Q.o_binding = o_bind; Q.o_tplus = o_tp; Q.Vin = b.V; Q.o_normal = o_nrm;
+    normal_reflect_kernel<<<(B + 7) / 8, 256, 0, ctx->stream>>>(Q);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    cudaMemcpyKind kind = host_out ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    CK(cudaMemcpyAsync(t_minus, o_tm, sizeof(double) * B, kind, ctx->stream));
+    CK(cudaMemcpyAsync(t_plus, o_tp, sizeof(double) * B, kind, ctx->stream));
+    CK(cudaMemcpyAsync(normal, o_nrm, sizeof(double) * (size_t)B * n, kind, ctx->stream));
+    if (kernel) CK(cudaMemcpyAsync(kernel, o_ker, sizeof(double) * (size_t)B * m, kind, ctx->stream));
+    CK(cudaMemcpyAsync(binding, o_bind, sizeof(int) * B, kind, ctx->stream));
+    std::vector<int> st(B);
+    CK(cudaMemcpyAsync(st.data(), o_stat, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(o_tm); cudaFree(o_tp); cudaFree(o_nrm); cudaFree(o_bind); cudaFree(o_stat);
+    if (o_ker) cudaFree(o_ker);
+    int worst = 0;
+    for (int i = 0; i < B; ++i) worst = std::max(worst, st[i] == 2 ? 2 : 0);
+    if (status_out) *status_out = worst;
+    return SPEC_OK;
+}
+
+static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
+                        double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
+                        bool host) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    if (batch < 0 || batch > (1LL << 30)) return fail(SPEC_EINVAL, "bad batch");
+    if (batch == 0) return SPEC_OK;
+    if (!x || !v || !t_minus || !t_plus || !normal || !binding) return fail(SPEC_EINVAL, "null buffer");
+    CK(cudaSetDevice(ctx->dev));
+    int rc = ensure_chains(ctx, batch);
+    if (rc) return rc;
+    const int n = ctx->n, m = ctx->m;
+    const double *dx = x, *dv = v, *du = u;
+    double *bx = nullptr, *bv = nullptr, *bu = nullptr;
+    if (host) {
+        CK(cudaMalloc(&bx, sizeof(double) * batch * n));
+        CK(cudaMalloc(&bv, sizeof(double) * batch * n));
+        CK(cudaMemcpyAsync(bx, x, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(bv, v, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (u) {
+            CK(cudaMalloc(&bu, sizeof(double) * batch * m));
+            CK(cudaMemcpyAsync(bu, u, sizeof(double) * batch * m, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        dx = bx; dv = bv; du = bu;
+    }
+    int status = 0;
+    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status);
+    if (bx) cudaFree(bx);
+    if (bv) cudaFree(bv);
+    if (bu) cudaFree(bu);
+    if (rc) return rc;
+    if (status == 2) return fail(SPEC_EPRECOND, "some x is not interior (Cholesky of F(x) failed)");
+    return SPEC_OK;
+}
+
+extern "C" int boundary_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
+                               double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding) {
+    return oracle_entry(ctx, batch, x, v, u, t_minus, t_plus, normal, kernel, binding, true);
+}
+extern "C" int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const double* v,
+                                   const double* u, double* t_minus, double* t_plus, double* normal,
+                                   double* kernel, int32_t* binding) {
+    return oracle_entry(ctx, batch, x, v, u, t_minus, t_plus, normal, kernel, binding, false);
+}
+
+// ---------------------------------------------------------------- walks
+struct TraceBufs {
+    int max_trace = 0;
+    int* cnt = nullptr;
+    double *hit = nullptr, *t = nullptr, *w = nullptr, *v = nullptr;
+    int* bind = nullptr;
+};
+
+// Walk state kept in the context between walk_begin / walk_rounds / walk_end.
+struct WalkRun {
+    bool active = false;
+    spec_walk_params p;
+    ChordParams P;
+    NormalParams Q;
+    int count = 0;  // upper bound of active chains (exact after each compaction)
+    int cur = 0;
+    long long rounds = 0;
+    double ms = 0.0;
+    bool timing = false;        // per-kernel CUDA-event timing
+    double kms[4] = {0, 0, 0, 0};  // K1, K2, K3, K4
+    long long kcount[4] = {0, 0, 0, 0};
+    long long k2_items = 0;        // chain-calls processed by K2 launches (upper bound incl. done)
+};
+static WalkRun& walk_run(spec_ctx* ctx);
+
+// Set up a walk: reset per-chain state, x_0, A(x_0) (K0) and the step-0 draws.
+static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx0, int x0_per_chain,
+                      const long long* dgid, TraceBufs* tr) {
+    ChainBuf& b = ctx->cb;
+    WalkRun& W = walk_run(ctx);
+    const int C = (int)p->chains;
+    const int n = ctx->n, np = ctx->np;
+    CK(cudaMemsetAsync(b.steps_done, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.refl, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.flags, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.nrej, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.ndeg, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.calls, 0, sizeof(long long) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.nrefl, 0, sizeof(long long) * C, ctx->stream));
+    {
+        std::vector<int> bnd(C, SW_BIND_NONE_DEV);
+        CK(cudaMemcpyAsync(b.bound, bnd.data(), sizeof(int) * C, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    int thr = 256;
+    int blocks = (int)std::min<long long>(((long long)C * np + thr - 1) / thr, 65535);
+    if (dx0) {
+        pad_rows_kernel<<<blocks, thr, 0, ctx->stream>>>(dx0, x0_per_chain ? n : 0, C, n, b.X, np);
+        ctx->launches++;
+    } else {
+        CK(cudaMemsetAsync(b.X, 0, sizeof(double) * (size_t)C * np, ctx->stream));
+    }
+    iota_kernel<<<(C + 255) / 256, 256, 0, ctx->stream>>>(b.list, C);
+    ctx->launches++;
+    launch_gemm_av(ctx, b.X, nullptr, nullptr, C, b.AX, ctx->a0);  // K0: A(x_0)
+    walk_start_kernel<<<(C + 7) / 8, 256, 0, ctx->stream>>>(C, n, np, ctx->mt, ctx->mtp, b.V, b.X, b.Xs, b.AX,
+                                                            b.AXs, b.ell, p->L, p->seed, p->tag, p->kind,
+                                                            p->chain_begin, dgid);
+    ctx->launches++;
+    W.p = *p;
+    W.count = C;
+    W.cur = 0;
+    W.rounds = 0;
+    W.ms = 0.0;
+    for (int i = 0; i < 4; ++i) W.kms[i] = 0.0, W.kcount[i] = 0;
+    W.k2_items = 0;
+    CK(cudaMemcpyAsync(b.counters, &W.count, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    ChordParams& P = W.P;
+    P = chord_params(ctx, 0);
+    P.steps_total = (int)p->steps;
+    P.Lpar = p->L;
+    P.rho = p->rho;
+    P.seed = p->seed;
+    P.tag = p->tag;
+    P.chain_base = p->chain_begin;
+    P.gid = dgid;
+    NormalParams& Q = W.Q;
+    Q = normal_params(ctx, 0);
+    Q.steps_total = (int)p->steps;
+    Q.Lpar = p->L;
+    Q.seed = p->seed;
+    Q.tag = p->tag;
+    Q.chain_base = p->chain_begin;
+    Q.gid = dgid;
+    if (tr) {
+        P.max_trace = tr->max_trace; P.tr_cnt = tr->cnt; P.tr_hit = tr->hit; P.tr_t = tr->t; P.tr_w = tr->w;
+        P.tr_v = tr->v; P.tr_bind = tr->bind;
+        Q.max_trace = tr->max_trace; Q.tr_cnt = tr->cnt; Q.tr_w = tr->w; Q.tr_v = tr->v;
+    }
+    W.active = true;
+    return SPEC_OK;
+}
+
+// Run up to max_rounds scheduler rounds (max_rounds <= 0: until every chain is
+// done).  Every round each active chain makes exactly one boundary-oracle call
+// (K1 -> K2 -> K3 -> K4); finished chains are compacted out every 8 rounds.
+static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
+    ChainBuf& b = ctx->cb;
+    WalkRun& W = walk_run(ctx);
+    ChordParams& P = W.P;
+    NormalParams& Q = W.Q;
+    int* lists[2] = {b.list, b.list2};
+    const int check = 8;
+    long long done_rounds = 0;
+    // per-kernel event pool: 5 events per round, read back at each compaction sync
+    const int pool = 5 * check;
+    std::vector<cudaEvent_t> ev;
+    if (W.timing) {
+        ev.resize(pool);
+        for (int i = 0; i < pool; ++i) CK(cudaEventCreate(&ev[i]));
+    }
+    CK(cudaEventRecord(ctx->e0, ctx->stream));
+    while (W.count > 0 && (max_rounds <= 0 || done_rounds < max_rounds)) {
+        int kr = 0;
+        for (int k = 0; k < check && W.count > 0 && (max_rounds <= 0 || done_rounds < max_rounds); ++k) {
+            int* list = lists[W.cur];
+            const int count = W.count;
+            cudaEvent_t* e = W.timing ? &ev[5 * k] : nullptr;
+            CK(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));
+            if (e) CK(cudaEventRecord(e[0], ctx->stream));
+            launch_gemm_av(ctx, b.V, list, b.counters, count, b.AV, nullptr);  // K1
+            if (e) CK(cudaEventRecord(e[1], ctx->stream));
+            P.list = list;
+            P.count_dev = b.counters;
+            P.count_host = count;
+            launch_chord(ctx, P, count);  // K2
+            if (e) CK(cudaEventRecord(e[2], ctx->stream));
+            launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
+            if (e) CK(cudaEventRecord(e[3], ctx->stream));
+            Q.nlist = b.nlist;
+            Q.ncount = b.counters + 2;
+            Q.count_host = count;
+            int nb = (count + 7) / 8;
+            if (nb > 65535 * 4) nb = 65535 * 4;
+            normal_reflect_kernel<<<nb, 256, 0, ctx->stream>>>(Q);  // K4
+            ctx->launches++;
+            if (e) CK(cudaEventRecord(e[4], ctx->stream));
+            W.k2_items += count;
+            ++W.rounds;
+            ++done_rounds;
+            ++kr;
+        }
+        CK(cudaMemsetAsync(b.counters + 1, 0, sizeof(int), ctx->stream));
+        compact_kernel<<<std::min((W.count + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+            lists[W.cur], b.counters, W.count, b.flags, lists[W.cur ^ 1], b.counters + 1);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(b.counters, b.counters + 1, sizeof(int), cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(&W.count, b.counters + 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaGetLastError());
+        if (W.timing) {
+            for (int k = 0; k < kr; ++k)
+                for (int i = 0; i < 4; ++i) {
+                    float t = 0.f;
+                    CK(cudaEventElapsedTime(&t, ev[5 * k + i], ev[5 * k + i + 1]));
+                    W.kms[i] += t;
+                    W.kcount[i] += 1;
+                }
+        }
+        W.cur ^= 1;
+    }
+    CK(cudaEventRecord(ctx->e1, ctx->stream));
+    CK(cudaEventSynchronize(ctx->e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->e0, ctx->e1));
+    W.ms += ms;
+    for (cudaEvent_t x : ev) cudaEventDestroy(x);
+    return SPEC_OK;
+}
+
+static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
+    ChainBuf& b = ctx->cb;
+    WalkRun& W = walk_run(ctx);
+    const int C = (int)W.p.chains;
+    CK(cudaMemsetAsync(ctx->dstats, 0, sizeof(long long) * 8, ctx->stream));
+    stats_kernel<<<std::min((C + 255) / 256, 1024), 256, 0, ctx->stream>>>(C, b.calls, b.nrefl, b.nrej, b.ndeg,
+                                                                           b.flags, b.steps_done, ctx->dstats);
+    ctx->launches++;
+    long long hs[8];
+    CK(cudaMemcpyAsync(hs, ctx->dstats, sizeof(long long) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (st) {
+        st->calls = hs[0];
+        st->reflections = hs[1];
+        st->rejects = hs[2];
+        st->degenerates = hs[3];
+        st->failures = hs[4];
+        st->steps = hs[5];
+        st->rounds = W.rounds;
+        st->device_ms = W.ms;
+    }
+    if (ctx->prof) {
+        unsigned long long ph[16];
+        CK(cudaMemcpy(ph, ctx->prof, sizeof(ph), cudaMemcpyDeviceToHost));
+        CK(cudaMemset(ctx->prof, 0, sizeof(ph)));
+        const char* names[] = {"unpack", "deflate", "cholesky", "congruence", "eigen", "extreme", "eigvec",
+                               "backtransform+y", "select+advance"};
+        double tot = 0;
+        for (int i = 0; i < 9; ++i) tot += (double)ph[i];
+        fprintf(stderr, "[specwalk prof] m=%d calls=%lld cycles/call:", ctx->m, (long long)hs[0]);
+        for (int i = 0; i < 9; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)ph[i] / (double)hs[0]);
+        fprintf(stderr, " total=%.0f\n", tot / (double)hs[0]);
+    }
+    return SPEC_OK;
+}
+
+static int run_walk(spec_ctx* ctx, const spec_walk_params* p, const double* dx0, int x0_per_chain,
+                    const long long* dgid, TraceBufs* tr, spec_walk_stats* st) {
+    int rc = walk_setup(ctx, p, dx0, x0_per_chain, dgid, tr);
+    if (rc) return rc;
+    rc = walk_do_rounds(ctx, 0);
+    if (rc) return rc;
+    rc = walk_collect_stats(ctx, st);
+    walk_run(ctx).active = false;
+    return rc;
+}
+
+static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
+    if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
+    if (p->kind != SPEC_WALK_BILLIARD) return fail(SPEC_EINVAL, "walk kind not supported by this build");
+    if (p->chains < 1 || p->chains > (1LL << 30)) return fail(SPEC_EINVAL, "chains out of range");
+    if (p->steps < 0 || p->steps > (1LL << 31) - 1) return fail(SPEC_EINVAL, "steps out of range");
+    if (!(p->L > 0.0) || !std::isfinite(p->L)) return fail(SPEC_EINVAL, "L must be > 0");
+    if (p->rho < 0) return fail(SPEC_EINVAL, "rho must be >= 0");
+    return SPEC_OK;
+}
+
+static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain,
+                      double* sum_x, double* sum_xx, double* final_x, spec_walk_stats* st, bool host) {
+    int rc = check_walk_params(ctx, p);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->dev));
+    rc = ensure_chains(ctx, p->chains);
+    if (rc) return rc;
+    const int C = (int)p->chains, n = ctx->n, np = ctx->np;
+    double* dx0 = nullptr;
+    const double* x0d = x0;
+    if (x0 && host) {
+        size_t cnt = (size_t)(x0_per_chain ? C : 1) * n;
+        CK(cudaMalloc(&dx0, sizeof(double) * cnt));
+        CK(cudaMemcpyAsync(dx0, x0, sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+        x0d = dx0;
+    }
+    spec_walk_stats local;
+    rc = run_walk(ctx, p, x0d, x0_per_chain, nullptr, nullptr, &local);
+    if (dx0) cudaFree(dx0);
+    if (rc) return rc;
+    if (st) *st = local;
+    // outputs
+    ChainBuf& b = ctx->cb;
+    double *dsx = nullptr, *dsxx = nullptr;
+    const int nxx = n * (n + 1) / 2;
+    if (sum_x || sum_xx) {
+        CK(cudaMalloc(&dsx, sizeof(double) * n));
+        CK(cudaMalloc(&dsxx, sizeof(double) * nxx));
+        moments_kernel<<<std::min((n + nxx + 127) / 128, 4096), 128, 0, ctx->stream>>>(b.X, np, n, C, dsx, dsxx);
+        ctx->launches++;
+        cudaMemcpyKind k = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (sum_x) CK(cudaMemcpyAsync(sum_x, dsx, sizeof(double) * n, k, ctx->stream));
+        if (sum_xx) CK(cudaMemcpyAsync(sum_xx, dsxx, sizeof(double) * nxx, k, ctx->stream));
+    }
+    if (final_x) {
+        if (host) {
+            double* tmp;
+            CK(cudaMalloc(&tmp, sizeof(double) * (size_t)C * n));
+            unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(b.X, np, C, n, tmp);
+            CK(cudaMemcpyAsync(final_x, tmp, sizeof(double) * (size_t)C * n, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            cudaFree(tmp);
+        } else {
+            unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(b.X, np, C, n, final_x);
+        }
+        ctx->launches++;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (dsx) cudaFree(dsx);
+    if (dsxx) cudaFree(dsxx);
+    if (local.failures > 0)
+        return fail(SPEC_EPRECOND, std::to_string(local.failures) + " chain(s) started outside int S");
+    return SPEC_OK;
+}
+
+extern "C" int walk_sample(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain,
+                           double* sum_x, double* sum_xx, double* final_x, spec_walk_stats* st) {
+    return walk_entry(ctx, p, x0, x0_per_chain, sum_x, sum_xx, final_x, st, true);
+}
+extern "C" int walk_sample_dev(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain,
+                               double* sum_x, double* sum_xx, double* final_x, spec_walk_stats* st) {
+    return walk_entry(ctx, p, x0, x0_per_chain, sum_x, sum_xx, final_x, st, false);
+}
+
+extern "C" int walk_trace(spec_ctx* ctx, const spec_walk_params* p, const int64_t* chain_ids, int64_t nchains,
+                          int64_t max_refl, double* hit_x, double* t, double* w, double* v_after, int32_t* binding,
+                          int64_t* nrec) {
+    if (!chain_ids || nchains < 1 || max_refl < 1) return fail(SPEC_EINVAL, "bad trace arguments");
+    spec_walk_params q = *p;
+    q.chains = nchains;
+    int rc = check_walk_params(ctx, &q);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->dev));
+    rc = ensure_chains(ctx, nchains);
+    if (rc) return rc;
+    const int C = (int)nchains, n = ctx->n;
+    const int R = (int)max_refl;
+    CK(cudaMemcpyAsync(ctx->cb.gid, chain_ids, sizeof(long long) * C, cudaMemcpyHostToDevice, ctx->stream));
+    TraceBufs tb;
+    tb.max_trace = R;
+    CK(zalloc(&tb.cnt, C));
+    CK(zalloc(&tb.hit, (size_t)C * R * n));
+    CK(zalloc(&tb.t, (size_t)C * R));
+    CK(zalloc(&tb.w, (size_t)C * R * n));
+    CK(zalloc(&tb.v, (size_t)C * R * n));
+    CK(zalloc(&tb.bind, (size_t)C * R));
+    spec_walk_stats local;
+    rc = run_walk(ctx, &q, nullptr, 0, ctx->cb.gid, &tb, &local);
+    if (!rc) {
+        std::vector<int> cnt(C);
+        CK(cudaMemcpy(cnt.data(), tb.cnt, sizeof(int) * C, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < C; ++i) nrec[i] = cnt[i];
+        CK(cudaMemcpy(hit_x, tb.hit, sizeof(double) * (size_t)C * R * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(t, tb.t, sizeof(double) * (size_t)C * R, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(w, tb.w, sizeof(double) * (size_t)C * R * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(v_after, tb.v, sizeof(double) * (size_t)C * R * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(binding, tb.bind, sizeof(int) * (size_t)C * R, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(tb.cnt); cudaFree(tb.hit); cudaFree(tb.t); cudaFree(tb.w); cudaFree(tb.v); cudaFree(tb.bind);
+    return rc;
+}
+
+static WalkRun& walk_run(spec_ctx* ctx) {
+    if (!ctx->walk) ctx->walk = new WalkRun();
+    return *(WalkRun*)ctx->walk;
+}
+static void free_walk(spec_ctx* ctx) {
+    delete (WalkRun*)ctx->walk;
+    ctx->walk = nullptr;
+}
+
+// ---------------------------------------------------------------- resumable walk API
+extern "C" int walk_begin(spec_ctx* ctx, const spec_walk_params* p, const double* x0_dev, int x0_per_chain) {
+    int rc = check_walk_params(ctx, p);
+    if (rc) return rc;
+    CK(cudaSetDevice(ctx->dev));
+    rc = ensure_chains(ctx, p->chains);
+    if (rc) return rc;
+    return walk_setup(ctx, p, x0_dev, x0_per_chain, nullptr, nullptr);
+}
+
+extern "C" int walk_rounds(spec_ctx* ctx, int64_t max_rounds, int64_t* active) {
+    if (!ctx || !walk_run(ctx).active) return fail(SPEC_EINVAL, "no walk in progress (call walk_begin)");
+    CK(cudaSetDevice(ctx->dev));
+    int rc = walk_do_rounds(ctx, max_rounds <= 0 ? 0 : max_rounds);
+    if (active) *active = walk_run(ctx).count;
+    return rc;
+}
+
+extern "C" int walk_end(spec_ctx* ctx, double* sum_x_dev, double* sum_xx_dev, double* final_x_dev,
+                        spec_walk_stats* st) {
+    if (!ctx || !walk_run(ctx).active) return fail(SPEC_EINVAL, "no walk in progress (call walk_begin)");
+    CK(cudaSetDevice(ctx->dev));
+    WalkRun& W = walk_run(ctx);
+    int rc = walk_collect_stats(ctx, st);
+    if (rc) return rc;
+    const int C = (int)W.p.chains, n = ctx->n, np = ctx->np;
+    if (sum_x_dev || sum_xx_dev) {
+        double *dsx = sum_x_dev, *dsxx = sum_xx_dev, *tx = nullptr, *txx = nullptr;
+        const int nxx = n * (n + 1) / 2;
+        if (!dsx) { CK(cudaMalloc(&tx, sizeof(double) * n)); dsx = tx; }
+        if (!dsxx) { CK(cudaMalloc(&txx, sizeof(double) * nxx)); dsxx = txx; }
+        moments_kernel<<<std::min((n + nxx + 127) / 128, 4096), 128, 0, ctx->stream>>>(ctx->cb.X, np, n, C, dsx,
+                                                                                         dsxx);
+        ctx->launches++;
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (tx) cudaFree(tx);
+        if (txx) cudaFree(txx);
+    }
+    if (final_x_dev) {
+        unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(ctx->cb.X, np, C, n, final_x_dev);
+        ctx->launches++;
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    W.active = false;
+    return SPEC_OK;
+}
+
+extern "C" int spec_kernel_timing(spec_ctx* ctx, int enable) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    WalkRun& W = walk_run(ctx);
+    W.timing = enable != 0;
+    for (int i = 0; i < 4; ++i) W.kms[i] = 0.0, W.kcount[i] = 0;
+    W.k2_items = 0;
+    return SPEC_OK;
+}
+
+extern "C" int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    WalkRun& W = walk_run(ctx);
+    for (int i = 0; i < 4; ++i) {
+        if (ms4) ms4[i] = W.kms[i];
+        if (launches4) launches4[i] = W.kcount[i];
+    }
+    if (k2_items) *k2_items = W.k2_items;
+    return SPEC_OK;
+}
+
+extern "C" int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st) {
+    if (!ctx || !walk_run(ctx).active) return fail(SPEC_EINVAL, "no walk in progress");
+    return walk_collect_stats(ctx, st);
+}
