@@ -78,6 +78,8 @@ struct ChordParams {
     double* scratch;
     long long scratch_stride;
     unsigned long long* prof;  // optional per-phase cycle counters (SPECWALK_PROF=1)
+    double* lsave;             // per-CTA global slice where L is parked during Lanczos
+    long long lsave_stride;
 };
 
 // ---------------------------------------------------------------- team helpers
@@ -141,9 +143,9 @@ __device__ void householder_congruence(const Team& T, double* X, int m, int ld, 
     double K = 0.5 * beta * block_sum(T, hp, red);
     for (int i = T.tid; i < m; i += T.nthr) p[i] = p[i] - K * h[i];  // q
     __syncthreads();
-    for (int e = T.tid; e < m * m; e += T.nthr) {
-        int i = e / m, j = e - i * m;
-        X[i * ld + j] -= h[i] * p[j] + p[i] * h[j];
+    for (int i = T.warp; i < m; i += T.nwarps) {
+        const double hi = h[i], pi = p[i];
+        for (int j = T.lane; j < m; j += 32) X[i * ld + j] -= hi * p[j] + pi * h[j];
     }
     __syncthreads();
 }
@@ -644,201 +646,7 @@ __global__ void __launch_bounds__(256) chord_kernel(ChordParams P) {
         }
 
         PROF_MARK(7);
-        // ---- 3. closed-form constraints + selection (warp 0)
-        if (T.warp == 0) {
-            double tpl = (theta_max > 0.0) ? 1.0 / theta_max : SW_INF;
-            double tmi = defl ? 0.0 : ((theta_min < 0.0) ? 1.0 / theta_min : -SW_INF);
-            if (outward) { tpl = 0.0; tmi = 0.0; }
-            int bind = (tpl < SW_INF) ? 0 : SW_BIND_NONE_DEV;
-            if (P.lo) {
-                double bt = SW_INF;
-                int bi = 0x7fffffff;
-                double tm = -SW_INF;
-                for (int i = T.lane; i < n; i += 32) {
-                    double vi = v[i], xi = x[i];
-                    double t = SW_INF, tn = -SW_INF;
-                    if (vi > 0.0) { t = (P.hi[i] - xi) / vi; tn = (P.lo[i] - xi) / vi; }
-                    else if (vi < 0.0) { t = (P.lo[i] - xi) / vi; tn = (P.hi[i] - xi) / vi; }
-                    if (t < bt) { bt = t; bi = i; }
-                    tm = fmax(tm, tn);
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    double ot = __shfl_xor_sync(0xffffffffu, bt, o);
-                    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (ot < bt || (ot == bt && oi < bi)) { bt = ot; bi = oi; }
-                }
-                tm = warp_max(tm);
-                if (bt < tpl) {
-                    tpl = bt;
-                    bind = (v[bi] > 0.0) ? 1 + 2 * bi : 2 + 2 * bi;
-                }
-                tmi = fmax(tmi, tm);
-            }
-            if (P.has_ball) {
-                double dv = 0.0, dd2 = 0.0, vv = 0.0;
-                for (int i = T.lane; i < n; i += 32) {
-                    double di = x[i] - P.ball_c[i];
-                    dv += di * v[i];
-                    dd2 += di * di;
-                    vv += v[i] * v[i];
-                }
-                dv = warp_sum(dv); dd2 = warp_sum(dd2); vv = warp_sum(vv);
-                double disc = dv * dv - vv * (dd2 - P.ball_r * P.ball_r);
-                double sq = sqrt(fmax(disc, 0.0));
-                double tb = (-dv + sq) / vv;
-                double tbm = (-dv - sq) / vv;
-                if (bnd == SW_BIND_BALL_DEV && tb <= 0.0) tb = SW_INF;
-                if (tb < tpl) { tpl = tb; bind = SW_BIND_BALL_DEV; }
-                tmi = fmax(tmi, fmin(tbm, 0.0));
-            }
-            if (T.lane == 0) {
-                sh_d[0] = tpl;
-                sh_d[1] = tmi;
-                sh_i[1] = bind;
-            }
-        }
-        __syncthreads();
-        const double tplus = sh_d[0];
-        const int bind = sh_i[1];
-
-        if (P.mode == 1) {
-            // ---- boundary_oracle batch outputs
-            if (T.tid == 0) {
-                P.o_tplus[slot] = tplus;
-                P.o_tminus[slot] = sh_d[1];
-                P.o_binding[slot] = bind;
-                P.o_status[slot] = failed ? 2 : (degenerate && bind == 0 ? 1 : 0);
-                P.flags[slot] = (bind == 0 && !failed) ? CF_NEED_NORMAL : 0;
-            }
-            if (P.o_kernel) {
-                for (int i = T.tid; i < m; i += T.nthr)
-                    P.o_kernel[(size_t)slot * m + i] = (bind == 0 && !failed) ? yy[i] : 0.0;
-            }
-            if (bind == 0 && !failed) {
-                double* yh = P.Yh + (size_t)slot * P.mtp;
-                for (int i = T.warp; i < m; i += T.nwarps)
-                    for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
-            }
-            continue;
-        }
-
-        // ---- 4. billiard advance (Alg. 5)
-        if (failed) {
-            if (T.tid == 0) {
-                P.flags[slot] |= CF_DONE | CF_FAILED;
-                P.calls[slot] += 1;
-            }
-            continue;
-        }
-        double el = P.ell[slot];
-        bool accept = (el <= tplus);  // reading R4: tie -> no reflection
-        double th = accept ? el : tplus;
-        for (int i = T.tid; i < n; i += T.nthr) x[i] += th * v[i];
-        for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] += th * av[i];
-        __syncthreads();
-        bool end_step = accept;
-        bool reject = false;
-        if (!accept) {
-            int rf = P.refl[slot] + 1;
-            if (T.tid == 0) {
-                P.refl[slot] = rf;
-                P.ell[slot] = el - th;
-                P.nrefl[slot] += 1;
-            }
-            if (rf > P.rho) {
-                reject = true;
-                end_step = true;
-                if (T.tid == 0) P.nrej[slot] += 1;
-            } else if (bind == 0) {
-                if (degenerate || outward) {
-                    reject = true;
-                    end_step = true;
-                    if (T.tid == 0) P.ndeg[slot] += 1;
-                } else {
-                    double* yh = P.Yh + (size_t)slot * P.mtp;
-                    for (int i = T.warp; i < m; i += T.nwarps)
-                        for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
-                    for (int i = T.tid; i < m; i += T.nthr) P.U[(size_t)slot * m + i] = yy[i];
-                    if (T.tid == 0) {
-                        P.bound[slot] = 0;
-                        P.flags[slot] |= CF_NEED_NORMAL;
-                        int q = atomicAdd(P.ncount, 1);
-                        P.nlist[q] = slot;
-                    }
-                }
-            } else if (bind == SW_BIND_BALL_DEV) {
-                // w = (x - c)/r ; v <- v - 2 <v,w> w
-                if (T.warp == 0) {
-                    double s = 0.0, q = 0.0;
-                    for (int i = T.lane; i < n; i += 32) {
-                        double di = x[i] - P.ball_c[i];
-                        s += di * v[i];
-                        q += di * di;
-                    }
-                    s = warp_sum(s);
-                    q = warp_sum(q);
-                    double f = 2.0 * s / q;
-                    for (int i = T.lane; i < n; i += 32) v[i] -= f * (x[i] - P.ball_c[i]);
-                    if (T.lane == 0) P.bound[slot] = SW_BIND_BALL_DEV;
-                }
-            } else if (bind > 0) {
-                if (T.tid == 0) {
-                    int i = (bind - 1) >> 1;
-                    v[i] = -v[i];  // w = +-e_i
-                    P.bound[slot] = bind;
-                }
-            }
-            // trace record (cube / ball complete here; dense completed by K4)
-            if (P.max_trace > 0 && !reject) {
-                __syncthreads();
-                int k = P.tr_cnt[slot];
-                if (k < P.max_trace) {
-                    size_t o = ((size_t)slot * P.max_trace + k);
-                    for (int i = T.tid; i < n; i += T.nthr) {
-                        P.tr_hit[o * n + i] = x[i];
-                        if (bind != 0) {
-                            P.tr_v[o * n + i] = v[i];
-                            double wi = 0.0;
-                            if (bind > 0) wi = (i == ((bind - 1) >> 1)) ? ((bind & 1) ? 1.0 : -1.0) : 0.0;
-                            else {
-                                wi = (x[i] - P.ball_c[i]) / P.ball_r;
-                            }
-                            P.tr_w[o * n + i] = wi;
-                        }
-                    }
-                    if (T.tid == 0) {
-                        P.tr_t[o] = th;
-                        P.tr_bind[o] = bind;
-                        P.tr_cnt[slot] = k + 1;
-                        if (k + 1 >= P.max_trace && bind != 0) P.flags[slot] |= CF_DONE;
-                    }
-                }
-            }
-        }
-        if (T.tid == 0) P.calls[slot] += 1;
-        __syncthreads();
-        PROF_MARK(8);
-        if (end_step) {
-            if (reject) {
-                const double* xs = P.Xs + (size_t)slot * P.np;
-                const double* axs = P.AXs + (size_t)slot * P.mtp;
-                for (int i = T.tid; i < n; i += T.nthr) x[i] = xs[i];
-                for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] = axs[i];
-            }
-            __syncthreads();
-            int sd = P.steps_done[slot] + 1;
-            if (T.tid == 0) {
-                P.steps_done[slot] = sd;
-                P.refl[slot] = 0;
-                P.bound[slot] = SW_BIND_NONE_DEV;
-            }
-            if (sd >= P.steps_total) {
-                if (T.tid == 0) P.flags[slot] |= CF_DONE;
-            } else {
-                step_start<true>(T, slot, gidv, sd, n, P.np, P.mt, P.mtp, P.V, P.X, P.Xs, P.AX, P.AXs, P.ell, P.Lpar,
-                                 P.seed, P.tag, 0, red);
-            }
-        }
+#include "chord_tail.inc"
     }
 }
 

@@ -1,0 +1,793 @@
+// chord2.cuh -- K2 v2: the per-chain boundary oracle, blocked and tensor-core based.
+//
+// Same mathematics as PAPER.md Alg. 2 / Lemma 3 and the
+// Cholesky-transformed pencil of P:1207-1215, reorganised for sm_100a:
+//   L L^T = A(x)              blocked right-looking Cholesky, nb = 8; the trailing
+//                             SYRK updates are DMMA m8n8k4 tiles
+//   M = -L^{-1} A(v) L^{-T}   two blocked TRSMs (natural and transposed view),
+//                             updates on DMMA tiles
+//   theta_max = lambda_max(M) Lanczos with full (CGS2) reorthogonalisation, M
+//                             register-resident across the CTA; convergence
+//                             checked on T_J by Sturm multisection plus the
+//                             residual beta_J |s_J| of the top Ritz pair
+//   y = L^{-T} Q s            the PEP eigenvector; t+ = 1/theta_max
+// Boundary starts (after a reflection) are Schur-deflated by the known kernel
+// vector (R6) and shifted to an aligned (m-1) problem.
+#pragma once
+#include "chord.cuh"
+
+namespace sw {
+
+constexpr int NVEC2 = 20;
+
+__device__ __forceinline__ void dmma_t(double (&d)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+// acc(8x8) -= A(8 x K) * B(K x 8).  A row-major (lda).  B element (k, c) at
+// Bp[k*ldb + c] (BNK = false) or Bp[c*ldb + k] (BNK = true).
+template <bool BNK>
+__device__ __forceinline__ void tile_msub(double (&acc)[2], const double* A, int lda, const double* Bp, int ldb,
+                                          int K, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+#pragma unroll 2
+    for (int k0 = 0; k0 < K; k0 += 4) {
+        double a = -A[r * lda + k0 + q];
+        double b = BNK ? Bp[r * ldb + k0 + q] : Bp[(k0 + q) * ldb + r];
+        dmma_t(acc, a, b);
+    }
+}
+
+// blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8)
+__device__ bool cholesky_blocked(const Team& T, double* G, int n, int ld, double* rdiag, int* flag) {
+    const int TB = n >> 3;
+    for (int kb = 0; kb < TB; ++kb) {
+        const int k0 = kb * 8;
+        double* D = G + k0 * ld + k0;
+        if (T.warp == 0) {
+            bool ok = true;
+            for (int c = 0; c < 8; ++c) {
+                double d = D[c * ld + c];
+                if (!(d > 0.0)) { ok = false; break; }
+                double l = sqrt(d);
+                double il = 1.0 / l;
+                __syncwarp();
+                if (T.lane > c && T.lane < 8) D[T.lane * ld + c] *= il;
+                if (T.lane == 0) {
+                    D[c * ld + c] = l;
+                    rdiag[k0 + c] = il;
+                }
+                __syncwarp();
+                for (int p = T.lane; p < 64; p += 32) {
+                    int i = p >> 3, j = p & 7;
+                    if (j > c && j <= i) D[i * ld + j] -= D[i * ld + c] * D[j * ld + c];
+                }
+                __syncwarp();
+            }
+            if (T.lane == 0) *flag = ok ? 0 : 1;
+        }
+        __syncthreads();
+        if (*flag) return false;
+        // panel TRSM: rows below the diagonal block, P = G_ib,kb L_kk^{-T}
+        for (int i = k0 + 8 + T.tid; i < n; i += T.nthr) {
+            double x[8];
+            double* row = G + i * ld + k0;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = row[c];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                double s = x[c];
+#pragma unroll
+                for (int cp = 0; cp < c; ++cp) s -= x[cp] * D[c * ld + cp];
+                x[c] = s * rdiag[k0 + c];
+            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c) row[c] = x[c];
+        }
+        __syncthreads();
+        // trailing SYRK on DMMA tiles: G_ij -= P_i P_j^T, kb < j <= i
+        const int Tr = TB - kb - 1;
+        const int ntile = Tr * (Tr + 1) / 2;
+        for (int t = T.warp; t < ntile; t += T.nwarps) {
+            int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+            while (ii * (ii + 1) / 2 > t) --ii;
+            int jj = t - ii * (ii + 1) / 2;
+            int ib = kb + 1 + ii, jb = kb + 1 + jj;
+            double* C = G + ib * 8 * ld + jb * 8;
+            const int r = T.lane >> 2, q = T.lane & 3;
+            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
+// B <- L^{-1} B on all n columns.  TR = true works on the transposed view
+// W(r, c) = B[c*ld + r].  Blocked right-looking, DMMA tile updates.
+template <bool TR>
+__device__ void trsm_blocked(const Team& T, const double* G, double* B, int n, int ld, const double* rdiag) {
+    const int TB = n >> 3;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    for (int kb = 0; kb < TB; ++kb) {
+        const int k0 = kb * 8;
+        const double* D = G + k0 * ld + k0;
+        for (int c = T.tid; c < n; c += T.nthr) {
+            double x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x[i] = TR ? B[c * ld + k0 + i] : B[(k0 + i) * ld + c];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                double s = x[i];
+#pragma unroll
+                for (int ip = 0; ip < i; ++ip) s -= D[i * ld + ip] * x[ip];
+                x[i] = s * rdiag[k0 + i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (TR) B[c * ld + k0 + i] = x[i];
+                else B[(k0 + i) * ld + c] = x[i];
+            }
+        }
+        __syncthreads();
+        const int nt = (TB - kb - 1) * TB;
+        for (int t = T.warp; t < nt; t += T.nwarps) {
+            int ib = kb + 1 + t / TB, cb = t % TB;
+            const double* A = G + ib * 8 * ld + k0;
+            double acc[2];
+            if (!TR) {
+                double* C = B + ib * 8 * ld + cb * 8;
+                acc[0] = C[r * ld + 2 * q];
+                acc[1] = C[r * ld + 2 * q + 1];
+                tile_msub<false>(acc, A, ld, B + k0 * ld + cb * 8, ld, 8, T.lane);
+                C[r * ld + 2 * q] = acc[0];
+                C[r * ld + 2 * q + 1] = acc[1];
+            } else {
+                double* Ct = B + cb * 8 * ld + ib * 8;  // W tile (ib, cb), element (r, c) at Ct[c*ld + r]
+                acc[0] = Ct[(2 * q) * ld + r];
+                acc[1] = Ct[(2 * q + 1) * ld + r];
+                tile_msub<true>(acc, A, ld, B + cb * 8 * ld + k0, ld, 8, T.lane);
+                Ct[(2 * q) * ld + r] = acc[0];
+                Ct[(2 * q + 1) * ld + r] = acc[1];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// extreme eigenvalue of the tridiagonal (al, be) of size J by CTA multisection
+// inside [lo, hi]; top = largest, else smallest.
+__device__ double tri_multisect(const Team& T, const double* al, const double* be, int J, bool top, double lo,
+                                double hi, double* red) {
+    const double eps = 2.220446049250313e-16;
+    for (int it = 0; it < 24; ++it) {
+        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
+        double sig = lo + (hi - lo) * ((double)(T.tid + 1) / (double)(T.nthr + 1));
+        int c = sturm_below(al, be, J, sig);
+        double ch, cl;
+        if (top) {
+            ch = (c == J) ? sig : SW_INF;
+            cl = (c < J) ? sig : -SW_INF;
+        } else {
+            ch = (c >= 1) ? sig : SW_INF;
+            cl = (c == 0) ? sig : -SW_INF;
+        }
+        double nh = block_min(T, ch, red);
+        double nl = block_max(T, cl, red);
+        hi = fmin(hi, nh);
+        lo = fmax(lo, nl);
+    }
+    return 0.5 * (lo + hi);
+}
+
+// four interleaved Sturm counts (independent dependency chains for ILP)
+__device__ __forceinline__ void sturm_below4(const double* d, const double* e, int md, const double (&sg)[4],
+                                             int (&cnt)[4]) {
+    double pp[4], p[4];
+    bool neg[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        pp[u] = 1.0;
+        p[u] = d[0] - sg[u];
+        cnt[u] = (p[u] <= 0.0) ? 1 : 0;
+        neg[u] = (p[u] <= 0.0);
+        if (p[u] == 0.0) p[u] = -1e-300;
+    }
+    for (int i = 1; i < md; ++i) {
+        const double e2 = e[i - 1] * e[i - 1], di = d[i];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            double pn = (di - sg[u]) * p[u] - e2 * pp[u];
+            bool nneg;
+            if (pn == 0.0) {
+                nneg = !neg[u];
+                pn = neg[u] ? 1e-300 : -1e-300;
+            } else {
+                nneg = pn < 0.0;
+            }
+            cnt[u] += (nneg != neg[u]) ? 1 : 0;
+            neg[u] = nneg;
+            pp[u] = p[u];
+            p[u] = pn;
+            double ap = fabs(pn);
+            if (ap > 0x1p+500) {
+                p[u] *= 0x1p-500;
+                pp[u] *= 0x1p-500;
+            } else if (ap < 0x1p-500 && fabs(pp[u]) < 0x1p-500) {
+                p[u] *= 0x1p+500;
+                pp[u] *= 0x1p+500;
+            }
+        }
+    }
+}
+
+// CTA multisection with 4 Sturm counts per thread (4*NT points per round)
+__device__ double tri_multisect4(const Team& T, const double* al, const double* be, int J, bool top, double lo,
+                                 double hi, double* red) {
+    const double eps = 2.220446049250313e-16;
+    const double inv = 1.0 / (double)(4 * T.nthr + 1);
+    for (int it = 0; it < 16; ++it) {
+        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
+        double sg[4];
+        int c[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) sg[u] = lo + (hi - lo) * ((double)(4 * T.tid + u + 1) * inv);
+        sturm_below4(al, be, J, sg, c);
+        double ch = SW_INF, cl = -SW_INF;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            bool above = top ? (c[u] == J) : (c[u] >= 1);
+            if (above) ch = fmin(ch, sg[u]);
+            else cl = fmax(cl, sg[u]);
+        }
+        ch = warp_min(ch);
+        cl = warp_max(cl);
+        if (T.lane == 0) {
+            red[T.warp] = ch;
+            red[32 + T.warp] = cl;
+        }
+        __syncthreads();
+        for (int w = 0; w < T.nwarps; ++w) {
+            hi = fmin(hi, red[w]);
+            lo = fmax(lo, red[32 + w]);
+        }
+        __syncthreads();
+    }
+    return 0.5 * (lo + hi);
+}
+
+// Extreme eigenvalue of the symmetric tridiagonal (al, be) of size J by
+// Laguerre's method on p(x) = det(x I - T) (all roots real): started above the
+// spectrum (top) it decreases monotonically to lambda_max, started below it
+// increases monotonically to lambda_min; cubic convergence.  p, p', p'' by the
+// three-term recurrence with exact power-of-two rescaling.  One thread.
+__device__ double tri_laguerre(const double* al, const double* be, int J, double x) {
+    const double eps = 2.220446049250313e-16;
+    if (J == 1) return al[0];
+    const double n = (double)J;
+    for (int it = 0; it < 40; ++it) {
+        double p0 = 1.0, d0 = 0.0, s0 = 0.0;          // p_{i-1}, p'_{i-1}, p''_{i-1}
+        double p1 = x - al[0], d1 = 1.0, s1 = 0.0;   // p_i ...
+        for (int i = 1; i < J; ++i) {
+            const double t = x - al[i], b2 = be[i - 1] * be[i - 1];
+            const double p2 = t * p1 - b2 * p0;
+            const double d2 = p1 + t * d1 - b2 * d0;
+            const double s2 = 2.0 * d1 + t * s1 - b2 * s0;
+            p0 = p1; d0 = d1; s0 = s1;
+            p1 = p2; d1 = d2; s1 = s2;
+            const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
+            if (ap > 0x1p+400) {
+                p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
+                p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
+            } else if (ap < 0x1p-400) {
+                p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
+                p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
+            }
+        }
+        if (p1 == 0.0) return x;
+        const double G = d1 / p1;
+        const double H = G * G - s1 / p1;
+        const double disc = fmax((n - 1.0) * (n * H - G * G), 0.0);
+        const double den = G + copysign(sqrt(disc), G);
+        if (den == 0.0) return x;
+        const double step = n / den;
+        x -= step;
+        if (fabs(step) <= 2.0 * eps * fabs(x)) break;
+    }
+    return x;
+}
+
+// warp-level multisection (32 Sturm counts per round, no block barriers)
+__device__ double tri_multisect_warp(int lane, const double* al, const double* be, int J, bool top, double lo,
+                                     double hi) {
+    const double eps = 2.220446049250313e-16;
+    for (int it = 0; it < 64; ++it) {
+        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
+        double sig = lo + (hi - lo) * ((double)(lane + 1) * (1.0 / 33.0));
+        int c = sturm_below(al, be, J, sig);
+        double ch, cl;
+        if (top) {
+            ch = (c == J) ? sig : SW_INF;
+            cl = (c < J) ? sig : -SW_INF;
+        } else {
+            ch = (c >= 1) ? sig : SW_INF;
+            cl = (c == 0) ? sig : -SW_INF;
+        }
+        hi = fmin(hi, warp_min(ch));
+        lo = fmax(lo, warp_max(cl));
+    }
+    return 0.5 * (lo + hi);
+}
+
+// Eigenvector s of the tridiagonal T_J (al, be) for the eigenvalue theta by a
+// twisted factorisation (Parlett-Dhillon): forward pivots D+ and backward
+// pivots D- of (T - theta I), twist index r = argmin |gamma_r|,
+// gamma_r = D+_r + D-_r - (al_r - theta); s_r = 1 and the two product sweeps
+// s_i = -(be_i / D+_i) s_{i+1} (i < r), s_i = -(be_{i-1} / D-_i) s_{i-1} (i > r).
+// Returns (to every thread) the Lanczos residual |beta_last| |s_{J-1}| / |s|;
+// s is normalised.  CTA-cooperative; dp, dm scratch of length J.
+__device__ double tri_twisted_vec(const Team& T, const double* al, const double* be, int J, double theta,
+                                  double beta_last, double* dp, double* dm, double* s, double* red, int* sh_r) {
+    const double tiny = 1e-290;
+    if (T.tid == 0) {
+        double d = al[0] - theta;
+        dp[0] = d;
+        for (int i = 1; i < J; ++i) {
+            double prev = dp[i - 1];
+            if (fabs(prev) < tiny) prev = (prev < 0.0 ? -tiny : tiny);
+            d = (al[i] - theta) - be[i - 1] * be[i - 1] / prev;
+            dp[i] = d;
+        }
+    } else if (T.tid == 32 || (T.nthr <= 32 && T.tid == 1)) {
+        double d = al[J - 1] - theta;
+        dm[J - 1] = d;
+        for (int i = J - 2; i >= 0; --i) {
+            double nxt = dm[i + 1];
+            if (fabs(nxt) < tiny) nxt = (nxt < 0.0 ? -tiny : tiny);
+            d = (al[i] - theta) - be[i] * be[i] / nxt;
+            dm[i] = d;
+        }
+    }
+    __syncthreads();
+    if (T.warp == 0) {
+        double bg = SW_INF;
+        int br = 0;
+        for (int i = T.lane; i < J; i += 32) {
+            double g = fabs(dp[i] + dm[i] - (al[i] - theta));
+            if (g < bg) { bg = g; br = i; }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double og = __shfl_xor_sync(0xffffffffu, bg, o);
+            int orr = __shfl_xor_sync(0xffffffffu, br, o);
+            if (og < bg || (og == bg && orr < br)) { bg = og; br = orr; }
+        }
+        if (T.lane == 0) *sh_r = br;
+    }
+    __syncthreads();
+    const int r = *sh_r;
+    if (T.tid == 0) {
+        s[r] = 1.0;
+        double prev = 1.0;
+        for (int i = r - 1; i >= 0; --i) {
+            double piv = dp[i];
+            if (fabs(piv) < tiny) piv = (piv < 0.0 ? -tiny : tiny);
+            double v = -(be[i] / piv) * prev;
+            if (fabs(v) > 1e200) v = copysign(1e200, v);
+            s[i] = v;
+            prev = v;
+        }
+    } else if (T.tid == 32 || (T.nthr <= 32 && T.tid == 1)) {
+        double prev = 1.0;
+        for (int i = r + 1; i < J; ++i) {
+            double piv = dm[i];
+            if (fabs(piv) < tiny) piv = (piv < 0.0 ? -tiny : tiny);
+            double v = -(be[i - 1] / piv) * prev;
+            if (fabs(v) > 1e200) v = copysign(1e200, v);
+            s[i] = v;
+            prev = v;
+        }
+    }
+    __syncthreads();
+    double nn = 0.0, mx = 0.0;
+    for (int i = T.tid; i < J; i += T.nthr) mx = fmax(mx, fabs(s[i]));
+    mx = block_max(T, mx, red);
+    double sc = 1.0 / mx;
+    for (int i = T.tid; i < J; i += T.nthr) {
+        double v = s[i] * sc;
+        nn += v * v;
+    }
+    nn = block_sum(T, nn, red);
+    double inv = sc / sqrt(nn);
+    for (int i = T.tid; i < J; i += T.nthr) s[i] *= inv;
+    __syncthreads();
+    return fabs(beta_last) * fabs(s[J - 1]);
+}
+
+template <int NT, bool SMEM>
+__global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
+    extern __shared__ __align__(16) double smem_dyn[];
+    Team T;
+    T.tid = threadIdx.x;
+    T.nthr = NT;
+    T.lane = T.tid & 31;
+    T.warp = T.tid >> 5;
+    T.nwarps = NT >> 5;
+    __shared__ double red[64];
+    __shared__ int sh_i[8];
+    __shared__ double sh_d[16];
+
+    const int m = P.m, n = P.n, ld = P.ld;
+    const int mp = (m + 7) & ~7;
+    double* base = SMEM ? smem_dyn : (P.scratch + (size_t)blockIdx.x * P.scratch_stride);
+    double* G = base;
+    double* B = base + (size_t)mp * ld;
+    double* Qm = G;  // Lanczos basis reuses L's space while L is parked in P.lsave
+    double* vec = B + (size_t)mp * ld;
+    double* Lsave = P.lsave + (size_t)blockIdx.x * P.lsave_stride;
+    const int vl = mp + 8;
+    double* uu = vec + 0 * vl;
+    double* hh = vec + 1 * vl;
+    double* pw = vec + 2 * vl;
+    double* rdiag = vec + 3 * vl;
+    double* wv = vec + 4 * vl;
+    double* hb = vec + 5 * vl;
+    double* al = vec + 6 * vl;
+    double* be = vec + 7 * vl;
+    double* sv = vec + 8 * vl;
+    double* zz = vec + 9 * vl;
+    double* yy = vec + 10 * vl;
+    double* dp = vec + 11 * vl;
+    double* bv = vec + 12 * vl;
+    double* sv2 = vec + 13 * vl;
+    double* dm = vec + 14 * vl;
+
+    const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
+    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
+        const int slot = P.list ? P.list[rr] : rr;
+        if (slot < 0) continue;
+        if (P.mode == 0 && (P.flags[slot] & CF_DONE)) continue;
+        const long long gidv = P.gid ? P.gid[slot] : P.chain_base + slot;
+        double* x = P.X + (size_t)slot * P.np;
+        double* v = P.V + (size_t)slot * P.np;
+        const double* av = P.AV + (size_t)slot * P.mtp;
+        double* ax = P.AX + (size_t)slot * P.mtp;
+        const int bnd = P.bound[slot];
+        __syncthreads();
+        long long t_prof = clock64();
+
+        // ---- 1. unpack A(x) -> G, A(v) -> B (full symmetric), zero padding
+        unpack_sym(T, ax, G, m, ld);
+        unpack_sym(T, av, B, m, ld);
+        const bool defl = (bnd == 0);
+        if (defl)
+            for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
+        __syncthreads();
+        PROF_MARK(0);
+        int md = m;
+        double a_schur = 0.0, beta_h = 0.0;
+        bool outward = false;
+        if (defl) {
+            double nu = 0.0;
+            for (int i = T.tid; i < m; i += T.nthr) nu += uu[i] * uu[i];
+            nu = sqrt(block_sum(T, nu, red));
+            for (int i = T.tid; i < m; i += T.nthr) hh[i] = uu[i] / nu;
+            __syncthreads();
+            if (T.tid == 0) hh[0] += (hh[0] >= 0.0 ? 1.0 : -1.0);
+            __syncthreads();
+            double h2 = 0.0;
+            for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
+            beta_h = 2.0 / block_sum(T, h2, red);
+            householder_congruence(T, G, m, ld, hh, beta_h, pw, red);
+            householder_congruence(T, B, m, ld, hh, beta_h, pw, red);
+            a_schur = B[0];
+            outward = !(a_schur > 0.0);
+            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld];
+            __syncthreads();
+            // Schur complement + shift the (1..m-1) block to (0..m-2): chunks of nwarps
+            // rows, each warp stages one source row in registers (m <= 256).
+            md = m - 1;
+            for (int i0 = 0; i0 < md; i0 += T.nwarps) {
+                constexpr int CMAX = 8;
+                double gv[CMAX], bvv[CMAX];
+                const int i = i0 + T.warp;
+#pragma unroll
+                for (int c = 0; c < CMAX; ++c) {
+                    int jx = T.lane + 32 * c;
+                    if (i < md && jx < md) {
+                        gv[c] = G[(i + 1) * ld + jx + 1];
+                        bvv[c] = outward ? 0.0 : B[(i + 1) * ld + jx + 1] - bv[i] * bv[jx] / a_schur;
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < CMAX; ++c) {
+                    int jx = T.lane + 32 * c;
+                    if (i < md && jx < md) {
+                        G[i * ld + jx] = gv[c];
+                        B[i * ld + jx] = bvv[c];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const int mdp = (md + 7) & ~7;
+        // padding rows/cols [md, mdp): G = I, B = 0
+        for (int i = md + T.warp; i < mdp; i += T.nwarps)
+            for (int j = T.lane; j < mdp; j += 32) {
+                G[i * ld + j] = (i == j) ? 1.0 : 0.0;
+                G[j * ld + i] = (i == j) ? 1.0 : 0.0;
+                B[i * ld + j] = 0.0;
+                B[j * ld + i] = 0.0;
+            }
+        __syncthreads();
+        PROF_MARK(1);
+
+        // ---- 2. dense chord
+        double theta_max = -SW_INF, theta_min = SW_INF;
+        bool degenerate = false, failed = false;
+        int lanczos_J = 0;
+        if (!outward && md >= 1) {
+            bool okc = cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2]);
+            PROF_MARK(2);
+            if (!okc) {
+                failed = true;
+            } else {
+                trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
+                trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                PROF_MARK(3);
+                // ---- M = -(B + B^T)/2 in place; park L (lower, with rdiag) in global
+                // scratch so that the Lanczos basis can use its shared memory.
+                for (int i = T.warp; i < mdp; i += T.nwarps) {
+                    for (int jx = T.lane; jx <= i; jx += 32) {
+                        double sv_ = -0.5 * (B[i * ld + jx] + B[jx * ld + i]);
+                        B[i * ld + jx] = sv_;
+                        B[jx * ld + i] = sv_;
+                        Lsave[i * ld + jx] = G[i * ld + jx];
+                    }
+                }
+                __syncthreads();
+                const int lrow = T.tid >> 2, lg = T.tid & 3;
+                // start vector: fixed pseudo-random, zero padding
+                double s0 = 0.0;
+                for (int e = T.tid; e < mdp; e += T.nthr) {
+                    double val = 0.0;
+                    if (e < md) {
+                        double f = (double)e * 0.6180339887498949;
+                        val = 0.5 + (f - floor(f));
+                    }
+                    Qm[e] = val;
+                    s0 += val * val;
+                }
+                s0 = block_sum(T, s0, red);
+                {
+                    double inv = 1.0 / sqrt(s0);
+                    for (int e = T.tid; e < mdp; e += T.nthr) Qm[e] *= inv;
+                }
+                __syncthreads();
+                const int jfirst = max(min(md, 12), (md * 9) / 20);
+                int next_check = jfirst;
+                double tnorm = 0.0;
+                double th_prev = -SW_INF, res_prev = SW_INF;
+                int J = 0;
+                for (int j = 0; j < md; ++j) {
+                    const double* qj = Qm + (size_t)j * ld;
+                    long long tl0 = clock64();
+                    // ---- w = M q_j: 4 threads per row, interleaved columns
+                    for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+                        const int rw = r0 + lrow;
+                        double a0 = 0.0, a1 = 0.0;
+                        if (rw < mdp) {
+                            const double* Mr = B + (size_t)rw * ld;
+                            for (int c = lg; c < mdp; c += 8) {
+                                a0 += Mr[c] * qj[c];
+                                a1 += Mr[c + 4] * qj[c + 4];
+                            }
+                        }
+                        a0 += a1;
+                        a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+                        a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+                        if (lg == 0 && rw < mdp) wv[rw] = a0;
+                    }
+                    __syncthreads();
+                    long long tl1 = clock64();
+                    long long tl2 = tl1, tl3 = tl1;
+                    // ---- classical Gram-Schmidt against q_0..q_j, second pass only if
+                    // the first one cancelled more than half of |w|^2 (DGKS).
+                    double alpha = 0.0, nn = 0.0, nn_before = 0.0;
+                    for (int pass = 0; pass < 2; ++pass) {
+                        const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w.w
+                        if (mdp <= 128) {
+                            double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+                            const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
+                            if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wv + i0);
+                            if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wv + i1);
+                            for (int i = T.warp; i < nrows; i += T.nwarps) {
+                                const double* qi = (i <= j) ? Qm + (size_t)i * ld : wv;
+                                double sacc = 0.0;
+                                if (i0 < mdp) {
+                                    double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
+                                    sacc += q0.x * w0.x + q0.y * w0.y;
+                                }
+                                if (i1 < mdp) {
+                                    double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
+                                    sacc += q1.x * w1.x + q1.y * w1.y;
+                                }
+                                sacc = warp_sum(sacc);
+                                if (T.lane == 0) hb[i] = sacc;
+                            }
+                        } else {
+                            for (int i = T.warp; i < nrows; i += T.nwarps) {
+                                const double* qi = (i <= j) ? Qm + (size_t)i * ld : wv;
+                                double sacc = 0.0;
+                                for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wv[c];
+                                sacc = warp_sum(sacc);
+                                if (T.lane == 0) hb[i] = sacc;
+                            }
+                        }
+                        __syncthreads();
+                        if (pass == 0) tl2 = clock64();
+                        alpha += hb[j];
+                        if (pass == 0) nn_before = hb[j + 1];
+                        {
+                            const int g = T.tid & 3, egrp = T.nthr >> 2;
+                            double nloc = 0.0;
+                            for (int e0 = 0; e0 < mdp; e0 += egrp) {
+                                const int e = e0 + (T.tid >> 2);
+                                double sa = 0.0, sb = 0.0;
+                                if (e < mdp) {
+                                    int i = g;
+                                    for (; i + 4 <= j; i += 8) {
+                                        sa += hb[i] * Qm[(size_t)i * ld + e];
+                                        sb += hb[i + 4] * Qm[(size_t)(i + 4) * ld + e];
+                                    }
+                                    for (; i <= j; i += 4) sa += hb[i] * Qm[(size_t)i * ld + e];
+                                }
+                                sa += sb;
+                                sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                                sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                                if (e < mdp) {
+                                    double wn = wv[e] - sa;
+                                    __syncwarp();
+                                    if (g == 0) wv[e] = wn;
+                                    nloc += (g == 0) ? wn * wn : 0.0;
+                                }
+                            }
+                            nn = block_sum(T, nloc, red);
+                        }
+                        if (pass == 0) tl3 = clock64();
+                        if (P.prof && T.tid == 0 && pass == 1) atomicAdd(&P.prof[15], 1ull);
+                        if (!(nn < 0.5 * nn_before)) break;
+                    }
+                    double beta = sqrt(nn);
+                    if (T.tid == 0) {
+                        al[j] = alpha;
+                        be[j] = beta;
+                    }
+                    tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
+                    J = j + 1;
+                    const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
+                    if (!exhausted) {
+                        double inv = 1.0 / beta;
+                        double* qn = Qm + (size_t)(j + 1) * ld;
+                        for (int e = T.tid; e < mdp; e += T.nthr) qn[e] = wv[e] * inv;
+                    }
+                    __syncthreads();
+                    if (P.prof && T.tid == 0) {
+                        long long tl4 = clock64();
+                        atomicAdd(&P.prof[12], (unsigned long long)(tl1 - tl0));
+                        atomicAdd(&P.prof[13], (unsigned long long)(tl2 - tl1));
+                        atomicAdd(&P.prof[14], (unsigned long long)(tl3 - tl2));
+                        atomicAdd(&P.prof[8 + 8], (unsigned long long)(tl4 - tl3));
+                    }
+                    if (exhausted || J >= next_check) {
+                        long long tc0 = clock64();
+                        // top Ritz value of T_J (and bottom in oracle mode): CTA multisection
+                        double glo = SW_INF, ghi = -SW_INF, amax = -SW_INF, amin = SW_INF;
+                        for (int i = T.tid; i < J; i += T.nthr) {
+                            double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
+                            glo = fmin(glo, al[i] - rsum);
+                            ghi = fmax(ghi, al[i] + rsum);
+                            amax = fmax(amax, al[i]);
+                            amin = fmin(amin, al[i]);
+                        }
+                        ghi = block_max(T, ghi, red);
+                        amax = block_max(T, amax, red);
+                        if (P.mode == 1) glo = block_min(T, glo, red);
+                        if (T.tid == 0) sh_d[4] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
+                        if (P.mode == 1 && T.tid == 32) sh_d[5] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
+                        __syncthreads();
+                        const double th = sh_d[4];
+                        double res = tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, &sh_i[3]);
+                        double thmin = SW_INF, resmin = 0.0;
+                        if (P.mode == 1) {
+                            thmin = sh_d[5];
+                            resmin = tri_twisted_vec(T, al, be, J, thmin, be[J - 1], dp, dm, sv2, red, &sh_i[3]);
+                        }
+                        th_prev = th;
+                        res_prev = res;
+                        theta_max = th;
+                        theta_min = thmin;
+                        if (P.prof && T.tid == 0) {
+                            atomicAdd(&P.prof[9], (unsigned long long)(clock64() - tc0));
+                            atomicAdd(&P.prof[11], 1ull);
+                        }
+                        const double tol = 1e-14 * tnorm;
+                        if (exhausted || (res <= tol && resmin <= tol)) break;
+                        next_check = min(md, J + 8);
+                    }
+                }
+                lanczos_J = J;
+                if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);
+                PROF_MARK(4);
+                if (T.tid == 0) {
+                    double th2 = theta_max - 1e-12 * fabs(theta_max);
+                    int c = sturm_below(al, be, J, th2);
+                    sh_i[0] = (md >= 2 && J >= 2 && c <= J - 2) ? 1 : 0;
+                }
+                __syncthreads();
+                degenerate = sh_i[0] != 0;
+                PROF_MARK(5);
+                if (theta_max > 0.0) {
+                    // z = Q s
+                    for (int e = T.tid; e < mdp; e += T.nthr) {
+                        double s = 0.0;
+                        for (int i = 0; i < J; ++i) s += sv[i] * Qm[(size_t)i * ld + e];
+                        zz[e] = s;
+                    }
+                    __syncthreads();
+                    for (int i = T.warp; i < md; i += T.nwarps)
+                        for (int jx = T.lane; jx < i; jx += 32) G[i * ld + jx] = Lsave[i * ld + jx];
+                    __syncthreads();
+                    PROF_MARK(6);
+                    if (T.warp == 0) {
+                        // y = L^{-T} z (column-oriented back substitution)
+                        for (int i = md - 1; i >= 0; --i) {
+                            double yi = zz[i] * rdiag[i];
+                            __syncwarp();
+                            if (T.lane == 0) yy[i] = yi;
+                            for (int k = T.lane; k < i; k += 32) zz[k] -= G[i * ld + k] * yi;
+                            __syncwarp();
+                        }
+                        if (defl) {  // y = H [ -b^T yh / a ; yh ]
+                            double s = 0.0;
+                            for (int i = T.lane; i < md; i += 32) s += bv[i] * yy[i];
+                            s = warp_sum(s);
+                            double alpha0 = -s / a_schur;
+                            __syncwarp();
+                            for (int base_i = md - 1; base_i >= 0; base_i -= 32) {
+                                int i = base_i - T.lane;
+                                double val = (i >= 0) ? yy[i] : 0.0;
+                                __syncwarp();
+                                if (i >= 0) yy[i + 1] = val;
+                                __syncwarp();
+                            }
+                            if (T.lane == 0) yy[0] = alpha0;
+                            __syncwarp();
+                            double hy = 0.0;
+                            for (int i = T.lane; i < m; i += 32) hy += hh[i] * yy[i];
+                            hy = warp_sum(hy) * beta_h;
+                            for (int i = T.lane; i < m; i += 32) yy[i] -= hy * hh[i];
+                            __syncwarp();
+                        }
+                        double yn = 0.0;
+                        for (int i = T.lane; i < m; i += 32) yn += yy[i] * yy[i];
+                        yn = sqrt(warp_sum(yn));
+                        for (int i = T.lane; i < m; i += 32) yy[i] /= yn;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        PROF_MARK(7);
+        (void)lanczos_J;
+
+#include "chord_tail.inc"
+    }
+}
+
+}  // namespace sw

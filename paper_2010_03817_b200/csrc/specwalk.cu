@@ -18,6 +18,7 @@
 #include "../../include/specwalk.h"
 #include "gemm.cuh"
 #include "walk.cuh"
+#include "chord2.cuh"
 
 using namespace sw;
 
@@ -68,12 +69,15 @@ struct spec_ctx {
     long long scratch_stride = 0;
     int scratch_ctas = 0;
     bool smem_path = true;
+    int k2_variant = 0;
     size_t smem_bytes = 0;
     int chord_threads = 256;
     int chord_grid_max = 0;
     int num_sms = 0;
     long long* dstats = nullptr;
     unsigned long long* prof = nullptr;
+    double* lsave = nullptr;
+    long long lsave_stride = 0;
     long long launches = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     void* walk = nullptr;  // WalkRun*
@@ -156,7 +160,6 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     ctx->np = roundup(n, 64);
     ctx->mt = m * (m + 1) / 2;
     ctx->mtp = roundup(ctx->mt, 64);
-    ctx->ld = m | 1;
     // packed, symmetrised, padded coefficient matrix
     std::vector<double> Ah((size_t)ctx->np * ctx->mtp, 0.0), a0((size_t)ctx->mtp, 0.0);
     double amax = 0.0;
@@ -185,24 +188,44 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     CK(zalloc(&ctx->c, ctx->np));
     CK(zalloc(&ctx->ball_c, ctx->np));
     CK(zalloc(&ctx->dstats, 8));
-    if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 16));
-    // K2 placement: shared memory if it fits, else a global scratch slice per CTA
-    size_t per_cta = (size_t)2 * m * ctx->ld + (size_t)NVEC * m + 64;
+    if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 32));
+    // K2 variant: M register-resident (m <= 128) with matrices in shared memory,
+    // else matrices + Lanczos basis in a per-CTA global scratch slice.
+    const int mp = roundup(m, 8);
+    ctx->ld = mp + 4;
+    if (mp <= 64) {
+        ctx->k2_variant = 0;
+        ctx->chord_threads = 256;
+    } else if (mp <= 128) {
+        ctx->k2_variant = 1;
+        ctx->chord_threads = 512;
+    } else {
+        ctx->k2_variant = 2;
+        ctx->chord_threads = 512;
+    }
+    size_t vecs = (size_t)NVEC2 * (mp + 8) + 64;
+    size_t per_cta = (size_t)2 * mp * ctx->ld + vecs;
     ctx->smem_bytes = per_cta * sizeof(double);
-    ctx->chord_threads = (m <= 32) ? 64 : (m <= 64 ? 128 : 256);
-    if (ctx->smem_bytes <= 200 * 1024) {
+    int occ = 0;
+    if (ctx->k2_variant < 2 && ctx->smem_bytes <= 227 * 1024) {
         ctx->smem_path = true;
-        CK(cudaFuncSetAttribute(chord_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)ctx->smem_bytes));
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel<true>, ctx->chord_threads,
-                                                         ctx->smem_bytes));
-        if (occ < 1) occ = 1;
+        if (ctx->k2_variant == 0) {
+            CK(cudaFuncSetAttribute(chord_kernel2<256, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_bytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<256, true>, 256,
+                                                             ctx->smem_bytes));
+        } else {
+            CK(cudaFuncSetAttribute(chord_kernel2<512, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_bytes));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, true>, 512,
+                                                             ctx->smem_bytes));
+        }
+        if (occ < 1) return fail(SPEC_ECUDA, "chord kernel cannot be resident (registers / shared memory)");
         ctx->chord_grid_max = occ * ctx->num_sms;
     } else {
         ctx->smem_path = false;
-        int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel<false>, ctx->chord_threads, 0));
+        ctx->k2_variant = 2;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false>, 512, 0));
         if (occ < 1) occ = 1;
         if (occ > 2) occ = 2;
         ctx->chord_grid_max = occ * ctx->num_sms;
@@ -211,6 +234,8 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
         ctx->smem_bytes = 0;
     }
+    ctx->lsave_stride = (long long)mp * ctx->ld;
+    CK(zalloc(&ctx->lsave, (size_t)ctx->lsave_stride * ctx->chord_grid_max));
     *out = ctx;
     return SPEC_OK;
 }
@@ -221,7 +246,7 @@ extern "C" int spec_destroy(spec_ctx* ctx) {
     free_walk(ctx);
     cudaSetDevice(ctx->dev);
     free_chains(ctx->cb);
-    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof};
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -293,16 +318,20 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.scratch = ctx->scratch; P.scratch_stride = ctx->scratch_stride;
     P.nlist = b.nlist; P.ncount = b.counters + 2;
     P.prof = ctx->prof;
+    P.lsave = ctx->lsave;
+    P.lsave_stride = ctx->lsave_stride;
     return P;
 }
 
 static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
     int grid = count_host < ctx->chord_grid_max ? count_host : ctx->chord_grid_max;
     if (grid < 1) grid = 1;
-    if (ctx->smem_path)
-        chord_kernel<true><<<grid, ctx->chord_threads, ctx->smem_bytes, ctx->stream>>>(P);
+    if (ctx->k2_variant == 0)
+        chord_kernel2<256, true><<<grid, 256, ctx->smem_bytes, ctx->stream>>>(P);
+    else if (ctx->k2_variant == 1)
+        chord_kernel2<512, true><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
     else
-        chord_kernel<false><<<grid, ctx->chord_threads, 0, ctx->stream>>>(P);
+        chord_kernel2<512, false><<<grid, 512, 0, ctx->stream>>>(P);
     ctx->launches++;
 }
 
@@ -609,7 +638,7 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         st->device_ms = W.ms;
     }
     if (ctx->prof) {
-        unsigned long long ph[16];
+        unsigned long long ph[32];
         CK(cudaMemcpy(ph, ctx->prof, sizeof(ph), cudaMemcpyDeviceToHost));
         CK(cudaMemset(ctx->prof, 0, sizeof(ph)));
         const char* names[] = {"unpack", "deflate", "cholesky", "congruence", "eigen", "extreme", "eigvec",
@@ -618,7 +647,12 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         for (int i = 0; i < 9; ++i) tot += (double)ph[i];
         fprintf(stderr, "[specwalk prof] m=%d calls=%lld cycles/call:", ctx->m, (long long)hs[0]);
         for (int i = 0; i < 9; ++i) fprintf(stderr, " %s=%.0f", names[i], (double)ph[i] / (double)hs[0]);
-        fprintf(stderr, " total=%.0f\n", tot / (double)hs[0]);
+        fprintf(stderr, " total=%.0f | lanczos: J/call=%.1f check_cycles/call=%.0f checks/call=%.2f\n",
+                tot / (double)hs[0], (double)ph[10] / (double)hs[0], (double)ph[9] / (double)hs[0],
+                (double)ph[11] / (double)hs[0]);
+        double it = (double)ph[10];
+        fprintf(stderr, "[specwalk prof] per lanczos iteration: matvec=%.0f dots=%.0f axpy+norm(+pass2)=%.0f qwrite=%.0f pass2_frac=%.3f\n",
+                ph[12] / it, ph[13] / it, ph[14] / it, ph[16] / it, ph[15] / it);
     }
     return SPEC_OK;
 }
