@@ -99,6 +99,17 @@ int boundary_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double*
 int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
                         double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding);
 
+/* hmc_oracle -- the reflective-HMC boundary oracle (Alg. 6) for
+ * the Boltzmann density exp(-c^T x / T) (c from spec_set_objective): the first
+ * positive root t+ of det F(x + t v - t^2 c / (2T)) (eq:boltz_ode P:1440-1446,
+ * a degree-2 PEP, eq:PEP P:307-316), by monotone Weyl stepping on the
+ * quadratic pencil (interior start) or on the sqrt(t)-deflated symmetric
+ * quartic (u != NULL: x on the dense boundary with unit kernel u).
+ * Outputs as boundary_oracle (no t_minus); normal is the outward normal at
+ * the hit.  EINVAL without an objective or T <= 0. */
+int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, double T,
+               double* t_plus, double* normal, double* kernel, int32_t* binding);
+
 /* ---- walks ---- */
 enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1 };
 

@@ -34,7 +34,7 @@ EXPORTS = (
     "spec_last_error", "spec_create", "spec_destroy", "spec_set_objective", "spec_set_ball", "boundary_oracle",
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
-    "spec_kernel_times",
+    "spec_kernel_times", "hmc_oracle",
 )
 
 
@@ -98,6 +98,7 @@ def load(build_if_missing: bool = True):
     l.spec_walk_stats_now.argtypes = [C.c_void_p, C.POINTER(WalkStats)]
     l.spec_kernel_timing.argtypes = [C.c_void_p, C.c_int]
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
+    l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     _lib = l
     return l
 
@@ -171,6 +172,24 @@ class Spectrahedron:
         _check(_lib.boundary_oracle(self._h, B, _p(x), _p(v), _p(ua), _p(tm), _p(tp), _p(nrm), _p(ker),
                                     bind.ctypes.data_as(_ip)))
         out = dict(t_minus=tm, t_plus=tp, normal=nrm, binding=bind)
+        if want_kernel:
+            out["kernel"] = ker
+        return out
+
+    def hmc_oracle(self, x, v, T: float, u=None, want_kernel: bool = False) -> dict:
+        """Reflective-HMC chord on x + v t - c t^2 / (2T) (Alg. 6, eq:boltz_ode)."""
+        x, v = _f64(x), _f64(v)
+        if x.ndim == 1:
+            x, v = x[None], v[None]
+        B = x.shape[0]
+        ua = _f64(u).reshape(B, self.m) if u is not None else None
+        tp = np.empty(B)
+        nrm = np.empty((B, self.n))
+        ker = np.empty((B, self.m)) if want_kernel else None
+        bind = np.empty(B, dtype=np.int32)
+        _check(_lib.hmc_oracle(self._h, B, _p(x), _p(v), _p(ua), float(T), _p(tp), _p(nrm), _p(ker),
+                               bind.ctypes.data_as(_ip)))
+        out = dict(t_plus=tp, normal=nrm, binding=bind)
         if want_kernel:
             out["kernel"] = ker
         return out
@@ -253,6 +272,7 @@ class Spectrahedron:
 
     def walk_trace(self, chain_ids, steps: int, L: float, rho: int, seed: int, max_refl: int,
                    kind: int = BILLIARD, T: float = 1.0) -> list:
+        """First max_refl reflections of the given global chain ids (parity entry)."""
         ids = np.ascontiguousarray(np.asarray(chain_ids, dtype=np.int64))
         k = len(ids)
         p = self._params(kind, k, steps, L, rho, seed, 0, 0, T)

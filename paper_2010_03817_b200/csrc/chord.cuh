@@ -80,6 +80,11 @@ struct ChordParams {
     unsigned long long* prof;  // optional per-phase cycle counters (SPECWALK_PROF=1)
     double* lsave;             // per-CTA global slice where L is parked during Lanczos
     long long lsave_stride;
+    // HMC-r (K5)
+    const double* Ac;  // packed A(c) = sum c_i A_i
+    const double* cvec;
+    double Temp;
+    double* tlast;  // t+ of the last hit (velocity at the hit = v - (c/T) t+)
 };
 
 // ---------------------------------------------------------------- team helpers

@@ -408,6 +408,192 @@ __device__ double tri_twisted_vec(const Team& T, const double* al, const double*
     return fabs(beta_last) * fabs(s[J - 1]);
 }
 
+// Lanczos (full CGS2/DGKS reorthogonalisation) on the symmetric md x md matrix M
+// (shared or global memory, leading dimension ld, zero padded to mdp).  Q holds
+// the basis (rows of length ld).  Convergence: residual beta_J |s_J| <= 1e-14 |T|
+// for the requested extreme Ritz pair(s) (top: sv, bottom: sv2), checked from
+// J = 0.45 md on, every 8 steps; Ritz values by Laguerre, vectors by a twisted
+// factorisation.  Returns J; theta_top / theta_bot set.
+__device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, int mdp, int ld, bool need_top,
+                           bool need_bot, double* wv, double* hb, double* al, double* be, double* sv, double* sv2,
+                           double* dp, double* dm, double* red, int* sh_r, double* shd,
+                           unsigned long long* prof, double* theta_top, double* theta_bot) {
+    const int lrow = T.tid >> 2, lg = T.tid & 3;
+    const int NT = T.nthr;
+    *theta_top = -SW_INF;
+    *theta_bot = SW_INF;
+    // start vector: fixed pseudo-random, zero padding
+    double s0 = 0.0;
+    for (int e = T.tid; e < mdp; e += T.nthr) {
+        double val = 0.0;
+        if (e < md) {
+            double f = (double)e * 0.6180339887498949;
+            val = 0.5 + (f - floor(f));
+        }
+        Q[e] = val;
+        s0 += val * val;
+    }
+    s0 = block_sum(T, s0, red);
+    {
+        double inv = 1.0 / sqrt(s0);
+        for (int e = T.tid; e < mdp; e += T.nthr) Q[e] *= inv;
+    }
+    __syncthreads();
+    const int jfirst = max(min(md, 12), (md * 9) / 20);
+    int next_check = jfirst;
+    double tnorm = 0.0;
+    double th_prev = -SW_INF, res_prev = SW_INF;
+    int J = 0;
+    for (int j = 0; j < md; ++j) {
+        const double* qj = Q + (size_t)j * ld;
+        long long tl0 = clock64();
+        // ---- w = M q_j: 4 threads per row, interleaved columns
+        for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+            const int rw = r0 + lrow;
+            double a0 = 0.0, a1 = 0.0;
+            if (rw < mdp) {
+                const double* Mr = M + (size_t)rw * ld;
+                for (int c = lg; c < mdp; c += 8) {
+                    a0 += Mr[c] * qj[c];
+                    a1 += Mr[c + 4] * qj[c + 4];
+                }
+            }
+            a0 += a1;
+            a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+            a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+            if (lg == 0 && rw < mdp) wv[rw] = a0;
+        }
+        __syncthreads();
+        long long tl1 = clock64();
+        long long tl2 = tl1, tl3 = tl1;
+        // ---- classical Gram-Schmidt against q_0..q_j, second pass only if
+        // the first one cancelled more than half of |w|^2 (DGKS).
+        double alpha = 0.0, nn = 0.0, nn_before = 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+            const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w.w
+            if (mdp <= 128) {
+                double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+                const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
+                if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wv + i0);
+                if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wv + i1);
+                for (int i = T.warp; i < nrows; i += T.nwarps) {
+                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wv;
+                    double sacc = 0.0;
+                    if (i0 < mdp) {
+                        double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
+                        sacc += q0.x * w0.x + q0.y * w0.y;
+                    }
+                    if (i1 < mdp) {
+                        double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
+                        sacc += q1.x * w1.x + q1.y * w1.y;
+                    }
+                    sacc = warp_sum(sacc);
+                    if (T.lane == 0) hb[i] = sacc;
+                }
+            } else {
+                for (int i = T.warp; i < nrows; i += T.nwarps) {
+                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wv;
+                    double sacc = 0.0;
+                    for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wv[c];
+                    sacc = warp_sum(sacc);
+                    if (T.lane == 0) hb[i] = sacc;
+                }
+            }
+            __syncthreads();
+            if (pass == 0) tl2 = clock64();
+            alpha += hb[j];
+            if (pass == 0) nn_before = hb[j + 1];
+            {
+                const int g = T.tid & 3, egrp = T.nthr >> 2;
+                double nloc = 0.0;
+                for (int e0 = 0; e0 < mdp; e0 += egrp) {
+                    const int e = e0 + (T.tid >> 2);
+                    double sa = 0.0, sb = 0.0;
+                    if (e < mdp) {
+                        int i = g;
+                        for (; i + 4 <= j; i += 8) {
+                            sa += hb[i] * Q[(size_t)i * ld + e];
+                            sb += hb[i + 4] * Q[(size_t)(i + 4) * ld + e];
+                        }
+                        for (; i <= j; i += 4) sa += hb[i] * Q[(size_t)i * ld + e];
+                    }
+                    sa += sb;
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                    if (e < mdp) {
+                        double wn = wv[e] - sa;
+                        __syncwarp();
+                        if (g == 0) wv[e] = wn;
+                        nloc += (g == 0) ? wn * wn : 0.0;
+                    }
+                }
+                nn = block_sum(T, nloc, red);
+            }
+            if (pass == 0) tl3 = clock64();
+            if (prof && T.tid == 0 && pass == 1) atomicAdd(&prof[15], 1ull);
+            if (!(nn < 0.5 * nn_before)) break;
+        }
+        double beta = sqrt(nn);
+        if (T.tid == 0) {
+            al[j] = alpha;
+            be[j] = beta;
+        }
+        tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
+        J = j + 1;
+        const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
+        if (!exhausted) {
+            double inv = 1.0 / beta;
+            double* qn = Q + (size_t)(j + 1) * ld;
+            for (int e = T.tid; e < mdp; e += T.nthr) qn[e] = wv[e] * inv;
+        }
+        __syncthreads();
+        if (prof && T.tid == 0) {
+            long long tl4 = clock64();
+            atomicAdd(&prof[12], (unsigned long long)(tl1 - tl0));
+            atomicAdd(&prof[13], (unsigned long long)(tl2 - tl1));
+            atomicAdd(&prof[14], (unsigned long long)(tl3 - tl2));
+            atomicAdd(&prof[8 + 8], (unsigned long long)(tl4 - tl3));
+        }
+        if (exhausted || J >= next_check) {
+            long long tc0 = clock64();
+            // top Ritz value of T_J (and bottom in oracle mode): CTA multisection
+            double glo = SW_INF, ghi = -SW_INF, amax = -SW_INF, amin = SW_INF;
+            for (int i = T.tid; i < J; i += T.nthr) {
+                double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
+                glo = fmin(glo, al[i] - rsum);
+                ghi = fmax(ghi, al[i] + rsum);
+                amax = fmax(amax, al[i]);
+                amin = fmin(amin, al[i]);
+            }
+            ghi = block_max(T, ghi, red);
+            amax = block_max(T, amax, red);
+            if (need_bot) glo = block_min(T, glo, red);
+            if (T.tid == 0) shd[0] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
+            if (need_bot && T.tid == 32) shd[1] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
+            __syncthreads();
+            const double th = shd[0];
+            double res = tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, sh_r);
+            double thmin = SW_INF, resmin = 0.0;
+            if (need_bot) {
+                thmin = shd[1];
+                resmin = tri_twisted_vec(T, al, be, J, thmin, be[J - 1], dp, dm, sv2, red, sh_r);
+            }
+            th_prev = th;
+            res_prev = res;
+            *theta_top = th;
+            *theta_bot = thmin;
+            if (prof && T.tid == 0) {
+                atomicAdd(&prof[9], (unsigned long long)(clock64() - tc0));
+                atomicAdd(&prof[11], 1ull);
+            }
+            const double tol = 1e-14 * tnorm;
+            if (exhausted || ((!need_top || res <= tol) && (!need_bot || resmin <= tol))) break;
+            next_check = min(md, J + 8);
+        }
+    }
+    return J;
+}
+
 template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
@@ -551,176 +737,8 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
                     }
                 }
                 __syncthreads();
-                const int lrow = T.tid >> 2, lg = T.tid & 3;
-                // start vector: fixed pseudo-random, zero padding
-                double s0 = 0.0;
-                for (int e = T.tid; e < mdp; e += T.nthr) {
-                    double val = 0.0;
-                    if (e < md) {
-                        double f = (double)e * 0.6180339887498949;
-                        val = 0.5 + (f - floor(f));
-                    }
-                    Qm[e] = val;
-                    s0 += val * val;
-                }
-                s0 = block_sum(T, s0, red);
-                {
-                    double inv = 1.0 / sqrt(s0);
-                    for (int e = T.tid; e < mdp; e += T.nthr) Qm[e] *= inv;
-                }
-                __syncthreads();
-                const int jfirst = max(min(md, 12), (md * 9) / 20);
-                int next_check = jfirst;
-                double tnorm = 0.0;
-                double th_prev = -SW_INF, res_prev = SW_INF;
-                int J = 0;
-                for (int j = 0; j < md; ++j) {
-                    const double* qj = Qm + (size_t)j * ld;
-                    long long tl0 = clock64();
-                    // ---- w = M q_j: 4 threads per row, interleaved columns
-                    for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
-                        const int rw = r0 + lrow;
-                        double a0 = 0.0, a1 = 0.0;
-                        if (rw < mdp) {
-                            const double* Mr = B + (size_t)rw * ld;
-                            for (int c = lg; c < mdp; c += 8) {
-                                a0 += Mr[c] * qj[c];
-                                a1 += Mr[c + 4] * qj[c + 4];
-                            }
-                        }
-                        a0 += a1;
-                        a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
-                        a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-                        if (lg == 0 && rw < mdp) wv[rw] = a0;
-                    }
-                    __syncthreads();
-                    long long tl1 = clock64();
-                    long long tl2 = tl1, tl3 = tl1;
-                    // ---- classical Gram-Schmidt against q_0..q_j, second pass only if
-                    // the first one cancelled more than half of |w|^2 (DGKS).
-                    double alpha = 0.0, nn = 0.0, nn_before = 0.0;
-                    for (int pass = 0; pass < 2; ++pass) {
-                        const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w.w
-                        if (mdp <= 128) {
-                            double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-                            const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
-                            if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wv + i0);
-                            if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wv + i1);
-                            for (int i = T.warp; i < nrows; i += T.nwarps) {
-                                const double* qi = (i <= j) ? Qm + (size_t)i * ld : wv;
-                                double sacc = 0.0;
-                                if (i0 < mdp) {
-                                    double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
-                                    sacc += q0.x * w0.x + q0.y * w0.y;
-                                }
-                                if (i1 < mdp) {
-                                    double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
-                                    sacc += q1.x * w1.x + q1.y * w1.y;
-                                }
-                                sacc = warp_sum(sacc);
-                                if (T.lane == 0) hb[i] = sacc;
-                            }
-                        } else {
-                            for (int i = T.warp; i < nrows; i += T.nwarps) {
-                                const double* qi = (i <= j) ? Qm + (size_t)i * ld : wv;
-                                double sacc = 0.0;
-                                for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wv[c];
-                                sacc = warp_sum(sacc);
-                                if (T.lane == 0) hb[i] = sacc;
-                            }
-                        }
-                        __syncthreads();
-                        if (pass == 0) tl2 = clock64();
-                        alpha += hb[j];
-                        if (pass == 0) nn_before = hb[j + 1];
-                        {
-                            const int g = T.tid & 3, egrp = T.nthr >> 2;
-                            double nloc = 0.0;
-                            for (int e0 = 0; e0 < mdp; e0 += egrp) {
-                                const int e = e0 + (T.tid >> 2);
-                                double sa = 0.0, sb = 0.0;
-                                if (e < mdp) {
-                                    int i = g;
-                                    for (; i + 4 <= j; i += 8) {
-                                        sa += hb[i] * Qm[(size_t)i * ld + e];
-                                        sb += hb[i + 4] * Qm[(size_t)(i + 4) * ld + e];
-                                    }
-                                    for (; i <= j; i += 4) sa += hb[i] * Qm[(size_t)i * ld + e];
-                                }
-                                sa += sb;
-                                sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-                                sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-                                if (e < mdp) {
-                                    double wn = wv[e] - sa;
-                                    __syncwarp();
-                                    if (g == 0) wv[e] = wn;
-                                    nloc += (g == 0) ? wn * wn : 0.0;
-                                }
-                            }
-                            nn = block_sum(T, nloc, red);
-                        }
-                        if (pass == 0) tl3 = clock64();
-                        if (P.prof && T.tid == 0 && pass == 1) atomicAdd(&P.prof[15], 1ull);
-                        if (!(nn < 0.5 * nn_before)) break;
-                    }
-                    double beta = sqrt(nn);
-                    if (T.tid == 0) {
-                        al[j] = alpha;
-                        be[j] = beta;
-                    }
-                    tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
-                    J = j + 1;
-                    const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
-                    if (!exhausted) {
-                        double inv = 1.0 / beta;
-                        double* qn = Qm + (size_t)(j + 1) * ld;
-                        for (int e = T.tid; e < mdp; e += T.nthr) qn[e] = wv[e] * inv;
-                    }
-                    __syncthreads();
-                    if (P.prof && T.tid == 0) {
-                        long long tl4 = clock64();
-                        atomicAdd(&P.prof[12], (unsigned long long)(tl1 - tl0));
-                        atomicAdd(&P.prof[13], (unsigned long long)(tl2 - tl1));
-                        atomicAdd(&P.prof[14], (unsigned long long)(tl3 - tl2));
-                        atomicAdd(&P.prof[8 + 8], (unsigned long long)(tl4 - tl3));
-                    }
-                    if (exhausted || J >= next_check) {
-                        long long tc0 = clock64();
-                        // top Ritz value of T_J (and bottom in oracle mode): CTA multisection
-                        double glo = SW_INF, ghi = -SW_INF, amax = -SW_INF, amin = SW_INF;
-                        for (int i = T.tid; i < J; i += T.nthr) {
-                            double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
-                            glo = fmin(glo, al[i] - rsum);
-                            ghi = fmax(ghi, al[i] + rsum);
-                            amax = fmax(amax, al[i]);
-                            amin = fmin(amin, al[i]);
-                        }
-                        ghi = block_max(T, ghi, red);
-                        amax = block_max(T, amax, red);
-                        if (P.mode == 1) glo = block_min(T, glo, red);
-                        if (T.tid == 0) sh_d[4] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
-                        if (P.mode == 1 && T.tid == 32) sh_d[5] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
-                        __syncthreads();
-                        const double th = sh_d[4];
-                        double res = tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, &sh_i[3]);
-                        double thmin = SW_INF, resmin = 0.0;
-                        if (P.mode == 1) {
-                            thmin = sh_d[5];
-                            resmin = tri_twisted_vec(T, al, be, J, thmin, be[J - 1], dp, dm, sv2, red, &sh_i[3]);
-                        }
-                        th_prev = th;
-                        res_prev = res;
-                        theta_max = th;
-                        theta_min = thmin;
-                        if (P.prof && T.tid == 0) {
-                            atomicAdd(&P.prof[9], (unsigned long long)(clock64() - tc0));
-                            atomicAdd(&P.prof[11], 1ull);
-                        }
-                        const double tol = 1e-14 * tnorm;
-                        if (exhausted || (res <= tol && resmin <= tol)) break;
-                        next_check = min(md, J + 8);
-                    }
-                }
+                int J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
+                                    &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min);
                 lanczos_J = J;
                 if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);
                 PROF_MARK(4);

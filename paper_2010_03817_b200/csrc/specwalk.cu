@@ -19,6 +19,7 @@
 #include "gemm.cuh"
 #include "walk.cuh"
 #include "chord2.cuh"
+#include "hmc.cuh"
 
 using namespace sw;
 
@@ -42,7 +43,7 @@ static int roundup(int a, int b) { return (a + b - 1) / b * b; }
 struct ChainBuf {
     long long cap = 0;
     double *X = nullptr, *Xs = nullptr, *V = nullptr, *AX = nullptr, *AXs = nullptr, *AV = nullptr, *Yh = nullptr,
-           *U = nullptr, *Gn = nullptr, *ell = nullptr;
+           *U = nullptr, *Gn = nullptr, *ell = nullptr, *tlast = nullptr;
     int *steps_done = nullptr, *refl = nullptr, *bound = nullptr, *flags = nullptr, *nrej = nullptr, *ndeg = nullptr;
     long long *calls = nullptr, *nrefl = nullptr;
     int *list = nullptr, *list2 = nullptr, *nlist = nullptr;
@@ -59,7 +60,12 @@ struct spec_ctx {
     double *lo = nullptr, *hi = nullptr;
     int has_cube = 0;
     double* c = nullptr;
+    double* Ac = nullptr;
     int has_obj = 0;
+    double* hmc_scratch = nullptr;
+    long long hmc_stride = 0;
+    int hmc_grid = 0;
+    size_t hmc_smem = 0;
     double* ball_c = nullptr;
     double ball_r = 0.0;
     int has_ball = 0;
@@ -84,7 +90,7 @@ struct spec_ctx {
 };
 
 static void free_chains(ChainBuf& b) {
-    void* ps[] = {b.X, b.Xs, b.V, b.AX, b.AXs, b.AV, b.Yh, b.U, b.Gn, b.ell, b.steps_done, b.refl, b.bound,
+    void* ps[] = {b.X, b.Xs, b.V, b.AX, b.AXs, b.AV, b.Yh, b.U, b.Gn, b.ell, b.tlast, b.steps_done, b.refl, b.bound,
                   b.flags, b.nrej, b.ndeg, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid};
     for (void* p : ps)
         if (p) cudaFree(p);
@@ -108,7 +114,7 @@ static int ensure_chains(spec_ctx* ctx, long long C) {
 #define ZA(ptr, cnt) \
     if (e == cudaSuccess) e = zalloc(&b.ptr, (size_t)(cnt));
     ZA(X, cap * np) ZA(Xs, cap * np) ZA(V, cap * np) ZA(Gn, cap * np) ZA(AX, cap * mtp) ZA(AXs, cap * mtp)
-    ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(steps_done, cap) ZA(refl, cap)
+    ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(tlast, cap) ZA(steps_done, cap) ZA(refl, cap)
     ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
     ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap)
 #undef ZA
@@ -186,6 +192,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         ctx->has_cube = 1;
     }
     CK(zalloc(&ctx->c, ctx->np));
+    CK(zalloc(&ctx->Ac, ctx->mtp));
     CK(zalloc(&ctx->ball_c, ctx->np));
     CK(zalloc(&ctx->dstats, 8));
     if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 32));
@@ -246,7 +253,7 @@ extern "C" int spec_destroy(spec_ctx* ctx) {
     free_walk(ctx);
     cudaSetDevice(ctx->dev);
     free_chains(ctx->cb);
-    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave};
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -263,6 +270,8 @@ extern "C" int spec_sync(spec_ctx* ctx) {
 extern "C" void* spec_stream(spec_ctx* ctx) { return (void*)ctx->stream; }
 extern "C" int64_t spec_kernel_launches(spec_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+static void launch_gemm_av(spec_ctx* ctx, const double* Arows, const int* list, const int* count_dev,
+                           int count_host, double* out, const double* bias);
 extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
     if (!ctx || !c) return fail(SPEC_EINVAL, "null argument");
     double s = 0.0;
@@ -270,6 +279,9 @@ extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
     if (!(s > 0.0) || !std::isfinite(s)) return fail(SPEC_EINVAL, "|c| must be finite and > 0");
     CK(cudaSetDevice(ctx->dev));
     CK(cudaMemcpy(ctx->c, c, sizeof(double) * ctx->n, cudaMemcpyHostToDevice));
+    // A(c) = sum_i c_i A_i (packed), the t^2 coefficient of the HMC pencil up to -1/(2T)
+    launch_gemm_av(ctx, ctx->c, nullptr, nullptr, 1, ctx->Ac, nullptr);
+    CK(cudaStreamSynchronize(ctx->stream));
     ctx->has_obj = 1;
     return SPEC_OK;
 }
@@ -320,6 +332,9 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.prof = ctx->prof;
     P.lsave = ctx->lsave;
     P.lsave_stride = ctx->lsave_stride;
+    P.Ac = ctx->Ac;
+    P.cvec = ctx->c;
+    P.tlast = b.tlast;
     return P;
 }
 
@@ -335,6 +350,31 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
     ctx->launches++;
 }
 
+// K5 (HMC-r) resources: 8 matrices of mp x ld per CTA in global scratch
+static int ensure_hmc(spec_ctx* ctx) {
+    if (ctx->hmc_scratch) return SPEC_OK;
+    const int mp = roundup(ctx->m, 8);
+    ctx->hmc_stride = (long long)8 * mp * ctx->ld;
+    ctx->hmc_smem = sizeof(double) * (size_t)14 * (mp + 8);
+    CK(cudaFuncSetAttribute(hmc_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->hmc_smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hmc_kernel<512>, 512, ctx->hmc_smem));
+    if (occ < 1) return fail(SPEC_ECUDA, "hmc kernel cannot be resident");
+    if (occ > 2) occ = 2;
+    ctx->hmc_grid = occ * ctx->num_sms;
+    CK(zalloc(&ctx->hmc_scratch, (size_t)ctx->hmc_stride * ctx->hmc_grid));
+    return SPEC_OK;
+}
+
+static void launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
+    int grid = count_host < ctx->hmc_grid ? count_host : ctx->hmc_grid;
+    if (grid < 1) grid = 1;
+    P.scratch = ctx->hmc_scratch;
+    P.scratch_stride = ctx->hmc_stride;
+    hmc_kernel<512><<<grid, 512, ctx->hmc_smem, ctx->stream>>>(P);
+    ctx->launches++;
+}
+
 static NormalParams normal_params(spec_ctx* ctx, int mode) {
     NormalParams Q;
     memset(&Q, 0, sizeof(Q));
@@ -343,6 +383,8 @@ static NormalParams normal_params(spec_ctx* ctx, int mode) {
     Q.Gn = b.Gn; Q.V = b.V; Q.X = b.X; Q.Xs = b.Xs; Q.AX = b.AX; Q.AXs = b.AXs; Q.ell = b.ell;
     Q.steps_done = b.steps_done; Q.refl = b.refl; Q.bound = b.bound; Q.flags = b.flags; Q.ndeg = b.ndeg;
     Q.amax = ctx->amax;
+    Q.cvec = ctx->c;
+    Q.tlast = b.tlast;
     Q.ball_c = ctx->ball_c; Q.ball_r = ctx->ball_r;
     return Q;
 }
@@ -350,7 +392,7 @@ static NormalParams normal_params(spec_ctx* ctx, int mode) {
 // ---------------------------------------------------------------- boundary_oracle
 static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const double* dv, const double* du,
                        double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
-                       bool host_out, int* status_out) {
+                       bool host_out, int* status_out, double hmcT = 0.0) {
     ChainBuf& b = ctx->cb;
     const int B = (int)batch;
     const int n = ctx->n, np = ctx->np, m = ctx->m;
@@ -377,7 +419,12 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     ChordParams P = chord_params(ctx, 1);
     P.count_host = B;
     P.o_tminus = o_tm; P.o_tplus = o_tp; P.o_kernel = o_ker; P.o_binding = o_bind; P.o_status = o_stat;
-    launch_chord(ctx, P, B);
+    if (hmcT > 0.0) {
+        P.Temp = hmcT;
+        launch_hmc(ctx, P, B);
+    } else {
+        launch_chord(ctx, P, B);
+    }
     // K3 normal contraction for every line (non-dense rows are ignored by K4)
     launch_gemm_normal(ctx, nullptr, nullptr, B);
     NormalParams Q = normal_params(ctx, 1);
@@ -405,7 +452,7 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
 
 static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
                         double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
-                        bool host) {
+                        bool host, double hmcT = 0.0) {
     if (!ctx) return fail(SPEC_EINVAL, "null ctx");
     if (batch < 0 || batch > (1LL << 30)) return fail(SPEC_EINVAL, "bad batch");
     if (batch == 0) return SPEC_OK;
@@ -428,7 +475,12 @@ static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const dou
         dx = bx; dv = bv; du = bu;
     }
     int status = 0;
-    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status);
+    if (hmcT > 0.0) {
+        if (!ctx->has_obj) return fail(SPEC_EINVAL, "hmc_oracle needs spec_set_objective");
+        rc = ensure_hmc(ctx);
+        if (rc) return rc;
+    }
+    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status, hmcT);
     if (bx) cudaFree(bx);
     if (bv) cudaFree(bv);
     if (bu) cudaFree(bu);
@@ -440,6 +492,12 @@ static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const dou
 extern "C" int boundary_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
                                double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding) {
     return oracle_entry(ctx, batch, x, v, u, t_minus, t_plus, normal, kernel, binding, true);
+}
+extern "C" int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
+                          double T, double* t_plus, double* normal, double* kernel, int32_t* binding) {
+    if (!(T > 0.0)) return fail(SPEC_EINVAL, "T must be > 0");
+    std::vector<double> tm((size_t)(batch > 0 ? batch : 1));
+    return oracle_entry(ctx, batch, x, v, u, tm.data(), t_plus, normal, kernel, binding, true, T);
 }
 extern "C" int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const double* v,
                                    const double* u, double* t_minus, double* t_plus, double* normal,
@@ -522,6 +580,7 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     P.tag = p->tag;
     P.chain_base = p->chain_begin;
     P.gid = dgid;
+    P.Temp = p->T;
     NormalParams& Q = W.Q;
     Q = normal_params(ctx, 0);
     Q.steps_total = (int)p->steps;
@@ -530,6 +589,8 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     Q.tag = p->tag;
     Q.chain_base = p->chain_begin;
     Q.gid = dgid;
+    Q.kind = p->kind;
+    Q.Tinv = (p->kind == SPEC_WALK_HMC) ? 1.0 / p->T : 0.0;
     if (tr) {
         P.max_trace = tr->max_trace; P.tr_cnt = tr->cnt; P.tr_hit = tr->hit; P.tr_t = tr->t; P.tr_w = tr->w;
         P.tr_v = tr->v; P.tr_bind = tr->bind;
@@ -571,7 +632,8 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             P.list = list;
             P.count_dev = b.counters;
             P.count_host = count;
-            launch_chord(ctx, P, count);  // K2
+            if (W.p.kind == SPEC_WALK_HMC) launch_hmc(ctx, P, count);  // K5
+            else launch_chord(ctx, P, count);                         // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
             launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
             if (e) CK(cudaEventRecord(e[3], ctx->stream));
@@ -670,7 +732,14 @@ static int run_walk(spec_ctx* ctx, const spec_walk_params* p, const double* dx0,
 
 static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
-    if (p->kind != SPEC_WALK_BILLIARD) return fail(SPEC_EINVAL, "walk kind not supported by this build");
+    if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC) return fail(SPEC_EINVAL, "unknown walk kind");
+    if (p->kind == SPEC_WALK_HMC) {
+        if (!ctx->has_obj) return fail(SPEC_EINVAL, "HMC needs spec_set_objective");
+        if (!(p->T > 0.0) || !std::isfinite(p->T)) return fail(SPEC_EINVAL, "HMC needs T > 0");
+        if (ctx->has_ball) return fail(SPEC_EINVAL, "HMC with a ball constraint is not supported");
+        int rc = ensure_hmc(ctx);
+        if (rc) return rc;
+    }
     if (p->chains < 1 || p->chains > (1LL << 30)) return fail(SPEC_EINVAL, "chains out of range");
     if (p->steps < 0 || p->steps > (1LL << 31) - 1) return fail(SPEC_EINVAL, "steps out of range");
     if (!(p->L > 0.0) || !std::isfinite(p->L)) return fail(SPEC_EINVAL, "L must be > 0");

@@ -43,6 +43,11 @@ struct NormalParams {
     int* tr_cnt;
     double* tr_w;
     double* tr_v;
+    // HMC-r: velocity at the hit u = v - (c/T) t+ before the reflection
+    int kind;
+    const double* cvec;
+    double Tinv;
+    const double* tlast;
 };
 
 // One warp per chain.  Walk: w = -g/|g| (outward, lemma:gradient P:752-764,
@@ -125,9 +130,19 @@ __global__ void __launch_bounds__(256) normal_reflect_kernel(NormalParams P) {
             if (sd < P.steps_total) {
                 long long gidv = P.gid ? P.gid[slot] : P.chain_base + slot;
                 step_start<false>(T, slot, gidv, sd, P.n, P.np, P.mt, P.mtp, P.V, P.X, (double*)P.Xs, P.AX, P.AXs,
-                                  P.ell, P.Lpar, P.seed, P.tag, 0, red);
+                                  P.ell, P.Lpar, P.seed, P.tag, P.kind, red);
             }
             continue;
+        }
+        if (P.kind == 1) {  // HMC: reflect the velocity at the hit, u = v - (c/T) t+
+            const double tl = P.tlast[slot];
+            gv = 0.0;
+            for (int i = lane; i < P.n; i += 32) {
+                double u = v[i] - P.cvec[i] * P.Tinv * tl;
+                v[i] = u;
+                gv += g[i] * u;
+            }
+            gv = warp_sum(gv);
         }
         // w = -g/|g|; v <- v - 2 <v,w> w = v - 2 (g.v / |g|^2) g
         double f = 2.0 * gv / gg;
