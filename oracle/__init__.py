@@ -311,3 +311,125 @@ def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho:
 def ball_volume(n: int, r: float = 1.0) -> float:
     """omega_n r^n = pi^(n/2) / Gamma(n/2+1) r^n."""
     return math.exp(0.5 * n * math.log(math.pi) - math.lgamma(0.5 * n + 1) + n * math.log(r))
+
+
+# ---------------------------------------------------------------------------
+# Estimators (SURVEY 8(c).1 O8, O9) -- orchestration over the C oracle
+# ---------------------------------------------------------------------------
+PURPOSE_VOLUME, PURPOSE_PILOT = 1, 3
+
+
+def vol_tag(purpose: int, phase: int, ball: bool, attempt: int = 0) -> int:
+    """Philox counter word 3: purpose in bits 28-31, (attempt, phase, walk/ball) below."""
+    return (purpose << 28) | (attempt << 20) | (phase << 1) | (1 if ball else 0)
+
+
+def ball_samples(seed: int, tag: int, begin: int, count: int, n: int, c0, r: float) -> np.ndarray:
+    """Exact uniform samples of B(c0, r): x = c0 + r eta^(1/n) g/|g| with the step-draw
+    layout of O7 (g from blocks 0..ceil(n/2)-1, eta from block ceil(n/2)), sample j at
+    counter (block, step 0, chain j, tag)."""
+    X = np.empty((count, n))
+    for k in range(count):
+        g, eta = step_draws(seed, tag, begin + k, 0, n)
+        X[k] = np.asarray(c0) + r * eta ** (1.0 / n) * g / np.linalg.norm(g)
+    return X
+
+
+def volume(inst, eps: float, seed: int, N: int, W: int = 10, burn: int = 40, L: float = None, rho: int = None,
+           rho_star: float = 0.325, q_stop: float = 0.25, max_phases: int = 64, max_growth: int = 16,
+           nthreads: int = 0) -> dict:
+    """Ball-phase multiphase Monte Carlo volume (eq:mmc_vol P:1291-1300, telescoping
+    product P:1246-1259; schedule = DESIGN.md readings R11-R14):
+
+    pilot   : S_0 = S; billiard samples of S_i (phase 0 burned in from c0 = 0);
+              r_{i+1} = rho*-quantile of |x - c0|; stop once q(r_{i+1}) =
+              P_{U(B(r_{i+1}))}[x in S] >= q_stop (exact ball sampling + membership).
+    estimate: fresh walks of S_i = S cap B(r_i), warm-started from the previous
+              phase's points inside B(r_i) (resampled in chain order);
+              rho_i = #{|x - c0| <= r_{i+1}} / N;  q = membership fraction of N
+              exact samples of B(r_k);  vol = omega_n r_k^n q / prod rho_i.
+    sigma_rel^2 = sum (1 - rho)/(N rho) + (1 - q)/(N q); N doubles (fresh tags)
+    until sigma_rel <= eps/2 or N reaches max_growth * N."""
+    n = inst.n
+    L = 2.0 * math.sqrt(n) if L is None else L
+    rho = 10 * n if rho is None else rho
+    c0 = np.zeros(n)
+    full = Lmi(inst)
+
+    def walk_phase(r, X0, steps, tag, count):
+        lmi = full if r is None else Lmi(inst, ball_c=c0, ball_r=r)
+        X, st = walk(lmi, BILLIARD, seed, 0, count, steps, L, rho, x0=X0, tag=tag, nthreads=nthreads)
+        return X, st
+
+    def q_of(r, tag, count):
+        B = ball_samples(seed, tag, 0, count, n, c0, r)
+        return float(np.mean([membership(full, b) for b in B]))
+
+    def resample(X, r, count):
+        # strictly inside B(r): the pilot's quantile point itself lies on the sphere
+        inside = X[np.linalg.norm(X - c0, axis=1) < r]
+        idx = np.arange(count) % len(inside)
+        return inside[idx]
+
+    calls = 0
+    # ---- pilot: radii
+    radii = [None]
+    X = np.zeros((N, n))
+    X, st = walk_phase(None, X, burn, vol_tag(PURPOSE_PILOT, 0, False), N)
+    calls += st["calls"]
+    burned = X.copy()
+    qs = []
+    for i in range(max_phases):
+        d = np.sort(np.linalg.norm(X - c0, axis=1))
+        r_next = float(d[max(0, int(math.ceil(rho_star * N)) - 1)])
+        q = q_of(r_next, vol_tag(PURPOSE_PILOT, i, True), N)
+        radii.append(r_next)
+        qs.append(q)
+        if q >= q_stop:
+            break
+        X, st = walk_phase(r_next, resample(X, r_next, N), W, vol_tag(PURPOSE_PILOT, i + 1, False), N)
+        calls += st["calls"]
+    k = len(radii) - 1
+    # ---- estimation
+    attempt, Ne = 0, N
+    while True:
+        X = burned if Ne == N else burned[np.arange(Ne) % N]
+        ratios = []
+        for i in range(k):
+            X, st = walk_phase(radii[i], X, W, vol_tag(PURPOSE_VOLUME, i, False, attempt), Ne)
+            calls += st["calls"]
+            inside = np.linalg.norm(X - c0, axis=1) <= radii[i + 1]
+            ratios.append(float(np.mean(inside)))
+            X = resample(X, radii[i + 1], Ne)
+        q = q_of(radii[k], vol_tag(PURPOSE_VOLUME, k, True, attempt), Ne)
+        ratios_a = np.array(ratios)
+        var = float(np.sum((1 - ratios_a) / (Ne * ratios_a)) + (1 - q) / (Ne * q))
+        sig = math.sqrt(var)
+        if sig <= eps / 2 or Ne >= max_growth * N:
+            break
+        attempt += 1
+        Ne *= 2
+    logv = math.log(ball_volume(n, radii[k])) + math.log(q) - float(np.sum(np.log(ratios_a)))
+    return dict(volume=math.exp(logv), log_volume=logv, std_rel=sig, phases=k, radii=radii[1:],
+                ratios=ratios, q=q, chains=Ne, calls=calls)
+
+
+def expectation(inst, f_id: str, seed: int, chains: int, steps: int, L: float, rho: int, T: float = None,
+                c=None, b1: float = None, b2: float = None, nthreads: int = 0) -> dict:
+    """E[f] over the chains' end points (reading R18): uniform law by the
+    billiard walk (T is None) or exp(-c.x/T) by HMC-r.  f in {"linear_c": c.x,
+    "sqnorm": |x|^2, "halfspace_union": 1(c.x <= b1 or c.x >= b2) (P:1355-1358)}.
+    stderr = sample sd / sqrt(chains) (O9)."""
+    lmi = Lmi(inst)
+    kind = BILLIARD if T is None else HMC
+    X, st = walk(lmi, kind, seed, 0, chains, steps, L, rho, T=1.0 if T is None else T, c=c, nthreads=nthreads)
+    if f_id == "linear_c":
+        vals = X @ np.asarray(c)
+    elif f_id == "sqnorm":
+        vals = np.sum(X * X, axis=1)
+    elif f_id == "halfspace_union":
+        cx = X @ np.asarray(c)
+        vals = ((cx <= b1) | (cx >= b2)).astype(float)
+    else:
+        raise ValueError(f_id)
+    return dict(est=float(vals.mean()), stderr=float(vals.std(ddof=1) / math.sqrt(chains)), calls=st["calls"])
