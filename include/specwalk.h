@@ -176,6 +176,68 @@ int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st);
 int spec_kernel_timing(spec_ctx* ctx, int enable);
 int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items);
 
+/* ---- estimators ----
+ * Multi-rank: spec_set_comm installs an allgather of equal HOST shards in rank
+ * order (e.g. torch.distributed over NCCL); chains are split into contiguous
+ * global-id ranges, every reduction is an ordered sum over global chain ids,
+ * so results are identical for any world size.  NULL = single rank. */
+typedef struct spec_comm {
+    void* user;
+    int rank, world;
+    int (*allgather_f64)(void* user, const double* in, int64_t n_local, double* out /* world*n_local */);
+} spec_comm;
+int spec_set_comm(spec_ctx* ctx, const spec_comm* comm);
+
+/* volume -- ball-phase multiphase Monte Carlo (eq:mmc_vol P:1291-1300, the
+ * telescoping ratio estimator P:1246-1259, schedule: DESIGN.md R11-R14):
+ * c0 = origin (must be interior).  Pilot: burned-in billiard samples of
+ * S_0 = S; r_{i+1} = rho_star-quantile of |x - c0| over the samples of
+ * S_i = S cap B(c0, r_i); stop when q(r) = P_{U(B(r))}[x in S] >= q_stop
+ * (exact ball sampling + MEMBERSHIP, Alg. 1).  Estimation: fresh walks of each
+ * S_i warm-started from the previous phase's points inside B(r_i), ratio
+ * rho_i = #{|x - c0| <= r_{i+1}} / N, q by N exact ball samples;
+ * vol = omega_n r_k^n q / prod rho_i.  N doubles (fresh randomness) until the
+ * binomial sigma_rel <= eps / 2 or N = max_growth * chains_per_phase.
+ * chains_per_phase: global N (divisible by the world size).  opts may be NULL
+ * (defaults in brackets).  EINVAL: eps outside (0,1); ERUNTIME: an empty phase. */
+#define SPEC_MAX_PHASES 64
+typedef struct spec_volume_opts {
+    int64_t walk_len; /* billiard steps per phase [10] */
+    int64_t burn;     /* phase-0 burn-in steps from c0 [40] */
+    double L;         /* billiard tau [2 sqrt(n)] */
+    int64_t rho;      /* reflection bound [10 n] */
+    double rho_star;  /* pilot quantile level [0.325] */
+    double q_stop;    /* stop threshold on q(r) [0.25] */
+    int max_phases;   /* [64] */
+    int max_growth;   /* [16] */
+} spec_volume_opts;
+typedef struct spec_volume_report {
+    double volume, log_volume, std_rel, q;
+    int phases;
+    int64_t chains; /* N of the accepted estimation round */
+    int64_t calls;  /* boundary-oracle calls of all walks (all ranks) */
+    double device_ms;
+    double radii[SPEC_MAX_PHASES];
+    double ratios[SPEC_MAX_PHASES];
+} spec_volume_report;
+int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_per_phase, const spec_volume_opts* opts,
+           spec_volume_report* out);
+
+/* expectation -- E[f] over the end points of p->chains independent chains
+ * (P:1326-1334): uniform law by the billiard walk if T <= 0 or T = +inf, the
+ * Boltzmann law exp(-c^T x / T) by HMC-r otherwise.  f: SPEC_F_LINEAR_C c^T x,
+ * SPEC_F_SQNORM |x|^2, SPEC_F_HALFSPACE_UNION 1(c^T x <= b1 or c^T x >= b2)
+ * (P:1355-1358).  est = mean, stderr = sample sd / sqrt(chains). */
+enum { SPEC_F_LINEAR_C = 0, SPEC_F_SQNORM = 1, SPEC_F_HALFSPACE_UNION = 2 };
+typedef struct spec_expect_params {
+    int64_t chains, steps;
+    double L;
+    int64_t rho;
+    double b1, b2;
+} spec_expect_params;
+int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, const spec_expect_params* p, double* est,
+                double* stderr_out);
+
 /* Make the host wait for all work queued on the context stream. */
 int spec_sync(spec_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers timing with events. */

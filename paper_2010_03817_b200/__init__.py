@@ -34,8 +34,32 @@ EXPORTS = (
     "spec_last_error", "spec_create", "spec_destroy", "spec_set_objective", "spec_set_ball", "boundary_oracle",
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
-    "spec_kernel_times", "hmc_oracle",
+    "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation",
 )
+F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
+MAX_PHASES = 64
+
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double))
+
+
+class Comm(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("rank", C.c_int), ("world", C.c_int), ("allgather_f64", ALLGATHER_FN)]
+
+
+class VolumeOpts(C.Structure):
+    _fields_ = [("walk_len", C.c_int64), ("burn", C.c_int64), ("L", C.c_double), ("rho", C.c_int64),
+                ("rho_star", C.c_double), ("q_stop", C.c_double), ("max_phases", C.c_int), ("max_growth", C.c_int)]
+
+
+class VolumeReport(C.Structure):
+    _fields_ = [("volume", C.c_double), ("log_volume", C.c_double), ("std_rel", C.c_double), ("q", C.c_double),
+                ("phases", C.c_int), ("chains", C.c_int64), ("calls", C.c_int64), ("device_ms", C.c_double),
+                ("radii", C.c_double * MAX_PHASES), ("ratios", C.c_double * MAX_PHASES)]
+
+
+class ExpectParams(C.Structure):
+    _fields_ = [("chains", C.c_int64), ("steps", C.c_int64), ("L", C.c_double), ("rho", C.c_int64),
+                ("b1", C.c_double), ("b2", C.c_double)]
 
 
 class SpecError(RuntimeError):
@@ -99,6 +123,10 @@ def load(build_if_missing: bool = True):
     l.spec_kernel_timing.argtypes = [C.c_void_p, C.c_int]
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
+    l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
+    l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
+                         C.POINTER(VolumeReport)]
+    l.expectation.argtypes = [C.c_void_p, C.c_int, C.c_double, C.c_uint64, C.POINTER(ExpectParams), _dp, _dp]
     _lib = l
     return l
 
@@ -148,6 +176,47 @@ class Spectrahedron:
 
     def set_ball(self, center, radius: float):
         _check(_lib.spec_set_ball(self._h, _p(_f64(center)) if center is not None else None, float(radius)))
+
+    def set_comm(self, allgather, rank: int, world: int):
+        """Multi-rank reductions: allgather(local: np.ndarray) -> np.ndarray (rank order).
+        None removes it (single rank)."""
+        if allgather is None:
+            self._comm_keep = None
+            _check(_lib.spec_set_comm(self._h, None))
+            return
+
+        def cb(user, inp, n_local, out):
+            try:
+                loc = np.ctypeslib.as_array(inp, shape=(n_local,)).copy()
+                glob = np.asarray(allgather(loc), dtype=np.float64).reshape(-1)
+                np.ctypeslib.as_array(out, shape=(n_local * world,))[:] = glob
+                return 0
+            except Exception:  # pragma: no cover - surfaced as ECUDA by the library
+                return 1
+
+        fn = ALLGATHER_FN(cb)
+        comm = Comm(None, rank, world, fn)
+        self._comm_keep = (fn, comm)
+        _check(_lib.spec_set_comm(self._h, C.byref(comm)))
+
+    def volume(self, eps: float, seed: int, chains_per_phase: int, walk_len: int = 0, burn: int = 0,
+               L: float = 0.0, rho: int = 0, rho_star: float = 0.0, q_stop: float = 0.0, max_phases: int = 0,
+               max_growth: int = 0) -> dict:
+        """Ball-phase MMC volume (eq:mmc_vol P:1291-1300)."""
+        o = VolumeOpts(walk_len, burn, float(L), rho, float(rho_star), float(q_stop), max_phases, max_growth)
+        r = VolumeReport()
+        _check(_lib.volume(self._h, float(eps), seed, chains_per_phase, C.byref(o), C.byref(r)))
+        k = r.phases
+        return dict(volume=r.volume, log_volume=r.log_volume, std_rel=r.std_rel, q=r.q, phases=k, chains=r.chains,
+                    calls=r.calls, device_ms=r.device_ms, radii=list(r.radii[:k]), ratios=list(r.ratios[:k]))
+
+    def expectation(self, f_id: int, T: float, seed: int, chains: int, steps: int, L: float, rho: int,
+                    b1: float = 0.0, b2: float = 0.0) -> dict:
+        """E[f] over chain end points; T <= 0 or inf: uniform (billiard)."""
+        p = ExpectParams(chains, steps, float(L), rho, float(b1), float(b2))
+        est, se = C.c_double(), C.c_double()
+        _check(_lib.expectation(self._h, f_id, float(T), seed, C.byref(p), C.byref(est), C.byref(se)))
+        return dict(est=est.value, stderr=se.value)
 
     def kernel_launches(self) -> int:
         return int(_lib.spec_kernel_launches(self._h))

@@ -20,6 +20,8 @@
 #include "walk.cuh"
 #include "chord2.cuh"
 #include "hmc.cuh"
+#include "estimators.cuh"
+#include <algorithm>
 
 using namespace sw;
 
@@ -87,6 +89,8 @@ struct spec_ctx {
     long long launches = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     void* walk = nullptr;  // WalkRun*
+    spec_comm comm{nullptr, 0, 1, nullptr};
+    int has_comm = 0;
 };
 
 static void free_chains(ChainBuf& b) {
@@ -730,6 +734,7 @@ static int run_walk(spec_ctx* ctx, const spec_walk_params* p, const double* dx0,
     return rc;
 }
 
+static int gather_f64(spec_ctx* ctx, const std::vector<double>& local, std::vector<double>& global);
 static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
     if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC) return fail(SPEC_EINVAL, "unknown walk kind");
@@ -768,18 +773,33 @@ static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0
     if (dx0) cudaFree(dx0);
     if (rc) return rc;
     if (st) *st = local;
-    // outputs
+    // outputs: end-point moments as chunk partials (1024 consecutive global chain ids
+    // per chunk, chain order), gathered over ranks and summed in global chunk order
     ChainBuf& b = ctx->cb;
-    double *dsx = nullptr, *dsxx = nullptr;
     const int nxx = n * (n + 1) / 2;
+    if ((sum_x || sum_xx) && ctx->has_comm && (C % 1024 || p->chain_begin % 1024))
+        return fail(SPEC_EINVAL, "multi-rank moments need shards of multiples of 1024 chains");
     if (sum_x || sum_xx) {
-        CK(cudaMalloc(&dsx, sizeof(double) * n));
-        CK(cudaMalloc(&dsxx, sizeof(double) * nxx));
-        moments_kernel<<<std::min((n + nxx + 127) / 128, 4096), 128, 0, ctx->stream>>>(b.X, np, n, C, dsx, dsxx);
+        const int CH = 1024;
+        const int nchunk = (C + CH - 1) / CH;
+        const int stride = n + nxx;
+        double* dpart;
+        CK(cudaMalloc(&dpart, sizeof(double) * (size_t)nchunk * stride));
+        moments_chunk_kernel<<<std::min((nchunk * stride + 255) / 256, 8192), 256, 0, ctx->stream>>>(
+            b.X, np, n, C, CH, dpart);
         ctx->launches++;
-        cudaMemcpyKind k = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-        if (sum_x) CK(cudaMemcpyAsync(sum_x, dsx, sizeof(double) * n, k, ctx->stream));
-        if (sum_xx) CK(cudaMemcpyAsync(sum_xx, dsxx, sizeof(double) * nxx, k, ctx->stream));
+        std::vector<double> part((size_t)nchunk * stride), allp;
+        CK(cudaMemcpyAsync(part.data(), dpart, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dpart);
+        rc = gather_f64(ctx, part, allp);
+        if (rc) return rc;
+        std::vector<double> acc(allp.begin(), allp.begin() + stride);
+        for (size_t k = 1; k < allp.size() / stride; ++k)
+            for (int q = 0; q < stride; ++q) acc[q] += allp[k * stride + q];
+        cudaMemcpyKind kk = host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
+        if (sum_x) CK(cudaMemcpy(sum_x, acc.data(), sizeof(double) * n, kk));
+        if (sum_xx) CK(cudaMemcpy(sum_xx, acc.data() + n, sizeof(double) * nxx, kk));
     }
     if (final_x) {
         if (host) {
@@ -795,8 +815,6 @@ static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0
         ctx->launches++;
     }
     CK(cudaStreamSynchronize(ctx->stream));
-    if (dsx) cudaFree(dsx);
-    if (dsxx) cudaFree(dsxx);
     if (local.failures > 0)
         return fail(SPEC_EPRECOND, std::to_string(local.failures) + " chain(s) started outside int S");
     return SPEC_OK;
@@ -928,4 +946,298 @@ extern "C" int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4,
 extern "C" int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st) {
     if (!ctx || !walk_run(ctx).active) return fail(SPEC_EINVAL, "no walk in progress");
     return walk_collect_stats(ctx, st);
+}
+
+// ---------------------------------------------------------------- multi-rank plumbing
+extern "C" int spec_set_comm(spec_ctx* ctx, const spec_comm* comm) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    if (!comm) {
+        ctx->has_comm = 0;
+        ctx->comm = spec_comm{nullptr, 0, 1, nullptr};
+        return SPEC_OK;
+    }
+    if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world || !comm->allgather_f64)
+        return fail(SPEC_EINVAL, "bad spec_comm");
+    ctx->comm = *comm;
+    ctx->has_comm = comm->world > 1;
+    return SPEC_OK;
+}
+
+// allgather of equal host shards in rank order (identity on one rank)
+static int gather_f64(spec_ctx* ctx, const std::vector<double>& local, std::vector<double>& global) {
+    const int W = ctx->has_comm ? ctx->comm.world : 1;
+    global.assign(local.size() * (size_t)W, 0.0);
+    if (W == 1) {
+        std::copy(local.begin(), local.end(), global.begin());
+        return SPEC_OK;
+    }
+    int rc = ctx->comm.allgather_f64(ctx->comm.user, local.data(), (int64_t)local.size(), global.data());
+    if (rc) return fail(SPEC_ECUDA, "allgather callback failed");
+    return SPEC_OK;
+}
+
+// ---------------------------------------------------------------- K6: ball sampling + membership
+static int ball_inside_count(spec_ctx* ctx, uint64_t seed, uint32_t tag, long long begin, int count,
+                             const double* c0_host, double r, long long* inside_out) {
+    ChainBuf& b = ctx->cb;
+    int rc = ensure_chains(ctx, count);
+    if (rc) return rc;
+    const int n = ctx->n, np = ctx->np, m = ctx->m;
+    double* dc0;
+    CK(cudaMalloc(&dc0, sizeof(double) * n));
+    CK(cudaMemcpyAsync(dc0, c0_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    ball_sample_kernel<<<(count + 7) / 8, 256, 0, ctx->stream>>>(count, begin, n, np, seed, tag, dc0, r, b.X);
+    ctx->launches++;
+    launch_gemm_av(ctx, b.X, nullptr, nullptr, count, b.AX, ctx->a0);  // A(x_j)
+    const int mp = roundup(m, 8);
+    const size_t smem = sizeof(double) * ((size_t)mp * ctx->ld + mp + 8);
+    const int NT = mp <= 64 ? 128 : 256;
+    if (NT == 128) {
+        CK(cudaFuncSetAttribute(membership_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        membership_kernel<128><<<std::min(count, ctx->num_sms * 8), 128, smem, ctx->stream>>>(
+            count, n, np, m, ctx->mt, ctx->mtp, ctx->ld, b.X, b.AX, ctx->has_cube ? ctx->lo : nullptr, ctx->hi,
+            b.steps_done);
+    } else {
+        CK(cudaFuncSetAttribute(membership_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        membership_kernel<256><<<std::min(count, ctx->num_sms * 2), 256, smem, ctx->stream>>>(
+            count, n, np, m, ctx->mt, ctx->mtp, ctx->ld, b.X, b.AX, ctx->has_cube ? ctx->lo : nullptr, ctx->hi,
+            b.steps_done);
+    }
+    ctx->launches++;
+    std::vector<int> flags(count);
+    CK(cudaMemcpyAsync(flags.data(), b.steps_done, sizeof(int) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaGetLastError());
+    cudaFree(dc0);
+    long long cnt = 0;
+    for (int v : flags) cnt += v;
+    *inside_out = cnt;
+    return SPEC_OK;
+}
+
+// ---------------------------------------------------------------- volume (ball-phase MMC)
+static uint32_t vol_tag(int purpose, int phase, bool ball, int attempt) {
+    return ((uint32_t)purpose << 28) | ((uint32_t)attempt << 20) | ((uint32_t)phase << 1) | (ball ? 1u : 0u);
+}
+
+static double log_ball_volume(int n, double r) {
+    return 0.5 * n * std::log(M_PI) - std::lgamma(0.5 * n + 1.0) + n * std::log(r);
+}
+
+extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_per_phase,
+                      const spec_volume_opts* o, spec_volume_report* out) {
+    if (!ctx || !out) return fail(SPEC_EINVAL, "null argument");
+    if (!(eps > 0.0 && eps < 1.0)) return fail(SPEC_EINVAL, "eps must be in (0,1)");
+    const int n = ctx->n;
+    spec_volume_opts opt;
+    opt.walk_len = 10; opt.burn = 40; opt.L = 2.0 * std::sqrt((double)n); opt.rho = 10 * n;
+    opt.rho_star = 0.325; opt.q_stop = 0.25; opt.max_phases = 64; opt.max_growth = 16;
+    if (o) {
+        if (o->walk_len > 0) opt.walk_len = o->walk_len;
+        if (o->burn > 0) opt.burn = o->burn;
+        if (o->L > 0) opt.L = o->L;
+        if (o->rho > 0) opt.rho = o->rho;
+        if (o->rho_star > 0) opt.rho_star = o->rho_star;
+        if (o->q_stop > 0) opt.q_stop = o->q_stop;
+        if (o->max_phases > 0) opt.max_phases = std::min(o->max_phases, (int)SPEC_MAX_PHASES);
+        if (o->max_growth > 0) opt.max_growth = o->max_growth;
+    }
+    const int W = ctx->has_comm ? ctx->comm.world : 1, R = ctx->has_comm ? ctx->comm.rank : 0;
+    const long long N = chains_per_phase;
+    if (N < 8 || N % W) return fail(SPEC_EINVAL, "chains_per_phase must be >= 8 and divisible by the world size");
+    CK(cudaSetDevice(ctx->dev));
+    std::vector<double> c0(n, 0.0);
+    long long calls = 0;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, ctx->stream));
+
+    auto walk_phase = [&](double r, const std::vector<double>& X0, long long Nt, long long steps, uint32_t tag,
+                          std::vector<double>& X) -> int {
+        const long long Cl = Nt / W, begin = (long long)R * Cl;
+        int rc2 = spec_set_ball(ctx, r > 0 ? c0.data() : nullptr, r > 0 ? r : 0.0);
+        if (rc2) return rc2;
+        spec_walk_params p;
+        p.kind = SPEC_WALK_BILLIARD; p.chain_begin = begin; p.chains = Cl; p.steps = steps; p.L = opt.L;
+        p.rho = opt.rho; p.seed = seed; p.tag = tag; p.T = 1.0;
+        X.assign((size_t)Cl * n, 0.0);
+        spec_walk_stats st;
+        rc2 = walk_entry(ctx, &p, X0.data(), 1, nullptr, nullptr, X.data(), &st, true);
+        calls += st.calls;
+        return rc2;
+    };
+    auto q_of = [&](double r, uint32_t tag, long long Nt, double* q) -> int {
+        const long long Cl = Nt / W, begin = (long long)R * Cl;
+        long long cnt = 0;
+        int rc2 = ball_inside_count(ctx, seed, tag, begin, (int)Cl, c0.data(), r, &cnt);
+        if (rc2) return rc2;
+        std::vector<double> loc(1, (double)cnt), glob;
+        rc2 = gather_f64(ctx, loc, glob);
+        if (rc2) return rc2;
+        double tot = 0.0;
+        for (double v : glob) tot += v;
+        *q = tot / (double)Nt;
+        return SPEC_OK;
+    };
+    auto norm = [&](const double* x) {
+        double s2 = 0.0;
+        for (int i = 0; i < n; ++i) s2 += (x[i] - c0[i]) * (x[i] - c0[i]);
+        return std::sqrt(s2);
+    };
+    // warm starts of this rank's chains [begin, begin + Cl) from the global points strictly inside B(r)
+    auto resample = [&](const std::vector<double>& Xg, double r, long long Nt, std::vector<double>& X0) -> int {
+        const long long Cl = Nt / W, begin = (long long)R * Cl;
+        std::vector<long long> inside;
+        const long long Ng = (long long)(Xg.size() / n);
+        for (long long j = 0; j < Ng; ++j)
+            if (norm(&Xg[(size_t)j * n]) < r) inside.push_back(j);
+        if (inside.empty()) return fail(SPEC_ERUNTIME, "no sample strictly inside the next ball");
+        X0.resize((size_t)Cl * n);
+        for (long long j = 0; j < Cl; ++j) {
+            long long src = inside[(size_t)((begin + j) % (long long)inside.size())];
+            std::copy(&Xg[(size_t)src * n], &Xg[(size_t)src * n] + n, &X0[(size_t)j * n]);
+        }
+        return SPEC_OK;
+    };
+
+    int rc = SPEC_OK;
+    std::vector<double> radii;  // r_1..r_k
+    std::vector<double> X, Xg, X0((size_t)(N / W) * n, 0.0), burned_g;
+    // ---- pilot
+    rc = walk_phase(-1.0, X0, N, opt.burn, vol_tag(3, 0, false, 0), X);
+    if (rc) return rc;
+    rc = gather_f64(ctx, X, burned_g);
+    if (rc) return rc;
+    Xg = burned_g;
+    for (int i = 0; i < opt.max_phases; ++i) {
+        std::vector<double> d((size_t)N);
+        for (long long j = 0; j < N; ++j) d[(size_t)j] = norm(&Xg[(size_t)j * n]);
+        std::sort(d.begin(), d.end());
+        long long qi = (long long)std::ceil(opt.rho_star * (double)N) - 1;
+        if (qi < 0) qi = 0;
+        const double r_next = d[(size_t)qi];
+        double q = 0.0;
+        rc = q_of(r_next, vol_tag(3, i, true, 0), N, &q);
+        if (rc) return rc;
+        radii.push_back(r_next);
+        if (q >= opt.q_stop) break;
+        rc = resample(Xg, r_next, N, X0);
+        if (rc) return rc;
+        rc = walk_phase(r_next, X0, N, opt.walk_len, vol_tag(3, i + 1, false, 0), X);
+        if (rc) return rc;
+        rc = gather_f64(ctx, X, Xg);
+        if (rc) return rc;
+    }
+    const int k = (int)radii.size();
+    // ---- estimation
+    int attempt = 0;
+    long long Ne = N;
+    std::vector<double> ratios;
+    double q = 0.0, sig = 0.0;
+    for (;;) {
+        const long long Cl = Ne / W, begin = (long long)R * Cl;
+        X0.resize((size_t)Cl * n);
+        for (long long j = 0; j < Cl; ++j) {
+            long long src = (begin + j) % N;
+            std::copy(&burned_g[(size_t)src * n], &burned_g[(size_t)src * n] + n, &X0[(size_t)j * n]);
+        }
+        ratios.clear();
+        for (int i = 0; i < k; ++i) {
+            rc = walk_phase(i == 0 ? -1.0 : radii[i - 1], X0, Ne, opt.walk_len, vol_tag(1, i, false, attempt), X);
+            if (rc) return rc;
+            rc = gather_f64(ctx, X, Xg);
+            if (rc) return rc;
+            long long in = 0;
+            for (long long j = 0; j < Ne; ++j) in += (norm(&Xg[(size_t)j * n]) <= radii[i]) ? 1 : 0;
+            ratios.push_back((double)in / (double)Ne);
+            if (in == 0) return fail(SPEC_ERUNTIME, "empty phase ratio");
+            rc = resample(Xg, radii[i], Ne, X0);
+            if (rc) return rc;
+        }
+        rc = q_of(radii[k - 1], vol_tag(1, k, true, attempt), Ne, &q);
+        if (rc) return rc;
+        if (!(q > 0.0)) return fail(SPEC_ERUNTIME, "no ball sample inside S");
+        double var = (1.0 - q) / ((double)Ne * q);
+        for (double rt : ratios) var += (1.0 - rt) / ((double)Ne * rt);
+        sig = std::sqrt(var);
+        if (sig <= eps / 2 || Ne >= (long long)opt.max_growth * N) break;
+        ++attempt;
+        Ne *= 2;
+    }
+    spec_set_ball(ctx, nullptr, 0.0);
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    double logv = log_ball_volume(n, radii[k - 1]) + std::log(q);
+    for (double rt : ratios) logv -= std::log(rt);
+    // calls summed over ranks
+    std::vector<double> cl(1, (double)calls), clg;
+    gather_f64(ctx, cl, clg);
+    double calls_tot = 0.0;
+    for (double v : clg) calls_tot += v;
+    memset(out, 0, sizeof(*out));
+    out->volume = std::exp(logv);
+    out->log_volume = logv;
+    out->std_rel = sig;
+    out->q = q;
+    out->phases = k;
+    out->chains = Ne;
+    out->calls = (int64_t)calls_tot;
+    out->device_ms = ms;
+    for (int i = 0; i < k; ++i) {
+        out->radii[i] = radii[i];
+        out->ratios[i] = ratios[i];
+    }
+    return SPEC_OK;
+}
+
+// ---------------------------------------------------------------- expectation
+extern "C" int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, const spec_expect_params* ep,
+                           double* est, double* stderr_out) {
+    if (!ctx || !ep || !est) return fail(SPEC_EINVAL, "null argument");
+    if (f_id < 0 || f_id > 2) return fail(SPEC_EINVAL, "unknown f_id");
+    if ((f_id == SPEC_F_LINEAR_C || f_id == SPEC_F_HALFSPACE_UNION) && !ctx->has_obj)
+        return fail(SPEC_EINVAL, "f needs the objective c (spec_set_objective)");
+    if (f_id == SPEC_F_HALFSPACE_UNION && !(ep->b2 > ep->b1)) return fail(SPEC_EINVAL, "need b2 > b1");
+    const int W = ctx->has_comm ? ctx->comm.world : 1, R = ctx->has_comm ? ctx->comm.rank : 0;
+    if (ep->chains < 2 || ep->chains % W) return fail(SPEC_EINVAL, "chains must be >= 2 and divisible by world");
+    const long long Cl = ep->chains / W;
+    spec_walk_params p;
+    const bool hmc = (T > 0.0) && std::isfinite(T);
+    p.kind = hmc ? SPEC_WALK_HMC : SPEC_WALK_BILLIARD;
+    p.chain_begin = (long long)R * Cl;
+    p.chains = Cl;
+    p.steps = ep->steps;
+    p.L = ep->L;
+    p.rho = ep->rho;
+    p.seed = seed;
+    p.tag = 0;
+    p.T = hmc ? T : 1.0;
+    spec_walk_stats st;
+    int rc = walk_entry(ctx, &p, nullptr, 0, nullptr, nullptr, nullptr, &st, true);
+    if (rc) return rc;
+    double* df;
+    CK(cudaMalloc(&df, sizeof(double) * Cl));
+    fvalue_kernel<<<(int)std::min<long long>((Cl + 7) / 8, 65535), 256, 0, ctx->stream>>>(
+        (int)Cl, ctx->n, ctx->np, ctx->cb.X, ctx->c, f_id, ep->b1, ep->b2, df);
+    ctx->launches++;
+    std::vector<double> fl((size_t)Cl), fg;
+    CK(cudaMemcpyAsync(fl.data(), df, sizeof(double) * Cl, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(df);
+    rc = gather_f64(ctx, fl, fg);
+    if (rc) return rc;
+    double s = 0.0;
+    for (double v : fg) s += v;  // global chain order: identical for any GPU count
+    const double Nd = (double)fg.size();
+    const double mean = s / Nd;
+    double ss = 0.0;
+    for (double v : fg) ss += (v - mean) * (v - mean);
+    *est = mean;
+    if (stderr_out) *stderr_out = std::sqrt(ss / (Nd - 1.0) / Nd);
+    return SPEC_OK;
 }

@@ -58,6 +58,7 @@ CASES = [
     ("rand_10_10", lambda: specgen.rand_cube(10, 10, 0)),
     ("rand_40_40", lambda: specgen.rand_cube(40, 40, 2)),
     ("rand_100_100", lambda: specgen.rand_cube(100, 100, 3)),
+    ("rand_200_200", lambda: specgen.rand_cube(200, 200, 4)),
     ("elliptope_20", lambda: specgen.elliptope(20)),
     ("mixed_binding_12_30", lambda: specgen.rand_cube(12, 30, 5, scale=1 / np.sqrt(12))),
     ("cube_dense_5", lambda: specgen.cube_dense(5)),
@@ -72,7 +73,7 @@ def test_boundary_oracle_interior_parity(name, make):
     import paper_2010_03817_b200 as sw
     inst = make()
     lmi = oracle.Lmi(inst)
-    count = 24 if inst.m >= 100 else 64
+    count = 6 if inst.m >= 200 else (24 if inst.m >= 100 else 64)
     xs, vs = _interior_batch(inst, lmi, count, seed=zlib.crc32(name.encode()) % 1000)
     refs = _oracle_refs(lmi, xs, vs)
     S = sw.Spectrahedron.from_instance(inst)
@@ -87,7 +88,7 @@ def test_boundary_oracle_interior_parity(name, make):
             assert abs(np.linalg.eigvalsh(F)[0]) <= 1e-12 * scale
 
 
-@pytest.mark.parametrize("name,make", CASES[:5], ids=[c[0] for c in CASES[:5]])
+@pytest.mark.parametrize("name,make", CASES[:6], ids=[c[0] for c in CASES[:6]])
 def test_boundary_oracle_boundary_start_parity(name, make):
     """Segments that start on the dense boundary (after a reflection): Schur deflation (R6)."""
     import paper_2010_03817_b200 as sw
@@ -95,7 +96,7 @@ def test_boundary_oracle_boundary_start_parity(name, make):
     lmi = oracle.Lmi(inst, cube=False)
     inst_nc = specgen.Instance(inst.name, inst.A)  # dense block only so every hit is dense
     n = inst.n
-    count = 16 if inst.m >= 100 else 48
+    count = 4 if inst.m >= 200 else (16 if inst.m >= 100 else 48)
     xs0, vs0 = _interior_batch(inst_nc, lmi, count, seed=7)
     hits, us, ss = [], [], []
     for k in range(count):
