@@ -122,13 +122,48 @@ __device__ __forceinline__ double block_min(const Team& T, double v, double* red
 
 // ---------------------------------------------------------------- dense LA on a CTA
 // unpack packed-lower P into full symmetric M (leading dimension ld)
+// (all loads of a thread are issued before its stores: one global round trip)
 __device__ __forceinline__ void unpack_sym(const Team& T, const double* __restrict__ P, double* M, int m, int ld) {
-    for (int i = T.warp; i < m; i += T.nwarps) {
-        const double* row = P + pk(i, 0);
-        for (int j = T.lane; j <= i; j += 32) {
-            double v = row[j];
-            M[i * ld + j] = v;
-            M[j * ld + i] = v;
+    const int mt = m * (m + 1) / 2;
+    constexpr int K = 16;
+    for (int e0 = 0; e0 < mt; e0 += K * T.nthr) {
+        double val[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int e = e0 + k * T.nthr + T.tid;
+            val[k] = (e < mt) ? __ldg(P + e) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int e = e0 + k * T.nthr + T.tid;
+            if (e < mt) {
+                int i = (int)((sqrt(8.0 * (double)e + 1.0) - 1.0) * 0.5);
+                if (pk(i + 1, 0) <= e) ++i;
+                if (pk(i, 0) > e) --i;
+                int j = e - pk(i, 0);
+                M[i * ld + j] = val[k];
+                M[j * ld + i] = val[k];
+            }
+        }
+    }
+}
+
+// ax += th * av over the packed vector, loads issued before stores
+__device__ __forceinline__ void packed_axpy(const Team& T, double* ax, const double* __restrict__ av, double th,
+                                            int mt) {
+    constexpr int K = 8;
+    for (int e0 = 0; e0 < mt; e0 += K * T.nthr) {
+        double a[K], b[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int e = e0 + k * T.nthr + T.tid;
+            a[k] = (e < mt) ? ax[e] : 0.0;
+            b[k] = (e < mt) ? __ldg(av + e) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            int e = e0 + k * T.nthr + T.tid;
+            if (e < mt) ax[e] = a[k] + th * b[k];
         }
     }
 }

@@ -40,6 +40,60 @@ __device__ __forceinline__ void tile_msub(double (&acc)[2], const double* A, int
     }
 }
 
+// X <- H X H and Y <- H Y H together (H = I - beta h h^T, X, Y symmetric m x m)
+__device__ void householder_congruence2(const Team& T, double* X, double* Y, int m, int ld, const double* h,
+                                        double beta, double* px, double* py, double* red) {
+    for (int i = T.warp; i < m; i += T.nwarps) {
+        double sx = 0.0, sy = 0.0;
+        for (int j = T.lane; j < m; j += 32) {
+            const double hj = h[j];
+            sx += X[i * ld + j] * hj;
+            sy += Y[i * ld + j] * hj;
+        }
+        sx = warp_sum(sx);
+        sy = warp_sum(sy);
+        if (T.lane == 0) {
+            px[i] = beta * sx;
+            py[i] = beta * sy;
+        }
+    }
+    __syncthreads();
+    double hx = 0.0, hy = 0.0;
+    for (int i = T.tid; i < m; i += T.nthr) {
+        hx += h[i] * px[i];
+        hy += h[i] * py[i];
+    }
+    hx = warp_sum(hx);
+    hy = warp_sum(hy);
+    if (T.lane == 0) {
+        red[T.warp] = hx;
+        red[32 + T.warp] = hy;
+    }
+    __syncthreads();
+    double Kx = 0.0, Ky = 0.0;
+    for (int w = 0; w < T.nwarps; ++w) {
+        Kx += red[w];
+        Ky += red[32 + w];
+    }
+    Kx *= 0.5 * beta;
+    Ky *= 0.5 * beta;
+    __syncthreads();
+    for (int i = T.tid; i < m; i += T.nthr) {
+        px[i] -= Kx * h[i];
+        py[i] -= Ky * h[i];
+    }
+    __syncthreads();
+    for (int i = T.warp; i < m; i += T.nwarps) {
+        const double hi = h[i], pxi = px[i], pyi = py[i];
+        for (int j = T.lane; j < m; j += 32) {
+            const double hj = h[j];
+            X[i * ld + j] -= hi * px[j] + pxi * hj;
+            Y[i * ld + j] -= hi * py[j] + pyi * hj;
+        }
+    }
+    __syncthreads();
+}
+
 // blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8)
 __device__ bool cholesky_blocked(const Team& T, double* G, int n, int ld, double* rdiag, int* flag) {
     const int TB = n >> 3;
@@ -47,24 +101,35 @@ __device__ bool cholesky_blocked(const Team& T, double* G, int n, int ld, double
         const int k0 = kb * 8;
         double* D = G + k0 * ld + k0;
         if (T.warp == 0) {
+            // 8x8 diagonal block in registers: lane r < 8 holds row r (lower part)
+            double a[8];
+            const int r = T.lane;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[c] = (r < 8 && c <= r) ? D[r * ld + c] : 0.0;
             bool ok = true;
+#pragma unroll
             for (int c = 0; c < 8; ++c) {
-                double d = D[c * ld + c];
-                if (!(d > 0.0)) { ok = false; break; }
-                double l = sqrt(d);
-                double il = 1.0 / l;
-                __syncwarp();
-                if (T.lane > c && T.lane < 8) D[T.lane * ld + c] *= il;
-                if (T.lane == 0) {
-                    D[c * ld + c] = l;
-                    rdiag[k0 + c] = il;
+                const double d = __shfl_sync(0xffffffffu, a[c], c);
+                if (!(d > 0.0)) ok = false;
+                const double l = sqrt(fmax(d, 1e-300));
+                const double il = 1.0 / l;
+                if (r == c) a[c] = l;
+                else if (r > c) a[c] *= il;
+#pragma unroll
+                for (int k = c + 1; k < 8; ++k) {
+                    const double lkc = __shfl_sync(0xffffffffu, a[c], k);
+                    if (r >= k) a[k] -= a[c] * lkc;
                 }
-                __syncwarp();
-                for (int p = T.lane; p < 64; p += 32) {
-                    int i = p >> 3, j = p & 7;
-                    if (j > c && j <= i) D[i * ld + j] -= D[i * ld + c] * D[j * ld + c];
-                }
-                __syncwarp();
+            }
+            if (r < 8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c <= r) D[r * ld + c] = a[c];
+                double dg = a[0];
+#pragma unroll
+                for (int c = 1; c < 8; ++c)
+                    if (c == r) dg = a[c];
+                rdiag[k0 + r] = 1.0 / dg;
             }
             if (T.lane == 0) *flag = ok ? 0 : 1;
         }
@@ -408,21 +473,28 @@ __device__ double tri_twisted_vec(const Team& T, const double* al, const double*
     return fabs(beta_last) * fabs(s[J - 1]);
 }
 
-// Lanczos (full CGS2/DGKS reorthogonalisation) on the symmetric md x md matrix M
+// Lanczos (CGS with a DGKS second pass) on the symmetric md x md matrix M
 // (shared or global memory, leading dimension ld, zero padded to mdp).  Q holds
-// the basis (rows of length ld).  Convergence: residual beta_J |s_J| <= 1e-14 |T|
-// for the requested extreme Ritz pair(s) (top: sv, bottom: sv2), checked from
-// J = 0.45 md on, every 8 steps; Ritz values by Laguerre, vectors by a twisted
-// factorisation.  Returns J; theta_top / theta_bot set.
+// the orthonormal basis (rows of length ld).  Per iteration: (A) w' = M (w / beta)
+// (ping-pong buffers, q_j stored on the fly), (B) dots with q_0..q_j and |w'|^2,
+// (C) w' -= Q h with per-warp partial norms; a second pass (D, E) only when the
+// first cancelled more than half of |w'|^2.  3 barriers per iteration (5 with
+// the second pass).  Convergence: residual beta_J |s_J| <= 1e-14 |T| for the
+// requested extreme Ritz pair(s) (top: sv, bottom: sv2), checked from J =
+// 0.45 md on, every 8 steps; Ritz values by Laguerre, vectors by a twisted
+// factorisation.  wv must hold 2 (mdp + 8) doubles.  Returns J.
 __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, int mdp, int ld, bool need_top,
                            bool need_bot, double* wv, double* hb, double* al, double* be, double* sv, double* sv2,
                            double* dp, double* dm, double* red, int* sh_r, double* shd,
                            unsigned long long* prof, double* theta_top, double* theta_bot) {
     const int lrow = T.tid >> 2, lg = T.tid & 3;
     const int NT = T.nthr;
+    double* red2 = red + 16;  // per-warp partial norms (NT <= 512)
     *theta_top = -SW_INF;
     *theta_bot = SW_INF;
-    // start vector: fixed pseudo-random, zero padding
+    double* win = wv;
+    double* wout = wv + (mdp + 8);
+    // start vector: fixed pseudo-random, zero padding (w_{-1} = q_0, beta_{-1} = 1)
     double s0 = 0.0;
     for (int e = T.tid; e < mdp; e += T.nthr) {
         double val = 0.0;
@@ -430,54 +502,52 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
             double f = (double)e * 0.6180339887498949;
             val = 0.5 + (f - floor(f));
         }
-        Q[e] = val;
+        win[e] = val;
         s0 += val * val;
     }
     s0 = block_sum(T, s0, red);
-    {
-        double inv = 1.0 / sqrt(s0);
-        for (int e = T.tid; e < mdp; e += T.nthr) Q[e] *= inv;
-    }
-    __syncthreads();
+    double invb = 1.0 / sqrt(s0);
     const int jfirst = max(min(md, 12), (md * 9) / 20);
     int next_check = jfirst;
     double tnorm = 0.0;
     double th_prev = -SW_INF, res_prev = SW_INF;
     int J = 0;
     for (int j = 0; j < md; ++j) {
-        const double* qj = Q + (size_t)j * ld;
+        double* qj = Q + (size_t)j * ld;
         long long tl0 = clock64();
-        // ---- w = M q_j: 4 threads per row, interleaved columns
+        // ---- (A) q_j = w / beta stored; w' = M q_j: 4 threads per row, double2 columns
+        for (int e = T.tid; e < mdp; e += T.nthr) qj[e] = win[e] * invb;
         for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
             const int rw = r0 + lrow;
             double a0 = 0.0, a1 = 0.0;
             if (rw < mdp) {
                 const double* Mr = M + (size_t)rw * ld;
-                for (int c = lg; c < mdp; c += 8) {
-                    a0 += Mr[c] * qj[c];
-                    a1 += Mr[c + 4] * qj[c + 4];
+                for (int c = 2 * lg; c < mdp; c += 8) {
+                    double2 mv = *reinterpret_cast<const double2*>(Mr + c);
+                    double2 wq = *reinterpret_cast<const double2*>(win + c);
+                    a0 += mv.x * wq.x;
+                    a1 += mv.y * wq.y;
                 }
             }
             a0 += a1;
             a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
             a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-            if (lg == 0 && rw < mdp) wv[rw] = a0;
+            if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
         }
         __syncthreads();
         long long tl1 = clock64();
         long long tl2 = tl1, tl3 = tl1;
-        // ---- classical Gram-Schmidt against q_0..q_j, second pass only if
-        // the first one cancelled more than half of |w|^2 (DGKS).
+        // ---- (B..E) classical Gram-Schmidt against q_0..q_j
         double alpha = 0.0, nn = 0.0, nn_before = 0.0;
         for (int pass = 0; pass < 2; ++pass) {
-            const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w.w
+            const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w'.w'
             if (mdp <= 128) {
                 double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
                 const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
-                if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wv + i0);
-                if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wv + i1);
+                if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wout + i0);
+                if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wout + i1);
                 for (int i = T.warp; i < nrows; i += T.nwarps) {
-                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wv;
+                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
                     double sacc = 0.0;
                     if (i0 < mdp) {
                         double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
@@ -492,9 +562,9 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                 }
             } else {
                 for (int i = T.warp; i < nrows; i += T.nwarps) {
-                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wv;
+                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
                     double sacc = 0.0;
-                    for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wv[c];
+                    for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wout[c];
                     sacc = warp_sum(sacc);
                     if (T.lane == 0) hb[i] = sacc;
                 }
@@ -521,19 +591,23 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                     sa += __shfl_xor_sync(0xffffffffu, sa, 1);
                     sa += __shfl_xor_sync(0xffffffffu, sa, 2);
                     if (e < mdp) {
-                        double wn = wv[e] - sa;
+                        double wn = wout[e] - sa;
                         __syncwarp();
-                        if (g == 0) wv[e] = wn;
+                        if (g == 0) wout[e] = wn;
                         nloc += (g == 0) ? wn * wn : 0.0;
                     }
                 }
-                nn = block_sum(T, nloc, red);
+                nloc = warp_sum(nloc);
+                if (T.lane == 0) red2[T.warp] = nloc;
             }
+            __syncthreads();
+            nn = 0.0;
+            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
             if (pass == 0) tl3 = clock64();
             if (prof && T.tid == 0 && pass == 1) atomicAdd(&prof[15], 1ull);
             if (!(nn < 0.5 * nn_before)) break;
         }
-        double beta = sqrt(nn);
+        const double beta = sqrt(nn);
         if (T.tid == 0) {
             al[j] = alpha;
             be[j] = beta;
@@ -541,32 +615,28 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
         tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
         J = j + 1;
         const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
-        if (!exhausted) {
-            double inv = 1.0 / beta;
-            double* qn = Q + (size_t)(j + 1) * ld;
-            for (int e = T.tid; e < mdp; e += T.nthr) qn[e] = wv[e] * inv;
-        }
-        __syncthreads();
         if (prof && T.tid == 0) {
             long long tl4 = clock64();
             atomicAdd(&prof[12], (unsigned long long)(tl1 - tl0));
             atomicAdd(&prof[13], (unsigned long long)(tl2 - tl1));
             atomicAdd(&prof[14], (unsigned long long)(tl3 - tl2));
-            atomicAdd(&prof[8 + 8], (unsigned long long)(tl4 - tl3));
+            atomicAdd(&prof[16], (unsigned long long)(tl4 - tl3));
         }
+        // next iteration uses q_{j+1} = w' / beta
+        double* tmp = win;
+        win = wout;
+        wout = tmp;
+        invb = 1.0 / beta;
         if (exhausted || J >= next_check) {
+            __syncthreads();  // al/be of this step visible
             long long tc0 = clock64();
-            // top Ritz value of T_J (and bottom in oracle mode): CTA multisection
-            double glo = SW_INF, ghi = -SW_INF, amax = -SW_INF, amin = SW_INF;
+            double glo = SW_INF, ghi = -SW_INF;
             for (int i = T.tid; i < J; i += T.nthr) {
                 double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
                 glo = fmin(glo, al[i] - rsum);
                 ghi = fmax(ghi, al[i] + rsum);
-                amax = fmax(amax, al[i]);
-                amin = fmin(amin, al[i]);
             }
             ghi = block_max(T, ghi, red);
-            amax = block_max(T, amax, red);
             if (need_bot) glo = block_min(T, glo, red);
             if (T.tid == 0) shd[0] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
             if (need_bot && T.tid == 32) shd[1] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
@@ -591,6 +661,9 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
             next_check = min(md, J + 8);
         }
     }
+    (void)th_prev;
+    (void)res_prev;
+    __syncthreads();
     return J;
 }
 
@@ -620,7 +693,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
     double* hh = vec + 1 * vl;
     double* pw = vec + 2 * vl;
     double* rdiag = vec + 3 * vl;
-    double* wv = vec + 4 * vl;
+    double* wv = vec + 15 * vl;  // 2 slots (ping-pong)
     double* hb = vec + 5 * vl;
     double* al = vec + 6 * vl;
     double* be = vec + 7 * vl;
@@ -668,8 +741,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
             double h2 = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
             beta_h = 2.0 / block_sum(T, h2, red);
-            householder_congruence(T, G, m, ld, hh, beta_h, pw, red);
-            householder_congruence(T, B, m, ld, hh, beta_h, pw, red);
+            householder_congruence2(T, G, B, m, ld, hh, beta_h, pw, yy, red);
             a_schur = B[0];
             outward = !(a_schur > 0.0);
             for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld];
@@ -762,15 +834,32 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
                         for (int jx = T.lane; jx < i; jx += 32) G[i * ld + jx] = Lsave[i * ld + jx];
                     __syncthreads();
                     PROF_MARK(6);
-                    if (T.warp == 0) {
-                        // y = L^{-T} z (column-oriented back substitution)
-                        for (int i = md - 1; i >= 0; --i) {
-                            double yi = zz[i] * rdiag[i];
-                            __syncwarp();
-                            if (T.lane == 0) yy[i] = yi;
-                            for (int k = T.lane; k < i; k += 32) zz[k] -= G[i * ld + k] * yi;
-                            __syncwarp();
+                    // y = L^{-T} z, blocked backwards over 8-row blocks: warp 0 solves the
+                    // 8x8 transposed diagonal block, all threads update the rows above
+                    for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
+                        const int k0 = kb * 8;
+                        if (T.warp == 0) {
+                            const int r = T.lane;
+                            double zr = (r < 8) ? zz[k0 + r] : 0.0;
+#pragma unroll
+                            for (int c = 7; c >= 0; --c) {
+                                // y_c = z_c / L_cc; then z_r -= L_cr y_c for r < c
+                                const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
+                                if (r == c) zr = yc;
+                                else if (r < c) zr -= G[(k0 + c) * ld + k0 + r] * yc;
+                            }
+                            if (r < 8) yy[k0 + r] = zr;
                         }
+                        __syncthreads();
+                        for (int i = T.tid; i < k0; i += T.nthr) {
+                            double acc = zz[i];
+#pragma unroll
+                            for (int c = 0; c < 8; ++c) acc -= G[(k0 + c) * ld + i] * yy[k0 + c];
+                            zz[i] = acc;
+                        }
+                        __syncthreads();
+                    }
+                    if (T.warp == 0) {
                         if (defl) {  // y = H [ -b^T yh / a ; yh ]
                             double s = 0.0;
                             for (int i = T.lane; i < md; i += 32) s += bv[i] * yy[i];

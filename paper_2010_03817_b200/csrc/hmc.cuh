@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
     double* hh = vec + 0 * vl;
     double* pw = vec + 1 * vl;
     double* rdiag = vec + 2 * vl;
-    double* wv = vec + 3 * vl;
+    double* wv = vec + 14 * vl;  // 2 slots (ping-pong)
     double* hb = vec + 4 * vl;
     double* al = vec + 5 * vl;
     double* be = vec + 6 * vl;

@@ -359,7 +359,7 @@ static int ensure_hmc(spec_ctx* ctx) {
     if (ctx->hmc_scratch) return SPEC_OK;
     const int mp = roundup(ctx->m, 8);
     ctx->hmc_stride = (long long)8 * mp * ctx->ld;
-    ctx->hmc_smem = sizeof(double) * (size_t)14 * (mp + 8);
+    ctx->hmc_smem = sizeof(double) * (size_t)16 * (mp + 8);
     CK(cudaFuncSetAttribute(hmc_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->hmc_smem));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hmc_kernel<512>, 512, ctx->hmc_smem));
