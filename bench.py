@@ -312,6 +312,28 @@ def run_ours(args):
                            f"the M100 instance (H2D x0, D2H end points + moments inside the region; includes the "
                            f"reflection-count tail of the step)"}
 
+    # ---- BASELINE metric, second half: volume time at n = m = 40 (configs[2], eps 0.1, 4096 chains/phase)
+    vol = None
+    if args.volume_seeds > 0:
+        import paper_2010_03817_b200.parallel as par
+        inst2 = specgen.config_instance(2)
+        S2 = sw.Spectrahedron.from_instance(inst2, device=dev)
+        if dist is not None:
+            par.attach(S2)
+        S2.volume(0.1, 99, 512 * world, walk_len=2, burn=4)  # warm-up
+        times, vols = [], []
+        for sd in range(args.volume_seeds):
+            barrier()
+            t0 = time.time()
+            r = S2.volume(0.1, sd, 4096)
+            barrier()
+            times.append(time.time() - t0)
+            vols.append(r)
+        vol = {"metric": "volume time at n=m=40 (configs[2], eps=0.1, 4096 chains/phase)", "unit": "s",
+               "seconds_mean": float(np.mean(times)), "seconds": times,
+               "volume": [v["volume"] for v in vols], "std_rel": [v["std_rel"] for v in vols],
+               "phases": [v["phases"] for v in vols], "oracle_calls": [v["calls"] for v in vols],
+               "paper_context": "PAPER Table 2 S-40-40: 6.7 s on an i7-6700 for the paper's own (elongated) instance"}
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -349,6 +371,7 @@ def run_ours(args):
                  "active_chains": active},
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "volume_n40": vol,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -365,6 +388,7 @@ def main():
     ap.add_argument("--chains", type=int, default=CHAINS, help="chains per GPU")
     ap.add_argument("--e2e-chains", type=int, default=2048)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--volume-seeds", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -517,22 +517,49 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
         long long tl0 = clock64();
         // ---- (A) q_j = w / beta stored; w' = M q_j: 4 threads per row, double2 columns
         for (int e = T.tid; e < mdp; e += T.nthr) qj[e] = win[e] * invb;
-        for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
-            const int rw = r0 + lrow;
-            double a0 = 0.0, a1 = 0.0;
-            if (rw < mdp) {
-                const double* Mr = M + (size_t)rw * ld;
-                for (int c = 2 * lg; c < mdp; c += 8) {
-                    double2 mv = *reinterpret_cast<const double2*>(Mr + c);
-                    double2 wq = *reinterpret_cast<const double2*>(win + c);
-                    a0 += mv.x * wq.x;
-                    a1 += mv.y * wq.y;
+        if (mdp <= 128) {
+            // fast path: 16 double2 loads per thread issued up front, 4 accumulators
+            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+                const int rw = r0 + lrow;
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                if (rw < mdp) {
+                    const double* Mr = M + (size_t)rw * ld;
+                    double2 mv[16], wq[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const int c = 2 * lg + 8 * k;
+                        mv[k] = (c < mdp) ? *reinterpret_cast<const double2*>(Mr + c) : make_double2(0.0, 0.0);
+                        wq[k] = (c < mdp) ? *reinterpret_cast<const double2*>(win + c) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        acc[k & 3] += mv[k].x * wq[k].x;
+                        acc[k & 3] += mv[k].y * wq[k].y;
+                    }
                 }
+                double a0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+                if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
             }
-            a0 += a1;
-            a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
-            a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-            if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
+        } else {
+            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+                const int rw = r0 + lrow;
+                double a0 = 0.0, a1 = 0.0;
+                if (rw < mdp) {
+                    const double* Mr = M + (size_t)rw * ld;
+                    for (int c = 2 * lg; c < mdp; c += 8) {
+                        double2 mv = *reinterpret_cast<const double2*>(Mr + c);
+                        double2 wq = *reinterpret_cast<const double2*>(win + c);
+                        a0 += mv.x * wq.x;
+                        a1 += mv.y * wq.y;
+                    }
+                }
+                a0 += a1;
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+                if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
+            }
         }
         __syncthreads();
         long long tl1 = clock64();
@@ -546,19 +573,35 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                 const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
                 if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wout + i0);
                 if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wout + i1);
-                for (int i = T.warp; i < nrows; i += T.nwarps) {
-                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
-                    double sacc = 0.0;
-                    if (i0 < mdp) {
-                        double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
-                        sacc += q0.x * w0.x + q0.y * w0.y;
+                const int NW = T.nwarps;
+                for (int ib = T.warp; ib < nrows; ib += 4 * NW) {
+                    double sacc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = ib + u * NW;
+                        const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
+                        double sa = 0.0;
+                        if (i < nrows) {
+                            if (i0 < mdp) {
+                                double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
+                                sa += q0.x * w0.x + q0.y * w0.y;
+                            }
+                            if (i1 < mdp) {
+                                double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
+                                sa += q1.x * w1.x + q1.y * w1.y;
+                            }
+                        }
+                        sacc[u] = sa;
                     }
-                    if (i1 < mdp) {
-                        double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
-                        sacc += q1.x * w1.x + q1.y * w1.y;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], o);
+                    if (T.lane == 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (ib + u * NW < nrows) hb[ib + u * NW] = sacc[u];
                     }
-                    sacc = warp_sum(sacc);
-                    if (T.lane == 0) hb[i] = sacc;
                 }
             } else {
                 for (int i = T.warp; i < nrows; i += T.nwarps) {
@@ -580,12 +623,15 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                     const int e = e0 + (T.tid >> 2);
                     double sa = 0.0, sb = 0.0;
                     if (e < mdp) {
-                        int i = g;
-                        for (; i + 4 <= j; i += 8) {
-                            sa += hb[i] * Q[(size_t)i * ld + e];
-                            sb += hb[i + 4] * Q[(size_t)(i + 4) * ld + e];
+                        for (int ibase = 0; ibase <= j; ibase += 64) {
+                            double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int i = ibase + g + 4 * k;
+                                if (i <= j) acc4[k & 3] += hb[i] * Q[(size_t)i * ld + e];
+                            }
+                            sa += (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
                         }
-                        for (; i <= j; i += 4) sa += hb[i] * Q[(size_t)i * ld + e];
                     }
                     sa += sb;
                     sa += __shfl_xor_sync(0xffffffffu, sa, 1);
@@ -597,7 +643,10 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                         nloc += (g == 0) ? wn * wn : 0.0;
                     }
                 }
-                nloc = warp_sum(nloc);
+                // partial norms live in the g == 0 lanes: reduce over lanes 4, 8, 16 apart
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 4);
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 8);
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 16);
                 if (T.lane == 0) red2[T.warp] = nloc;
             }
             __syncthreads();
