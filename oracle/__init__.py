@@ -106,6 +106,8 @@ def lib():
                                C.POINTER(_Stats), C.c_int]
         l.orc_trace.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp, _dp, _dp,
                                 _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        l.orc_replay.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp,
+                                 C.POINTER(C.c_int64)]
         l.orc_qep_root.argtypes = [C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]
         l.orc_hmc_chord.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp,
                                     C.POINTER(_ChordRes)]
@@ -306,6 +308,20 @@ def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho:
         raise ValueError(f"orc_trace rc={rc}")
     k = nrec.value
     return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k])
+
+
+def replay(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_calls: int,
+           x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK):
+    """x of one chain after exactly max_calls chord calls (GPU state after that many rounds)."""
+    n = lmi.n
+    x0 = _arr(np.zeros(n) if x0 is None else x0)
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    x = np.zeros(n)
+    calls = C.c_int64()
+    rc = lib().orc_replay(lmi._h, C.byref(p), chain, _p(x0), max_calls, _p(x), C.byref(calls))
+    if rc:
+        raise ValueError(f"orc_replay rc={rc}")
+    return x, calls.value
 
 
 def ball_volume(n: int, r: float = 1.0) -> float:

@@ -964,6 +964,7 @@ typedef struct {
     double* w;
     double* u;    /* unit kernel vector of the bound block */
     orc_chord_res* res;
+    int64_t budget; /* stop after this many chord calls (-1: none) */
 } walk_ws;
 
 static void ws_init(walk_ws* W, const orc_lmi* L) {
@@ -976,6 +977,7 @@ static void ws_init(walk_ws* W, const orc_lmi* L) {
         if (L->mb[b] > maxmb) maxmb = L->mb[b];
     W->u = dalloc(maxmb);
     W->res = (orc_chord_res*)xmalloc(sizeof(orc_chord_res));
+    W->budget = -1;
 }
 static void ws_free(walk_ws* W) {
     free(W->x); free(W->xs); free(W->v); free(W->g); free(W->w); free(W->F); free(W->Fs);
@@ -1016,6 +1018,7 @@ static int walk_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain,
     int bound = -1;
     st->steps += 1;
     for (;;) {
+        if (W->budget >= 0 && st->calls >= W->budget) return 5; /* replay budget reached mid-step */
         orc_dir_block(L, 0, W->v, W->F1);
         orc_chord_res* r = W->res;
         int rc;
@@ -1151,6 +1154,29 @@ int orc_walk(const orc_lmi* L, const orc_walk_params* p, int64_t chain_begin, in
     pthread_mutex_destroy(&J.mu);
     if (st) *st = J.st;
     return J.rc;
+}
+
+/* State of one chain after exactly max_calls chord calls (the GPU scheduler's
+ * state after max_calls rounds).  Returns 0, or 2 if a start was not interior. */
+int orc_replay(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0, int64_t max_calls,
+               double* x_out, int64_t* calls_out) {
+    int n = L->n;
+    walk_ws W;
+    ws_init(&W, L);
+    W.budget = max_calls;
+    orc_stats st = {0, 0, 0, 0, 0, 0};
+    memcpy(W.x, x0, sizeof(double) * n);
+    orc_eval_block(L, 0, W.x, W.F);
+    int rc = 0;
+    for (int64_t s = 0; s < p->steps && st.calls < max_calls; ++s) {
+        rc = walk_step(L, p, (uint32_t)chain, (uint32_t)s, &W, &st, NULL);
+        if (rc == 5) { rc = 0; break; }
+        if (rc) break;
+    }
+    memcpy(x_out, W.x, sizeof(double) * n);
+    *calls_out = st.calls;
+    ws_free(&W);
+    return rc;
 }
 
 int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,

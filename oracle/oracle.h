@@ -108,6 +108,11 @@ typedef struct orc_walk_params {
 int orc_walk(const orc_lmi* L, const orc_walk_params* p, int64_t chain_begin, int64_t chain_end,
              const double* x0, int x0_stride, double* final_x, orc_stats* st, int nthreads);
 
+/* State of one chain after exactly max_calls chord calls (parity entry for the
+ * GPU round scheduler: one call per active chain per round). */
+int orc_replay(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0, int64_t max_calls,
+               double* x_out, int64_t* calls_out);
+
 /* Record the first max_refl reflections of one chain (parity entry). */
 int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
               int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,

@@ -1,0 +1,118 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (65536 chains through the round scheduler): sampled chains are compared
+with the oracle replaying exactly the same number of boundary-oracle calls
+(one call per chain per round), plus full-population laws with closed forms
+and oracle-vs-GPU statistics at configs the oracle can finish."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import specgen
+
+pytestmark = pytest.mark.gpu
+SAMPLED = [0, 1, 777, 32768, 65535]
+
+
+def _device_state(S, chains, rounds, steps, L, rho, seed, kind=0, T=1.0):
+    import torch
+    S.walk_begin(chains, steps, L, rho, seed, kind=kind, T=T)
+    S.walk_rounds(rounds)
+    X = torch.empty((chains, S.n), dtype=torch.float64, device="cuda")
+    st = S.walk_end(final_x=X)
+    return X.cpu().numpy(), st
+
+
+def test_m100_bench_configuration_sampled_chains():
+    """bench.py's workload: configs[3] instance, 65536 billiard chains, L=2sqrt(n), rho=10n, seed 4."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.config_instance(3)
+    S = sw.Spectrahedron.from_instance(inst)
+    R = 12
+    X, st = _device_state(S, 65536, R, 100, 20.0, 1000, 4)
+    assert st["calls"] == 65536 * R
+    lmi = oracle.Lmi(inst)
+    for c in SAMPLED:
+        xo, calls = oracle.replay(lmi, oracle.BILLIARD, 4, c, 100, 20.0, 1000, R)
+        assert calls == R
+        assert np.linalg.norm(X[c] - xo) <= 1e-8 * max(np.linalg.norm(xo), 0.1), c
+
+
+def test_m200_configs4_sampled_chains():
+    """configs[4]: n = m = 200 (global-scratch K2 variant), 65536 chains, seed 4."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.config_instance(4)
+    S = sw.Spectrahedron.from_instance(inst)
+    R = 2
+    L = 2 * math.sqrt(200)
+    X, st = _device_state(S, 65536, R, 100, L, 2000, 4)
+    lmi = oracle.Lmi(inst)
+    for c in (0, 65535):
+        xo, calls = oracle.replay(lmi, oracle.BILLIARD, 4, c, 100, L, 2000, R)
+        assert np.linalg.norm(X[c] - xo) <= 1e-8 * max(np.linalg.norm(xo), 0.1), c
+
+
+def test_hmc_configs3_sampled_chains():
+    """configs[3] HMC-r workload (65536 chains, T = 1, c ~ N(0, I) normalised), sampled."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.config_instance(3)
+    c = specgen.objective(100, 3)
+    S = sw.Spectrahedron.from_instance(inst)
+    S.set_objective(c)
+    R, L = 2, 1.09  # L = diam_est
+    X, st = _device_state(S, 65536, R, 200, L, 1000, 3, kind=sw.HMC, T=1.0)
+    lmi = oracle.Lmi(inst)
+    for ch in (0, 40000):
+        xo, calls = oracle.replay(lmi, oracle.HMC, 3, ch, 200, L, 1000, R, T=1.0, c=c)
+        assert np.linalg.norm(X[ch] - xo) <= 1e-8 * max(np.linalg.norm(xo), 0.1), ch
+
+
+def test_elliptope_configs1_moments():
+    """configs[1]: elliptope k=20 (n=190, m=20), 16384 chains from 0, L=2sqrt(n):
+    uniform law has E[x]=0, E[x^2]=1/(k+1)=1/21."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.config_instance(1)
+    S = sw.Spectrahedron.from_instance(inst)
+    out = S.walk_sample(16384, 20, 2 * math.sqrt(190), 1900, seed=1)
+    X = out["final_x"]
+    per_chain_x2 = (X ** 2).mean(1)
+    se = per_chain_x2.std(ddof=1) / math.sqrt(len(X))
+    assert abs(per_chain_x2.mean() - 1 / 21) <= 4 * se, (per_chain_x2.mean(), 1 / 21, se)
+    mx = X.mean(1)
+    assert abs(mx.mean()) <= 4 * mx.std(ddof=1) / math.sqrt(len(X))
+    # sum_x / sum_xx outputs agree with the end points
+    assert np.allclose(out["sum_x"], X.sum(0), rtol=0, atol=1e-9)
+
+
+def test_configs0_full_walk_statistics_vs_oracle():
+    """configs[0]: 64 chains x 1000 steps, L=2sqrt(n), rho=10n, seed 0 -- GPU and oracle
+    end-point laws agree (chaos makes long walks differ pointwise)."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.config_instance(0)
+    S = sw.Spectrahedron.from_instance(inst)
+    L = 2 * math.sqrt(10)
+    g = S.walk_sample(64, 1000, L, 100, seed=0)
+    o, st = oracle.walk(oracle.Lmi(inst), oracle.BILLIARD, 0, 0, 64, 1000, L, 100)
+    a, b = (g["final_x"] ** 2).mean(1), (o ** 2).mean(1)
+    se = math.sqrt(a.var(ddof=1) / 64 + b.var(ddof=1) / 64)
+    assert abs(a.mean() - b.mean()) <= 4 * se
+    assert g["stats"]["steps"] == 64 * 1000
+    # reflection rate matches the oracle's within sampling noise
+    rg = g["stats"]["reflections"] / g["stats"]["steps"]
+    ro = st["reflections"] / st["steps"]
+    assert abs(rg - ro) <= 0.1 * ro
+
+
+def test_volume_vs_oracle_rand_cube_10_seeds():
+    """configs[2]-style body at reduced size (rand-cube n=m=12): GPU and oracle volume
+    estimators over the same 10 seeds agree within 2 sigma of the oracle's spread."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.rand_cube(12, 12, 2)
+    S = sw.Spectrahedron.from_instance(inst)
+    seeds = range(10)
+    g = np.array([S.volume(0.1, s, 256, walk_len=5, burn=20)["volume"] for s in seeds])
+    o = np.array([oracle.volume(inst, 0.1, s, 256, W=5, burn=20)["volume"] for s in seeds])
+    sd = o.std(ddof=1)
+    assert abs(g.mean() - o.mean()) <= 2 * sd, (g.mean(), o.mean(), sd)
+    assert np.all(np.abs(g - o.mean()) <= 3.5 * sd), (g, o.mean(), sd)
