@@ -385,7 +385,12 @@ def volume(inst, eps: float, seed: int, N: int, W: int = 10, burn: int = 40, L: 
         # strictly inside B(r): the pilot's quantile point itself lies on the sphere
         inside = X[np.linalg.norm(X - c0, axis=1) < r]
         idx = np.arange(count) % len(inside)
-        return inside[idx]
+        return warm(inside[idx])
+
+    def warm(X):
+        # DESIGN.md R24: a warm start re-forms F(x); an end point within rounding of
+        # the boundary is contracted towards the interior point c0 by 2^-40
+        return c0 + (1.0 - 2.0 ** -40) * (X - c0)
 
     calls = 0
     # ---- pilot: radii
@@ -409,7 +414,7 @@ def volume(inst, eps: float, seed: int, N: int, W: int = 10, burn: int = 40, L: 
     # ---- estimation
     attempt, Ne = 0, N
     while True:
-        X = burned if Ne == N else burned[np.arange(Ne) % N]
+        X = warm(burned if Ne == N else burned[np.arange(Ne) % N])
         ratios = []
         for i in range(k):
             X, st = walk_phase(radii[i], X, W, vol_tag(PURPOSE_VOLUME, i, False, attempt), Ne)

@@ -1085,6 +1085,13 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         for (int i = 0; i < n; ++i) s2 += (x[i] - c0[i]) * (x[i] - c0[i]);
         return std::sqrt(s2);
     };
+    // A warm start re-forms F(x) from x, and a walk end point can lie within
+    // rounding of the boundary (a step may end at l = t+ - ulp): contract it
+    // towards the interior point c0 by 2^-40 (R24; the oracle does the same).
+    auto warm = [&](const double* x, double* out) {
+        const double lam = 1.0 - 0x1p-40;
+        for (int i = 0; i < n; ++i) out[i] = c0[i] + lam * (x[i] - c0[i]);
+    };
     // warm starts of this rank's chains [begin, begin + Cl) from the global points strictly inside B(r)
     auto resample = [&](const std::vector<double>& Xg, double r, long long Nt, std::vector<double>& X0) -> int {
         const long long Cl = Nt / W, begin = (long long)R * Cl;
@@ -1096,7 +1103,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         X0.resize((size_t)Cl * n);
         for (long long j = 0; j < Cl; ++j) {
             long long src = inside[(size_t)((begin + j) % (long long)inside.size())];
-            std::copy(&Xg[(size_t)src * n], &Xg[(size_t)src * n] + n, &X0[(size_t)j * n]);
+            warm(&Xg[(size_t)src * n], &X0[(size_t)j * n]);
         }
         return SPEC_OK;
     };
@@ -1140,7 +1147,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         X0.resize((size_t)Cl * n);
         for (long long j = 0; j < Cl; ++j) {
             long long src = (begin + j) % N;
-            std::copy(&burned_g[(size_t)src * n], &burned_g[(size_t)src * n] + n, &X0[(size_t)j * n]);
+            warm(&burned_g[(size_t)src * n], &X0[(size_t)j * n]);
         }
         ratios.clear();
         for (int i = 0; i < k; ++i) {
