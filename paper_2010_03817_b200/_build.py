@@ -31,7 +31,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "specwalk.cu")]
+    extra = os.environ.get("SPECWALK_DEFS", "").split()  # e.g. -DSW_PROF_LANCZOS=1 (profiling builds)
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", LIB + ".tmp", os.path.join(CSRC, "specwalk.cu")]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd, cwd=HERE)

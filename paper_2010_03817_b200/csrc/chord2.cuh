@@ -19,6 +19,9 @@
 namespace sw {
 
 constexpr int NVEC2 = 20;
+#ifndef SW_PROF_LANCZOS
+#define SW_PROF_LANCZOS 0  // per-stage clock64 counters of lanczos_reg (build with -DSW_PROF_LANCZOS=1)
+#endif
 
 __device__ __forceinline__ void dmma_t(double (&d)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -396,7 +399,7 @@ __device__ double tri_multisect_warp(int lane, const double* al, const double* b
 // s_i = -(be_i / D+_i) s_{i+1} (i < r), s_i = -(be_{i-1} / D-_i) s_{i-1} (i > r).
 // Returns (to every thread) the Lanczos residual |beta_last| |s_{J-1}| / |s|;
 // s is normalised.  CTA-cooperative; dp, dm scratch of length J.
-__device__ double tri_twisted_vec(const Team& T, const double* al, const double* be, int J, double theta,
+__device__ __noinline__ double tri_twisted_vec(const Team& T, const double* al, const double* be, int J, double theta,
                                   double beta_last, double* dp, double* dm, double* s, double* red, int* sh_r) {
     const double tiny = 1e-290;
     if (T.tid == 0) {
@@ -716,7 +719,373 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
     return J;
 }
 
-template <int NT, bool SMEM>
+// |s_J| / |s| for the eigenvector s of the tridiagonal T_J (al, be) at the
+// eigenvalue th, by the backward recurrence from s_J = 1 (the top Ritz vector
+// grows towards the first Lanczos indices, so this direction is stable);
+// rbe = 1 / be.  One thread.  The Lanczos residual is be[J-1] times this.
+__device__ double tri_back_lastcomp(const double* al, const double* be, const double* rbe, int J, double th) {
+    if (J <= 1) return 1.0;
+    double sJ = 1.0, s1 = 1.0;
+    double s0 = (th - al[J - 1]) * rbe[J - 2];
+    double nn = 1.0 + s0 * s0;
+    for (int i = J - 2; i >= 1; --i) {
+        const double sm = ((th - al[i]) * s0 - be[i] * s1) * rbe[i - 1];
+        s1 = s0;
+        s0 = sm;
+        nn += sm * sm;
+        if (nn > 0x1p+600) {
+            s0 *= 0x1p-300; s1 *= 0x1p-300; sJ *= 0x1p-300; nn *= 0x1p-600;
+        }
+    }
+    return sJ / sqrt(nn);
+}
+
+// Lanczos with full (classical Gram-Schmidt) reorthogonalisation on the
+// symmetric md x md matrix M, M REGISTER-resident: thread (r = tid/4, g = tid%4)
+// holds row r at the column pairs 2g + 8k, k < NT/32 (so md <= NT/4).
+// Iteration j (three barriers):
+//   (1) w' = M q_j: 4 lanes per row, q_j read from the unnormalised copy u_j
+//       (ping-pong buffer wu) times 1/beta_{j-1}; the row owner stores the
+//       normalised q_j into the basis Q and w' into wp;
+//   (2) h_i = q_i . w' for i <= j, four dots per warp in flight; alpha_j = h_j;
+//   (3) w = w' - Q h (4 lanes per row split i), beta_j = |w|, u_{j+1} = w.
+// Plain Lanczos (no reorthogonalisation) was measured to lose 1e-6..1e-3 of
+// theta_max near the boundary (huge |theta_min| converging first); one CGS pass
+// keeps theta_max within ~20 eps |M| of LAPACK on BASELINE instances.
+// Convergence: residual be[J-1] |s_J| of the requested extreme Ritz pair(s)
+// <= 1e-14 |T_J|; Ritz values by Laguerre from the Gershgorin bound, |s_J| by
+// the backward recurrence; the first check at J = 0.4 md, the next ones
+// predicted from the observed linear rate (at most 8 iterations apart).
+// On return sv holds the top Ritz vector of T_J (z = Q sv).  wv: 3 (mdp + 8).
+// Extreme eigenvalue of the tridiagonal T_J (diagonal sm[oA..], squared
+// off-diagonal sm[oB2..]) by Laguerre's method on p(x) = det(x I - T) (all roots
+// real, cubic convergence, monotone from outside the spectrum).  Started at x
+// (a warm bound); if the Sturm signs of the first sweep show that x is not
+// outside the spectrum, restarted at xsafe (Gershgorin).  Stops at 2 eps |x| or
+// when the step changes direction (rounding-noise level).  One thread; the
+// recurrence is rescaled by powers of two every 4 steps.
+__device__ double tri_laguerre_sm(const int oA, const int oB2, const int J, double x, const double xsafe,
+                                  const bool top) {
+    extern __shared__ __align__(16) double sm[];
+    const double eps = 2.220446049250313e-16;
+    if (J == 1) return sm[oA];
+    const double n = (double)J;
+    bool first = true, has_step = false;
+    double last_step = 0.0;
+    for (int it = 0; it < 40; ++it) {
+        double p0 = 1.0, d0 = 0.0, s0 = 0.0;
+        double p1 = x - sm[oA], d1 = 1.0, s1 = 0.0;
+        // outside the spectrum: all p_k > 0 (above) / sign (-1)^k (below)
+        bool outside = top ? (p1 > 0.0) : (p1 < 0.0);
+        int i = 1;
+        for (; i < J; ++i) {
+            const double t = x - sm[oA + i], b2 = sm[oB2 + i - 1];
+            const double p2 = t * p1 - b2 * p0;
+            const double d2 = p1 + t * d1 - b2 * d0;
+            const double s2 = 2.0 * d1 + t * s1 - b2 * s0;
+            p0 = p1; d0 = d1; s0 = s1;
+            p1 = p2; d1 = d2; s1 = s2;
+            if (first) outside = outside && (top ? (p1 > 0.0) : ((i & 1) ? (p1 > 0.0) : (p1 < 0.0)));
+            if ((i & 3) == 0) {
+                const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
+                if (ap > 0x1p+400) {
+                    p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
+                    p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
+                } else if (ap < 0x1p-400) {
+                    p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
+                    p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
+                }
+            }
+        }
+        if (first && !outside && x != xsafe) {
+            x = xsafe;
+            first = false;
+            continue;
+        }
+        first = false;
+        if (p1 == 0.0) return x;
+        const double G = d1 / p1;
+        const double H = G * G - s1 / p1;
+        const double disc = fmax((n - 1.0) * (n * H - G * G), 0.0);
+        const double den = G + copysign(sqrt(disc), G);
+        if (den == 0.0) return x;
+        const double step = n / den;
+        if (has_step && (step > 0.0) != (last_step > 0.0)) break;  // direction flip: noise level
+        x -= step;
+        last_step = step;
+        has_step = true;
+        if (fabs(step) <= 2.0 * eps * fabs(x)) break;
+    }
+    return x;
+}
+
+// |s_J| / |s| of the eigenvector of T_J at the eigenvalue th (backward
+// recurrence from s_J = 1, as tri_back_lastcomp) on shared-memory arrays.
+__device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB, const int J, const double th) {
+    extern __shared__ __align__(16) double sm[];
+    if (J <= 1) return 1.0;
+    double sJ = 1.0, s1 = 1.0;
+    double s0 = (th - sm[oA + J - 1]) * sm[oRB + J - 2];
+    double nn = 1.0 + s0 * s0;
+    for (int i = J - 2; i >= 1; --i) {
+        const double sm_ = ((th - sm[oA + i]) * s0 - sm[oB + i] * s1) * sm[oRB + i - 1];
+        s1 = s0;
+        s0 = sm_;
+        nn += sm_ * sm_;
+        if (nn > 0x1p+600) {
+            s0 *= 0x1p-300; s1 *= 0x1p-300; sJ *= 0x1p-300; nn *= 0x1p-600;
+        }
+    }
+    return sJ / sqrt(nn);
+}
+
+// Lanczos convergence check (thread 0: top, thread 32: bottom): Ritz value by
+// Laguerre from the warm bound (previous value + residual, else Gershgorin),
+// residual be[J-1] |s_J|.  Out of line: it runs on one or two threads while
+// the CTA waits.  Results: sm[oShd + 0..3] = theta_top, res_top, theta_bot, res_bot.
+__device__ __noinline__ void lanczos_check(const int tid, const int oAl, const int oBe, const int oB2, const int oRbe,
+                                           const int J, const double beta, const double ghi, const double glo,
+                                           const double tnorm, const bool need_bot, const double warm_top,
+                                           const double warm_bot, const int oShd) {
+    extern __shared__ __align__(16) double sm[];
+    if (tid == 0) {
+        const double xs = ghi + 1e-13 * tnorm;
+        const double th = tri_laguerre_sm(oAl, oB2, J, fmin(xs, warm_top), xs, true);
+        sm[oShd + 0] = th;
+        sm[oShd + 1] = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
+    } else if (need_bot && tid == 32) {
+        const double xs = glo - 1e-13 * tnorm;
+        const double th = tri_laguerre_sm(oAl, oB2, J, fmax(xs, warm_bot), xs, false);
+        sm[oShd + 2] = th;
+        sm[oShd + 3] = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
+    }
+}
+
+// K2 vector slots (length vl = mp + 8 each) in the shared vector area
+enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
+             V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
+
+template <int NT, int KC>
+__device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
+                                           const bool need_bot, const int oVec, const int vl, const int oRed,
+                                           unsigned long long* prof) {
+    // everything addressed as offsets into the dynamic shared memory (32-bit LDS/STS)
+    extern __shared__ __align__(16) double sm[];
+    static_assert(KC <= NT / 32, "M row segment of a thread: 8 KC columns <= NT / 4 rows");
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = NT / 32;
+    const int oAl = oVec + V_AL * vl, oBe = oVec + V_BE * vl, oRbe = oVec + V_RBE * vl, oHb = oVec + V_HB * vl;
+    const int oB2 = oVec + V_B2 * vl;
+    const int oWu = oVec + V_LZ * vl;  // wu0, wu1 (ping-pong), wp: 3 x (mdp + 8)
+    const int oWp = oWu + 2 * (mdp + 8);
+    const int oRB = oRed + 16;         // per-warp partial norms
+    const int oShd = oRed + 32;        // check results (4) and thetas (2)
+    const int oQT = oM;                // transposed basis, in M's space once M is in registers
+    const int r = tid >> 2, g = tid & 3;
+    const bool rowok = r < md;
+    const bool owner = (g == 0) && (r < mdp);
+    double2 mr[KC];
+    {
+        const int oMr = oM + (r < mdp ? r : 0) * ld;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const int c = 2 * g + 8 * k;
+            mr[k] = (r < mdp && c < mdp) ? *reinterpret_cast<const double2*>(sm + oMr + c) : make_double2(0.0, 0.0);
+        }
+    }
+    // dots: 8 lanes per dot (lane = 8 u + s), element pairs 2 s + 16 t, t < tcnt
+    const int du = lane >> 3, ds = lane & 7;
+    const int tcnt = (mdp - 2 * ds + 15) >> 4;
+    // start vector u_0 (fixed, zero padded)
+    double wr = 0.0;
+    if (rowok) {
+        double f = (double)r * 0.6180339887498949;
+        wr = 0.5 + (f - floor(f));
+    }
+    if (owner) sm[oWu + r] = wr;
+    double p0 = (g == 0) ? wr * wr : 0.0;
+    p0 = warp_sum(p0);
+    if (lane == 0) sm[oRB + warp] = p0;
+    __syncthreads();  // also: every thread has its M row in registers (QT may overwrite M)
+    double nn0 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) nn0 += sm[oRB + w];
+    double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
+    double tnorm = 0.0, ghi = -SW_INF, glo = SW_INF, bjm1 = 0.0;
+    int next_check = max(min(md, 12), (md * 2) / 5);
+    int jprev = 0;
+    double lres_prev = 0.0;
+    int J = 0;
+    double th_top = -SW_INF, th_bot = SW_INF, warm_top = SW_INF, warm_bot = -SW_INF;
+#if SW_PROF_LANCZOS
+    long long c_mv = 0, c_dot = 0, c_upd = 0, c_chk = 0, c_t = clock64();
+#define SW_LZ_STAMP(acc) if (prof) { long long c = clock64(); acc += c - c_t; c_t = c; }
+#else
+#define SW_LZ_STAMP(acc)
+#endif
+    for (int j = 0; j < md; ++j) {
+        const int oU = oWu + (j & 1) * (mdp + 8);
+        const int oUn = oWu + ((j + 1) & 1) * (mdp + 8);
+        // ---- (1) w' = M q_j
+        double a4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k0 = 0; k0 < KC; k0 += 4) {
+            double2 wq[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int c = 2 * g + 8 * (k0 + k);
+                wq[k] = (k0 + k < KC && c < mdp) ? *reinterpret_cast<const double2*>(sm + oU + c)
+                                                 : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k0 + k < KC) {
+                    a4[k] = fma(mr[k0 + k].x, wq[k].x, a4[k]);
+                    a4[k] = fma(mr[k0 + k].y, wq[k].y, a4[k]);
+                }
+            }
+        }
+        double y = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+        y += __shfl_xor_sync(0xffffffffu, y, 1);
+        y += __shfl_xor_sync(0xffffffffu, y, 2);
+        const double wpr = rowok ? y * sj : 0.0;
+        if (owner) {
+            const double q = wr * sj;  // q_j (wr = u_j[r])
+            sm[oQ + j * ld + r] = q;
+            sm[oQT + r * ld + j] = q;
+            sm[oWp + r] = wpr;
+        }
+        __syncthreads();
+        SW_LZ_STAMP(c_mv)
+        // ---- (2)+(3) classical Gram-Schmidt of w' against q_0..q_j; a second pass
+        // (DGKS) only on severe cancellation (|w| < 1e-6 |w'|, e.g. an invariant subspace)
+        double wcur = wpr, alpha = 0.0, nnb = 0.0, nn = 0.0;
+        for (int pass = 0; pass < 2; ++pass) {
+            // (2) h_i = q_i . w for i <= j, and |w|^2 (slot j + 1): 8 lanes per dot, 4 dots per warp
+            for (int ib = 4 * warp; ib <= j + 1; ib += 4 * NW) {
+                const int i = ib + du;
+                double sacc = 0.0;
+                if (i <= j + 1) {
+                    const int oQi = (i <= j ? oQ + i * ld : oWp) + 2 * ds;
+                    const int oW = oWp + 2 * ds;
+                    double s2 = 0.0;
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        if (t < tcnt) {
+                            const double2 q2 = *reinterpret_cast<const double2*>(sm + oQi + 16 * t);
+                            const double2 w2 = *reinterpret_cast<const double2*>(sm + oW + 16 * t);
+                            if (t & 1) { s2 = fma(q2.x, w2.x, s2); s2 = fma(q2.y, w2.y, s2); }
+                            else { sacc = fma(q2.x, w2.x, sacc); sacc = fma(q2.y, w2.y, sacc); }
+                        }
+                    }
+                    sacc += s2;
+                }
+                sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+                sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+                sacc += __shfl_xor_sync(0xffffffffu, sacc, 4);
+                if (ds == 0 && i <= j + 1) {
+                    sm[oHb + i] = (i <= j) ? sacc : 0.0;  // hb[j + 1] = 0 pads the last pair
+                    if (i == j + 1) sm[oShd + 8] = sacc;
+                }
+            }
+            __syncthreads();
+            SW_LZ_STAMP(c_dot)
+            // (3) w -= Q h (row r: lane g takes the pairs i = 2 g + 8 k)
+            double acc0 = 0.0, acc1 = 0.0;
+            if (r < mdp) {
+                const int oQr = oQT + r * ld;
+                for (int i = 2 * g; i <= j; i += 8) {
+                    const double2 h2 = *reinterpret_cast<const double2*>(sm + oHb + i);
+                    const double2 q2 = *reinterpret_cast<const double2*>(sm + oQr + i);
+                    acc0 = fma(h2.x, q2.x, acc0);
+                    acc1 = fma(h2.y, q2.y, acc1);
+                }
+            }
+            double qh = acc0 + acc1;
+            qh += __shfl_xor_sync(0xffffffffu, qh, 1);
+            qh += __shfl_xor_sync(0xffffffffu, qh, 2);
+            wcur = rowok ? wcur - qh : 0.0;
+            alpha += sm[oHb + j];
+            if (pass == 0) nnb = sm[oShd + 8];
+            double pb = (g == 0) ? wcur * wcur : 0.0;
+            pb = warp_sum(pb);
+            if (lane == 0) sm[oRB + warp] = pb;
+            if (owner) sm[oUn + r] = wcur;
+            __syncthreads();
+            nn = 0.0;
+#pragma unroll
+            for (int ww = 0; ww < NW; ++ww) nn += sm[oRB + ww];
+            if (nn >= 1e-12 * nnb) break;
+            if (owner) sm[oWp + r] = wcur;  // second pass on w
+            __syncthreads();
+        }
+        wr = wcur;
+        const double beta = sqrt(nn);
+        if (tid == 0) {
+            sm[oAl + j] = alpha;
+            sm[oBe + j] = beta;
+            sm[oB2 + j] = nn;
+            sm[oRbe + j] = 1.0 / beta;
+        }
+        tnorm = fmax(tnorm, fabs(alpha) + beta + bjm1);
+        ghi = fmax(ghi, alpha + beta + bjm1);
+        glo = fmin(glo, alpha - beta - bjm1);
+        bjm1 = beta;
+        sj = 1.0 / beta;
+        J = j + 1;
+        const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
+        SW_LZ_STAMP(c_upd)
+        if (exhausted || J >= next_check) {
+            __syncthreads();  // al / be / b2 / rbe of this step visible
+            lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, ghi, glo, tnorm, need_bot, warm_top, warm_bot, oShd);
+            __syncthreads();
+            const double res = sm[oShd + 1], resb = need_bot ? sm[oShd + 3] : 0.0;
+            th_top = sm[oShd + 0];
+            th_bot = need_bot ? sm[oShd + 2] : SW_INF;
+            SW_LZ_STAMP(c_chk)
+            const double tol = 1e-14 * tnorm;
+            if (exhausted || (res <= tol && resb <= tol)) break;
+            // warm bounds for the next check (the extreme eigenvalue of M lies within res of the Ritz value)
+            warm_top = th_top + 1.001 * res + 1e-13 * tnorm;
+            warm_bot = th_bot - 1.001 * resb - 1e-13 * tnorm;
+            // predict the crossing from the observed linear rate
+            const double lres = log(fmax(res, resb));
+            int step = 8;
+            if (jprev > 0 && lres < lres_prev) {
+                const double rate = (lres_prev - lres) / (double)(J - jprev);
+                step = (int)ceil((lres - log(tol)) / rate);
+                step = max(1, min(8, step));
+            }
+            jprev = J;
+            lres_prev = lres;
+            next_check = min(md, J + step);
+        }
+    }
+#if SW_PROF_LANCZOS
+    if (prof && tid == 0) {
+        atomicAdd(&prof[12], (unsigned long long)c_mv);
+        atomicAdd(&prof[13], (unsigned long long)c_dot);
+        atomicAdd(&prof[14], (unsigned long long)c_upd);
+        atomicAdd(&prof[9], (unsigned long long)c_chk);
+    }
+#endif
+#undef SW_LZ_STAMP
+    (void)prof;
+    __syncthreads();
+    if (tid == 0) {
+        sm[oShd + 4] = th_top;
+        sm[oShd + 5] = th_bot;
+    }
+    // top Ritz vector of T_J (z = Q sv, Q orthonormal)
+    Team T;
+    T.tid = tid; T.nthr = NT; T.lane = lane; T.warp = warp; T.nwarps = NW;
+    int* sh_r = reinterpret_cast<int*>(sm + oShd + 6);
+    tri_twisted_vec(T, sm + oAl, sm + oBe, J, th_top, sm[oBe + J - 1], sm + oVec + V_DP * vl, sm + oVec + V_DM * vl,
+                    sm + oVec + V_SV * vl, sm + oRed, sh_r);
+    return J;
+}
+
+template <int NT, bool SMEM, int KC>
 __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
@@ -858,7 +1227,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
                     }
                 }
                 __syncthreads();
-                int J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
+                int J;
+                if (SMEM)
+                {
+                    // vector area + 64 slack doubles: [0,32) partial sums, [32,40) check results
+                    const int oVec = (int)(vec - smem_dyn), oRed = oVec + NVEC2 * vl;
+                    J = lanczos_reg<NT, KC>((int)(B - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
+                                            vl, oRed, P.prof);
+                    theta_max = smem_dyn[oRed + 32 + 4];
+                    theta_min = smem_dyn[oRed + 32 + 5];
+                }
+                else
+                    J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
                                     &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min);
                 lanczos_J = J;
                 if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);

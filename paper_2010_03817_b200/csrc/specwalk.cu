@@ -204,11 +204,16 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     // else matrices + Lanczos basis in a per-CTA global scratch slice.
     const int mp = roundup(m, 8);
     ctx->ld = mp + 4;
+    // K2 variants: 0 = <256, smem, KC 8> (mp <= 64), 1 = <512, smem, KC 13> (mp <= 104),
+    // 3 = <512, smem, KC 16> (mp <= 128), 2 = global scratch (larger m).
     if (mp <= 64) {
         ctx->k2_variant = 0;
         ctx->chord_threads = 256;
-    } else if (mp <= 128) {
+    } else if (mp <= 104) {
         ctx->k2_variant = 1;
+        ctx->chord_threads = 512;
+    } else if (mp <= 128) {
+        ctx->k2_variant = 3;
         ctx->chord_threads = 512;
     } else {
         ctx->k2_variant = 2;
@@ -218,25 +223,26 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     size_t per_cta = (size_t)2 * mp * ctx->ld + vecs;
     ctx->smem_bytes = per_cta * sizeof(double);
     int occ = 0;
-    if (ctx->k2_variant < 2 && ctx->smem_bytes <= 227 * 1024) {
+    if (ctx->k2_variant != 2 && ctx->smem_bytes <= 227 * 1024) {
         ctx->smem_path = true;
+#define SW_K2_SETUP(NT_, KC_)                                                                                   \
+    CK(cudaFuncSetAttribute(chord_kernel2<NT_, true, KC_>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                            (int)ctx->smem_bytes));                                                           \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<NT_, true, KC_>, NT_, ctx->smem_bytes));
         if (ctx->k2_variant == 0) {
-            CK(cudaFuncSetAttribute(chord_kernel2<256, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_bytes));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<256, true>, 256,
-                                                             ctx->smem_bytes));
+            SW_K2_SETUP(256, 8)
+        } else if (ctx->k2_variant == 1) {
+            SW_K2_SETUP(512, 13)
         } else {
-            CK(cudaFuncSetAttribute(chord_kernel2<512, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->smem_bytes));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, true>, 512,
-                                                             ctx->smem_bytes));
+            SW_K2_SETUP(512, 16)
         }
+#undef SW_K2_SETUP
         if (occ < 1) return fail(SPEC_ECUDA, "chord kernel cannot be resident (registers / shared memory)");
         ctx->chord_grid_max = occ * ctx->num_sms;
     } else {
         ctx->smem_path = false;
         ctx->k2_variant = 2;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false>, 512, 0));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false, 16>, 512, 0));
         if (occ < 1) occ = 1;
         if (occ > 2) occ = 2;
         ctx->chord_grid_max = occ * ctx->num_sms;
@@ -346,11 +352,13 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
     int grid = count_host < ctx->chord_grid_max ? count_host : ctx->chord_grid_max;
     if (grid < 1) grid = 1;
     if (ctx->k2_variant == 0)
-        chord_kernel2<256, true><<<grid, 256, ctx->smem_bytes, ctx->stream>>>(P);
+        chord_kernel2<256, true, 8><<<grid, 256, ctx->smem_bytes, ctx->stream>>>(P);
     else if (ctx->k2_variant == 1)
-        chord_kernel2<512, true><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
+        chord_kernel2<512, true, 13><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
+    else if (ctx->k2_variant == 3)
+        chord_kernel2<512, true, 16><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
     else
-        chord_kernel2<512, false><<<grid, 512, 0, ctx->stream>>>(P);
+        chord_kernel2<512, false, 16><<<grid, 512, 0, ctx->stream>>>(P);
     ctx->launches++;
 }
 
@@ -716,6 +724,9 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         fprintf(stderr, " total=%.0f | lanczos: J/call=%.1f check_cycles/call=%.0f checks/call=%.2f\n",
                 tot / (double)hs[0], (double)ph[10] / (double)hs[0], (double)ph[9] / (double)hs[0],
                 (double)ph[11] / (double)hs[0]);
+        fprintf(stderr, "[specwalk prof] lanczos_reg per iteration: matvec=%.0f dots=%.0f update=%.0f | check/call=%.0f\n",
+                (double)ph[12] / fmax((double)ph[10], 1.0), (double)ph[13] / fmax((double)ph[10], 1.0),
+                (double)ph[14] / fmax((double)ph[10], 1.0), (double)ph[9] / (double)hs[0]);
         double it = (double)ph[10];
         fprintf(stderr, "[specwalk prof] per lanczos iteration: matvec=%.0f dots=%.0f axpy+norm(+pass2)=%.0f qwrite=%.0f pass2_frac=%.3f\n",
                 ph[12] / it, ph[13] / it, ph[14] / it, ph[16] / it, ph[15] / it);
