@@ -85,6 +85,12 @@ struct ChordParams {
     const double* cvec;
     double Temp;
     double* tlast;  // t+ of the last hit (velocity at the hit = v - (c/T) t+)
+    int* jlast;     // Lanczos iterations of the chain's previous call (first-check hint)
+    // K2 split into factor / Lanczos / tail kernels: per-slot work buffers
+    double* wM;     // M = -L^{-1} A(v) L^{-T} (mdp x mdp rows, leading dimension ld)
+    double* wL;     // L (lower incl. diagonal, rows of leading dimension ld)
+    double* wS;     // scalars + vectors (chord3.cuh: S_*)
+    long long w_mstride, w_sstride;
 };
 
 // ---------------------------------------------------------------- team helpers

@@ -827,11 +827,26 @@ __device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB
     double sJ = 1.0, s1 = 1.0;
     double s0 = (th - sm[oA + J - 1]) * sm[oRB + J - 2];
     double nn = 1.0 + s0 * s0;
-    for (int i = J - 2; i >= 1; --i) {
-        const double sm_ = ((th - sm[oA + i]) * s0 - sm[oB + i] * s1) * sm[oRB + i - 1];
-        s1 = s0;
-        s0 = sm_;
-        nn += sm_ * sm_;
+    // i = J-2 .. 1 in groups of 4: the coefficients of a group (loads, products)
+    // are formed before its chain, so the chain itself is one FMA per step
+    for (int i0 = J - 2; i0 >= 1; i0 -= 4) {
+        double c[4], d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int ii = max(i0 - u, 1);
+            const double rb = sm[oRB + ii - 1];
+            c[u] = (th - sm[oA + ii]) * rb;
+            d[u] = -sm[oB + ii] * rb;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i0 - u >= 1) {
+                const double sm_ = fma(c[u], s0, d[u] * s1);
+                s1 = s0;
+                s0 = sm_;
+                nn = fma(sm_, sm_, nn);
+            }
+        }
         if (nn > 0x1p+600) {
             s0 *= 0x1p-300; s1 *= 0x1p-300; sJ *= 0x1p-300; nn *= 0x1p-600;
         }
@@ -839,36 +854,157 @@ __device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB
     return sJ / sqrt(nn);
 }
 
-// Lanczos convergence check (thread 0: top, thread 32: bottom): Ritz value by
-// Laguerre from the warm bound (previous value + residual, else Gershgorin),
-// residual be[J-1] |s_J|.  Out of line: it runs on one or two threads while
-// the CTA waits.  Results: sm[oShd + 0..3] = theta_top, res_top, theta_bot, res_bot.
-__device__ __noinline__ void lanczos_check(const int tid, const int oAl, const int oBe, const int oB2, const int oRbe,
-                                           const int J, const double beta, const double ghi, const double glo,
-                                           const double tnorm, const bool need_bot, const double warm_top,
-                                           const double warm_bot, const int oShd) {
+// Warp-parallel extreme Ritz value of T_J: every lane runs Laguerre (one
+// recurrence sweep per iteration) from its own start x_l = lo + (hi - lo) 2^(-l/2)
+// (top; mirrored for the bottom).  A start is valid if its first sweep shows it
+// outside the spectrum (all Sturm signs positive, resp. alternating): from there
+// Laguerre is monotone to the extreme root.  The lanes stop together once the
+// valid lane with the closest start has converged (2 eps |x| or a direction
+// flip); its value is returned to all lanes.  lo must be an inner bound (a Ritz
+// value of a smaller T or max/min alpha), hi an outer (Gershgorin) bound.
+__device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, const double lo, const double hi,
+                                    const bool top, const int lane) {
     extern __shared__ __align__(16) double sm[];
-    if (tid == 0) {
-        const double xs = ghi + 1e-13 * tnorm;
-        const double th = tri_laguerre_sm(oAl, oB2, J, fmin(xs, warm_top), xs, true);
-        sm[oShd + 0] = th;
-        sm[oShd + 1] = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
-    } else if (need_bot && tid == 32) {
-        const double xs = glo - 1e-13 * tnorm;
-        const double th = tri_laguerre_sm(oAl, oB2, J, fmax(xs, warm_bot), xs, false);
-        sm[oShd + 2] = th;
-        sm[oShd + 3] = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
+    const double eps = 2.220446049250313e-16;
+    if (J == 1) return sm[oA];
+    const double n = (double)J;
+    double x = lo + (hi - lo) * exp2(-0.5 * (double)lane);
+    if (lane == 0) x = hi;
+    bool valid = true, done = false, has_step = false;
+    double last_step = 0.0;
+    for (int it = 0; it < 40; ++it) {
+        double p0 = 1.0, d0 = 0.0, s0 = 0.0;
+        double p1 = x - sm[oA], d1 = 1.0, s1 = 0.0;
+        bool outside = top ? (p1 > 0.0) : (p1 < 0.0);
+        // steps i = 1 .. J-1 in groups of 4, the next group's a / b2 loaded ahead
+        // (reads up to 7 slots past J: inside the vector slot, values unused)
+        double an[4], bn[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { an[u] = sm[oA + 1 + u]; bn[u] = sm[oB2 + u]; }
+        for (int i0 = 1; i0 < J; i0 += 4) {
+            double ac[4], bc[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { ac[u] = an[u]; bc[u] = bn[u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) { an[u] = sm[oA + i0 + 4 + u]; bn[u] = sm[oB2 + i0 + 3 + u]; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u;
+                if (i < J) {
+                    const double t = x - ac[u], b2 = bc[u];
+                    const double qp = -b2 * p0, qd = fma(-b2, d0, p1), qs = fma(-b2, s0, 2.0 * d1);
+                    p0 = p1; d0 = d1; s0 = s1;
+                    p1 = fma(t, p0, qp);
+                    d1 = fma(t, d0, qd);
+                    s1 = fma(t, s0, qs);
+                    if (it == 0) outside = outside && (top ? (p1 > 0.0) : ((i & 1) ? (p1 > 0.0) : (p1 < 0.0)));
+                }
+            }
+            const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
+            if (ap > 0x1p+400) {
+                p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
+                p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
+            } else if (ap < 0x1p-400) {
+                p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
+                p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
+            }
+        }
+        if (it == 0) valid = outside;
+        if (!done) {
+            if (p1 == 0.0) {
+                done = true;
+            } else {
+                const double G = d1 / p1;
+                const double H = G * G - s1 / p1;
+                const double disc = fmax((n - 1.0) * (n * H - G * G), 0.0);
+                const double den = G + copysign(sqrt(disc), G);
+                if (den == 0.0) {
+                    done = true;
+                } else {
+                    const double step = n / den;
+                    if (has_step && (step > 0.0) != (last_step > 0.0)) {
+                        done = true;
+                    } else {
+                        x -= step;
+                        last_step = step;
+                        has_step = true;
+                        if (fabs(step) <= 2.0 * eps * fabs(x)) done = true;
+                    }
+                }
+            }
+        }
+        // the valid lane with the innermost start converges first and is the answer
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const int best = top ? 31 - __clz(vmask) : 31 - __clz(vmask);  // highest lane = innermost start
+        if (vmask == 0u) break;
+        const bool bdone = __shfl_sync(0xffffffffu, done ? 1 : 0, best) != 0;
+        if (bdone) return __shfl_sync(0xffffffffu, x, best);
     }
+    const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+    const int best = vmask ? 31 - __clz(vmask) : 0;
+    return __shfl_sync(0xffffffffu, x, best);
+}
+
+// Lanczos check state in shared memory (offsets from oShd): results, the
+// bookkeeping of lanczos_reg kept out of registers, and the decision.
+enum : int { CK_TTOP = 0, CK_RTOP = 1, CK_TBOT = 2, CK_RBOT = 3, CK_TNORM = 10 /* 2 slots (parity) */,
+             CK_GHI = 12, CK_GLO = 13, CK_INTOP = 14, CK_INBOT = 15, CK_LRES = 16, CK_JPREV = 17, CK_NEXT = 18,
+             CK_DONE = 19 };
+
+// Lanczos convergence check, run by warp 0 (lane 0 does the bookkeeping): Ritz
+// value(s) by the warp-parallel Laguerre between the inner bound (previous Ritz
+// value or max/min alpha) and Gershgorin, residual be[J-1] |s_J| by the
+// backward recurrence; converged when <= 1e-14 |T_J| (or exhausted); else the
+// next check is predicted from the observed linear rate (<= 8 iterations on).
+// Out of line: one warp works while the CTA waits.
+__device__ __noinline__ void lanczos_check(const int tid, const int oAl, const int oBe, const int oB2, const int oRbe,
+                                           const int J, const double beta, const double tnorm, const bool need_bot,
+                                           const bool exhausted, const int md, const int oShd) {
+    extern __shared__ __align__(16) double sm[];
+    if ((tid >> 5) != 0) return;
+    const int lane = tid & 31;
+    const double th = tri_laguerre_warp(oAl, oB2, J, sm[oShd + CK_INTOP], sm[oShd + CK_GHI] + 1e-13 * tnorm, true,
+                                        lane);
+    double thb = SW_INF;
+    if (need_bot)
+        thb = tri_laguerre_warp(oAl, oB2, J, sm[oShd + CK_INBOT], sm[oShd + CK_GLO] - 1e-13 * tnorm, false, lane);
+    if (lane != 0) return;
+    const double res = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
+    const double resb = need_bot ? beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, thb) : 0.0;
+    sm[oShd + CK_TTOP] = th;
+    sm[oShd + CK_RTOP] = res;
+    sm[oShd + CK_TBOT] = thb;
+    sm[oShd + CK_RBOT] = resb;
+    const double tol = 1e-14 * tnorm;
+    const bool done = exhausted || (res <= tol && resb <= tol);
+    sm[oShd + CK_DONE] = done ? 1.0 : 0.0;
+    if (done) return;
+    // Ritz values of T_J are inner bounds for those of every larger T
+    sm[oShd + CK_INTOP] = fmax(sm[oShd + CK_INTOP], th);
+    if (need_bot) sm[oShd + CK_INBOT] = fmin(sm[oShd + CK_INBOT], thb);
+    const double lres = log(fmax(res, resb));
+    const int jprev = (int)sm[oShd + CK_JPREV];
+    const double lres_prev = sm[oShd + CK_LRES];
+    int step = 8;
+    if (jprev > 0 && lres < lres_prev) {
+        const double rate = (lres_prev - lres) / (double)(J - jprev);
+        step = (int)ceil((lres - log(tol)) / rate);
+        step = max(1, min(8, step));
+    }
+    sm[oShd + CK_JPREV] = (double)J;
+    sm[oShd + CK_LRES] = lres;
+    sm[oShd + CK_NEXT] = (double)min(md, J + step);
 }
 
 // K2 vector slots (length vl = mp + 8 each) in the shared vector area
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
 
-template <int NT, int KC>
+template <int NT, int KC, bool GM = false>
 __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
                                            const bool need_bot, const int oVec, const int vl, const int oRed,
-                                           unsigned long long* prof) {
+                                           const int jhint, unsigned long long* prof, const double* __restrict__ Mg = nullptr,
+                                           int oQTin = -1) {
     // everything addressed as offsets into the dynamic shared memory (32-bit LDS/STS)
     extern __shared__ __align__(16) double sm[];
     static_assert(KC <= NT / 32, "M row segment of a thread: 8 KC columns <= NT / 4 rows");
@@ -880,12 +1016,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     const int oWp = oWu + 2 * (mdp + 8);
     const int oRB = oRed + 16;         // per-warp partial norms
     const int oShd = oRed + 32;        // check results (4) and thetas (2)
-    const int oQT = oM;                // transposed basis, in M's space once M is in registers
+    // transposed basis: in M's shared space once M is in registers, or a given region
+    const int oQT = (oQTin >= 0) ? oQTin : oM;
     const int r = tid >> 2, g = tid & 3;
     const bool rowok = r < md;
     const bool owner = (g == 0) && (r < mdp);
     double2 mr[KC];
-    {
+    if (GM) {  // M rows straight from global memory (K2b): all loads of a thread in flight at once
+        const double* Mr = Mg + (size_t)(r < mdp ? r : 0) * ld;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const int c = 2 * g + 8 * k;
+            mr[k] = (r < mdp && c < mdp) ? __ldg(reinterpret_cast<const double2*>(Mr + c)) : make_double2(0.0, 0.0);
+        }
+    } else {
         const int oMr = oM + (r < mdp ? r : 0) * ld;
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
@@ -911,12 +1055,22 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
 #pragma unroll
     for (int w = 0; w < NW; ++w) nn0 += sm[oRB + w];
     double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
-    double tnorm = 0.0, ghi = -SW_INF, glo = SW_INF, bjm1 = 0.0;
+    double bjm1 = 0.0;
     int next_check = max(min(md, 12), (md * 2) / 5);
-    int jprev = 0;
-    double lres_prev = 0.0;
+    (void)jhint;  // a per-chain hint was measured to raise J (consecutive calls differ): unused
     int J = 0;
-    double th_top = -SW_INF, th_bot = SW_INF, warm_top = SW_INF, warm_bot = -SW_INF;
+    if (tid == 0) {  // bookkeeping of the checks lives in shared memory (register pressure)
+        sm[oShd + CK_TNORM] = 0.0;
+        sm[oShd + CK_TNORM + 1] = 0.0;
+        sm[oShd + CK_GHI] = -SW_INF;
+        sm[oShd + CK_GLO] = SW_INF;
+        sm[oShd + CK_INTOP] = -SW_INF;
+        sm[oShd + CK_INBOT] = SW_INF;
+        sm[oShd + CK_JPREV] = 0.0;
+        sm[oShd + CK_LRES] = 0.0;
+        sm[oShd + CK_TTOP] = -SW_INF;
+        sm[oShd + CK_TBOT] = SW_INF;
+    }
 #if SW_PROF_LANCZOS
     long long c_mv = 0, c_dot = 0, c_upd = 0, c_chk = 0, c_t = clock64();
 #define SW_LZ_STAMP(acc) if (prof) { long long c = clock64(); acc += c - c_t; c_t = c; }
@@ -953,6 +1107,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             const double q = wr * sj;  // q_j (wr = u_j[r])
             sm[oQ + j * ld + r] = q;
             sm[oQT + r * ld + j] = q;
+            sm[oQT + r * ld + j + 1] = 0.0;  // the update reads pairs (i, i + 1): never stale (NaN) data
             sm[oWp + r] = wpr;
         }
         __syncthreads();
@@ -1027,38 +1182,27 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             sm[oB2 + j] = nn;
             sm[oRbe + j] = 1.0 / beta;
         }
-        tnorm = fmax(tnorm, fabs(alpha) + beta + bjm1);
-        ghi = fmax(ghi, alpha + beta + bjm1);
-        glo = fmin(glo, alpha - beta - bjm1);
+        // |T| bound: the previous iteration's value (parity slot) and this row
+        const double tnorm = fmax(j > 0 ? sm[oShd + CK_TNORM + ((j - 1) & 1)] : 0.0, fabs(alpha) + beta + bjm1);
+        if (tid == 0) {
+            sm[oShd + CK_TNORM + (j & 1)] = tnorm;
+            sm[oShd + CK_GHI] = fmax(sm[oShd + CK_GHI], alpha + beta + bjm1);
+            sm[oShd + CK_GLO] = fmin(sm[oShd + CK_GLO], alpha - beta - bjm1);
+            sm[oShd + CK_INTOP] = fmax(sm[oShd + CK_INTOP], alpha);  // Rayleigh quotients: inner bounds
+            sm[oShd + CK_INBOT] = fmin(sm[oShd + CK_INBOT], alpha);
+        }
         bjm1 = beta;
         sj = 1.0 / beta;
         J = j + 1;
         const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
         SW_LZ_STAMP(c_upd)
         if (exhausted || J >= next_check) {
-            __syncthreads();  // al / be / b2 / rbe of this step visible
-            lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, ghi, glo, tnorm, need_bot, warm_top, warm_bot, oShd);
+            __syncthreads();  // al / be / b2 / rbe and the bookkeeping of this step visible
+            lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, tnorm, need_bot, exhausted, md, oShd);
             __syncthreads();
-            const double res = sm[oShd + 1], resb = need_bot ? sm[oShd + 3] : 0.0;
-            th_top = sm[oShd + 0];
-            th_bot = need_bot ? sm[oShd + 2] : SW_INF;
             SW_LZ_STAMP(c_chk)
-            const double tol = 1e-14 * tnorm;
-            if (exhausted || (res <= tol && resb <= tol)) break;
-            // warm bounds for the next check (the extreme eigenvalue of M lies within res of the Ritz value)
-            warm_top = th_top + 1.001 * res + 1e-13 * tnorm;
-            warm_bot = th_bot - 1.001 * resb - 1e-13 * tnorm;
-            // predict the crossing from the observed linear rate
-            const double lres = log(fmax(res, resb));
-            int step = 8;
-            if (jprev > 0 && lres < lres_prev) {
-                const double rate = (lres_prev - lres) / (double)(J - jprev);
-                step = (int)ceil((lres - log(tol)) / rate);
-                step = max(1, min(8, step));
-            }
-            jprev = J;
-            lres_prev = lres;
-            next_check = min(md, J + step);
+            if (sm[oShd + CK_DONE] != 0.0) break;
+            next_check = (int)sm[oShd + CK_NEXT];
         }
     }
 #if SW_PROF_LANCZOS
@@ -1072,9 +1216,10 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
 #undef SW_LZ_STAMP
     (void)prof;
     __syncthreads();
+    const double th_top = sm[oShd + CK_TTOP];
     if (tid == 0) {
         sm[oShd + 4] = th_top;
-        sm[oShd + 5] = th_bot;
+        sm[oShd + 5] = sm[oShd + CK_TBOT];
     }
     // top Ritz vector of T_J (z = Q sv, Q orthonormal)
     Team T;
@@ -1232,8 +1377,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordPa
                 {
                     // vector area + 64 slack doubles: [0,32) partial sums, [32,40) check results
                     const int oVec = (int)(vec - smem_dyn), oRed = oVec + NVEC2 * vl;
+                    const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
                     J = lanczos_reg<NT, KC>((int)(B - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
-                                            vl, oRed, P.prof);
+                                            vl, oRed, jhint, P.prof);
+                    if (P.jlast && T.tid == 0) P.jlast[slot] = J;
                     theta_max = smem_dyn[oRed + 32 + 4];
                     theta_min = smem_dyn[oRed + 32 + 5];
                 }

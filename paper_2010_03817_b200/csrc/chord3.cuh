@@ -1,0 +1,339 @@
+// chord3.cuh -- K2 split into three kernels per scheduler round (m <= 128):
+//
+//   K2a factor_kernel   unpack A(x), A(v); Schur deflation of a boundary start
+//                       (R6); L L^T = A(x) (blocked Cholesky, DMMA
+//                       trailing updates); M = -L^{-1} A(v) L^{-T} (two blocked
+//                       TRSMs) -> M, L, deflation data to per-slot work buffers
+//   K2b lanczos_kernel  theta_max (theta_min in oracle mode) of M by the
+//                       register-resident Lanczos (lanczos_reg); z = Q s
+//   K2c tail_kernel     y = L^{-T} z, the deflation back-transform, then the
+//                       closed-form cube / ball constraints, selection, advance
+//                       and step logic (chord_tail.inc)
+//
+// Same mathematics as chord_kernel2 (Alg. 2, Lemma 3
+// P:587-651, the Cholesky-transformed pencil of P:1207-1215, the PEP
+// eigenvector y = L^{-T} z of P:784-791).  The split gives each phase the whole
+// register file (the fused kernel spilled the Lanczos loop to local memory) and
+// its own launch shape; the work buffers cost ~4 x 86 KB of HBM traffic per
+// chain-call at m = 100 (~3% of a round).
+#pragma once
+#include "chord2.cuh"
+
+namespace sw {
+
+// per-slot scalar/vector area (doubles), vl = mp + 8
+enum : int { S_A = 0, S_BH = 1, S_MD = 2, S_ST = 3, S_TMAX = 4, S_TMIN = 5, S_DEG = 6, S_J = 7, S_VEC = 8 };
+enum : int { ST_OUTWARD = 1, ST_FAILED = 2, ST_DEFL = 4 };
+__host__ __device__ __forceinline__ long long s_stride(int mp) { return S_VEC + 4LL * (mp + 8); }
+
+// ---------------------------------------------------------------- K2a
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
+    extern __shared__ __align__(16) double smem_dyn[];
+    Team T;
+    T.tid = threadIdx.x;
+    T.nthr = NT;
+    T.lane = T.tid & 31;
+    T.warp = T.tid >> 5;
+    T.nwarps = NT >> 5;
+    __shared__ double red[64];
+    __shared__ int sh_i[8];
+    const int m = P.m, ld = P.ld;
+    const int mp = (m + 7) & ~7;
+    const int vl = mp + 8;
+    double* G = smem_dyn;
+    double* B = G + (size_t)mp * ld;
+    double* vec = B + (size_t)mp * ld;
+    double* uu = vec + V_UU * vl;
+    double* hh = vec + V_HH * vl;
+    double* pw = vec + V_PW * vl;
+    double* rdiag = vec + V_RDIAG * vl;
+    double* yy = vec + V_YY * vl;
+    double* bv = vec + V_BV * vl;
+
+    const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
+    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
+        const int slot = P.list ? P.list[rr] : rr;
+        if (slot < 0) continue;
+        if (P.mode == 0 && (P.flags[slot] & CF_DONE)) continue;
+        const double* av = P.AV + (size_t)slot * P.mtp;
+        const double* ax = P.AX + (size_t)slot * P.mtp;
+        double* S = P.wS + (size_t)slot * P.w_sstride;
+        const int bnd = P.bound[slot];
+        __syncthreads();
+        unpack_sym(T, ax, G, m, ld);
+        unpack_sym(T, av, B, m, ld);
+        const bool defl = (bnd == 0);
+        if (defl)
+            for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
+        __syncthreads();
+        int md = m;
+        double a_schur = 0.0, beta_h = 0.0;
+        bool outward = false;
+        if (defl) {
+            double nu = 0.0;
+            for (int i = T.tid; i < m; i += T.nthr) nu += uu[i] * uu[i];
+            nu = sqrt(block_sum(T, nu, red));
+            for (int i = T.tid; i < m; i += T.nthr) hh[i] = uu[i] / nu;
+            __syncthreads();
+            if (T.tid == 0) hh[0] += (hh[0] >= 0.0 ? 1.0 : -1.0);
+            __syncthreads();
+            double h2 = 0.0;
+            for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
+            beta_h = 2.0 / block_sum(T, h2, red);
+            householder_congruence2(T, G, B, m, ld, hh, beta_h, pw, yy, red);
+            a_schur = B[0];
+            outward = !(a_schur > 0.0);
+            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld];
+            __syncthreads();
+            // Schur complement + shift the (1..m-1) block to (0..m-2)
+            md = m - 1;
+            for (int i0 = 0; i0 < md; i0 += T.nwarps) {
+                constexpr int CMAX = 8;
+                double gv[CMAX], bvv[CMAX];
+                const int i = i0 + T.warp;
+#pragma unroll
+                for (int c = 0; c < CMAX; ++c) {
+                    int jx = T.lane + 32 * c;
+                    if (i < md && jx < md) {
+                        gv[c] = G[(i + 1) * ld + jx + 1];
+                        bvv[c] = outward ? 0.0 : B[(i + 1) * ld + jx + 1] - bv[i] * bv[jx] / a_schur;
+                    }
+                }
+                __syncthreads();
+#pragma unroll
+                for (int c = 0; c < CMAX; ++c) {
+                    int jx = T.lane + 32 * c;
+                    if (i < md && jx < md) {
+                        G[i * ld + jx] = gv[c];
+                        B[i * ld + jx] = bvv[c];
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const int mdp = (md + 7) & ~7;
+        for (int i = md + T.warp; i < mdp; i += T.nwarps)
+            for (int j = T.lane; j < mdp; j += 32) {
+                G[i * ld + j] = (i == j) ? 1.0 : 0.0;
+                G[j * ld + i] = (i == j) ? 1.0 : 0.0;
+                B[i * ld + j] = 0.0;
+                B[j * ld + i] = 0.0;
+            }
+        __syncthreads();
+        int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
+        if (!outward && md >= 1) {
+            const bool okc = cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2]);
+            if (!okc) {
+                status |= ST_FAILED;
+            } else {
+                trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
+                trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
+                double* Mw = P.wM + (size_t)slot * P.w_mstride;
+                double* Lw = P.wL + (size_t)slot * P.w_mstride;
+                for (int i = T.warp; i < mdp; i += T.nwarps)
+                    for (int jx = T.lane; jx < mdp; jx += 32) {
+                        Mw[i * ld + jx] = -0.5 * (B[i * ld + jx] + B[jx * ld + i]);
+                        if (jx <= i) Lw[i * ld + jx] = G[i * ld + jx];
+                    }
+            }
+        }
+        // scalars and vectors of the slot
+        if (T.tid == 0) {
+            S[S_A] = a_schur;
+            S[S_BH] = beta_h;
+            S[S_MD] = (double)md;
+            S[S_ST] = (double)status;
+        }
+        for (int i = T.tid; i < mp; i += T.nthr) {
+            S[S_VEC + i] = hh[i];
+            S[S_VEC + vl + i] = bv[i];
+            S[S_VEC + 2 * vl + i] = rdiag[i];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2b
+template <int NT, int KC>
+__global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
+    extern __shared__ __align__(16) double smem_dyn[];
+    const int m = P.m, ld = P.ld;
+    const int mp = (m + 7) & ~7;
+    const int vl = mp + 8;
+    // Q (rows of ld), QT (rows of ld), vector area (NVEC2 slots) + 64 slack
+    const int oQ = 0, oQT = mp * ld, oVec = 2 * mp * ld, oRed = oVec + NVEC2 * vl;
+    const int tid = threadIdx.x;
+    __shared__ int sh_deg;
+    const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
+    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
+        const int slot = P.list ? P.list[rr] : rr;
+        if (slot < 0) continue;
+        if (P.mode == 0 && (P.flags[slot] & CF_DONE)) continue;
+        double* S = P.wS + (size_t)slot * P.w_sstride;
+        const int status = (int)S[S_ST];
+        const int md = (int)S[S_MD];
+        __syncthreads();
+        if ((status & (ST_OUTWARD | ST_FAILED)) || md < 1) {
+            if (tid == 0) {
+                S[S_TMAX] = -SW_INF;
+                S[S_TMIN] = SW_INF;
+                S[S_DEG] = 0.0;
+            }
+            continue;
+        }
+        const int mdp = (md + 7) & ~7;
+        const double* Mw = P.wM + (size_t)slot * P.w_mstride;
+        const int J = lanczos_reg<NT, KC, true>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, 0, P.prof, Mw, oQT);
+        const double theta_max = smem_dyn[oRed + 32 + 4];
+        const double theta_min = smem_dyn[oRed + 32 + 5];
+        const double* al = smem_dyn + oVec + V_AL * vl;
+        const double* be = smem_dyn + oVec + V_BE * vl;
+        const double* sv = smem_dyn + oVec + V_SV * vl;
+        if (tid == 0) {
+            const double th2 = theta_max - 1e-12 * fabs(theta_max);
+            const int c = sturm_below(al, be, J, th2);
+            sh_deg = (md >= 2 && J >= 2 && c <= J - 2) ? 1 : 0;
+        }
+        // z = Q s (rows of Q are the normalised Lanczos vectors)
+        double* zg = S + S_VEC + 3 * vl;
+        if (theta_max > 0.0) {
+            for (int e = tid; e < mdp; e += NT) {
+                double s0 = 0.0, s1 = 0.0;
+                int i = 0;
+                for (; i + 1 < J; i += 2) {
+                    s0 = fma(sv[i], smem_dyn[oQ + i * ld + e], s0);
+                    s1 = fma(sv[i + 1], smem_dyn[oQ + (i + 1) * ld + e], s1);
+                }
+                if (i < J) s0 = fma(sv[i], smem_dyn[oQ + i * ld + e], s0);
+                zg[e] = s0 + s1;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            S[S_TMAX] = theta_max;
+            S[S_TMIN] = theta_min;
+            S[S_DEG] = (double)sh_deg;
+            S[S_J] = (double)J;
+            if (P.prof) atomicAdd(&P.prof[10], (unsigned long long)J);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K2c
+template <int NT>
+__global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
+    extern __shared__ __align__(16) double smem_dyn[];
+    Team T;
+    T.tid = threadIdx.x;
+    T.nthr = NT;
+    T.lane = T.tid & 31;
+    T.warp = T.tid >> 5;
+    T.nwarps = NT >> 5;
+    __shared__ double red[64];
+    __shared__ int sh_i[8];
+    __shared__ double sh_d[16];
+    const int m = P.m, n = P.n, ld = P.ld;
+    const int mp = (m + 7) & ~7;
+    const int vl = mp + 8;
+    double* G = smem_dyn;  // L (lower)
+    double* vec = G + (size_t)mp * ld;
+    double* zz = vec + 0 * vl;
+    double* yy = vec + 1 * vl;
+    double* hh = vec + 2 * vl;
+    double* bv = vec + 3 * vl;
+    double* rdiag = vec + 4 * vl;
+    const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
+    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
+        const int slot = P.list ? P.list[rr] : rr;
+        if (slot < 0) continue;
+        if (P.mode == 0 && (P.flags[slot] & CF_DONE)) continue;
+        const long long gidv = P.gid ? P.gid[slot] : P.chain_base + slot;
+        double* x = P.X + (size_t)slot * P.np;
+        double* v = P.V + (size_t)slot * P.np;
+        const double* av = P.AV + (size_t)slot * P.mtp;
+        double* ax = P.AX + (size_t)slot * P.mtp;
+        const int bnd = P.bound[slot];
+        const double* S = P.wS + (size_t)slot * P.w_sstride;
+        const int status = (int)S[S_ST];
+        const int md = (int)S[S_MD];
+        const double a_schur = S[S_A], beta_h = S[S_BH];
+        const double theta_max = S[S_TMAX], theta_min = S[S_TMIN];
+        const bool degenerate = S[S_DEG] != 0.0;
+        const bool outward = (status & ST_OUTWARD) != 0;
+        const bool failed = (status & ST_FAILED) != 0;
+        const bool defl = (bnd == 0);
+        long long t_prof = clock64();
+        __syncthreads();
+        if (!outward && !failed && md >= 1 && theta_max > 0.0) {
+            const int mdp = (md + 7) & ~7;
+            const double* Lw = P.wL + (size_t)slot * P.w_mstride;
+            for (int i = T.warp; i < mdp; i += T.nwarps)
+                for (int jx = T.lane; jx <= i; jx += 32) G[i * ld + jx] = Lw[i * ld + jx];
+            for (int i = T.tid; i < mdp; i += T.nthr) {
+                zz[i] = S[S_VEC + 3 * vl + i];
+                rdiag[i] = S[S_VEC + 2 * vl + i];
+            }
+            if (defl)
+                for (int i = T.tid; i < m; i += T.nthr) {
+                    hh[i] = S[S_VEC + i];
+                    bv[i] = S[S_VEC + vl + i];
+                }
+            __syncthreads();
+            // y = L^{-T} z, blocked backwards over 8-row blocks
+            for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
+                const int k0 = kb * 8;
+                if (T.warp == 0) {
+                    const int r = T.lane;
+                    double zr = (r < 8) ? zz[k0 + r] : 0.0;
+#pragma unroll
+                    for (int c = 7; c >= 0; --c) {
+                        const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
+                        if (r == c) zr = yc;
+                        else if (r < c) zr -= G[(k0 + c) * ld + k0 + r] * yc;
+                    }
+                    if (r < 8) yy[k0 + r] = zr;
+                }
+                __syncthreads();
+                for (int i = T.tid; i < k0; i += T.nthr) {
+                    double acc = zz[i];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) acc -= G[(k0 + c) * ld + i] * yy[k0 + c];
+                    zz[i] = acc;
+                }
+                __syncthreads();
+            }
+            if (T.warp == 0) {
+                if (defl) {  // y = H [ -b^T yh / a ; yh ]
+                    double s = 0.0;
+                    for (int i = T.lane; i < md; i += 32) s += bv[i] * yy[i];
+                    s = warp_sum(s);
+                    double alpha0 = -s / a_schur;
+                    __syncwarp();
+                    for (int base_i = md - 1; base_i >= 0; base_i -= 32) {
+                        int i = base_i - T.lane;
+                        double val = (i >= 0) ? yy[i] : 0.0;
+                        __syncwarp();
+                        if (i >= 0) yy[i + 1] = val;
+                        __syncwarp();
+                    }
+                    if (T.lane == 0) yy[0] = alpha0;
+                    __syncwarp();
+                    double hy = 0.0;
+                    for (int i = T.lane; i < m; i += 32) hy += hh[i] * yy[i];
+                    hy = warp_sum(hy) * beta_h;
+                    for (int i = T.lane; i < m; i += 32) yy[i] -= hy * hh[i];
+                    __syncwarp();
+                }
+                double yn = 0.0;
+                for (int i = T.lane; i < m; i += 32) yn += yy[i] * yy[i];
+                yn = sqrt(warp_sum(yn));
+                for (int i = T.lane; i < m; i += 32) yy[i] /= yn;
+            }
+            __syncthreads();
+        }
+#include "chord_tail.inc"
+    }
+}
+
+}  // namespace sw

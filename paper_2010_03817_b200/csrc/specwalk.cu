@@ -19,6 +19,7 @@
 #include "gemm.cuh"
 #include "walk.cuh"
 #include "chord2.cuh"
+#include "chord3.cuh"
 #include "hmc.cuh"
 #include "estimators.cuh"
 #include <algorithm>
@@ -47,6 +48,8 @@ struct ChainBuf {
     double *X = nullptr, *Xs = nullptr, *V = nullptr, *AX = nullptr, *AXs = nullptr, *AV = nullptr, *Yh = nullptr,
            *U = nullptr, *Gn = nullptr, *ell = nullptr, *tlast = nullptr;
     int *steps_done = nullptr, *refl = nullptr, *bound = nullptr, *flags = nullptr, *nrej = nullptr, *ndeg = nullptr;
+    int* jlast = nullptr;
+    double *wM = nullptr, *wL = nullptr, *wS = nullptr;  // K2 split work buffers
     long long *calls = nullptr, *nrefl = nullptr;
     int *list = nullptr, *list2 = nullptr, *nlist = nullptr;
     int* counters = nullptr;  // [0] count, [1] count2, [2] ncount
@@ -78,6 +81,9 @@ struct spec_ctx {
     int scratch_ctas = 0;
     bool smem_path = true;
     int k2_variant = 0;
+    int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
+    int f_grid = 0, l_grid = 0, t_grid = 0;
+    size_t f_smem = 0, l_smem = 0, t_smem = 0;
     size_t smem_bytes = 0;
     int chord_threads = 256;
     int chord_grid_max = 0;
@@ -95,7 +101,7 @@ struct spec_ctx {
 
 static void free_chains(ChainBuf& b) {
     void* ps[] = {b.X, b.Xs, b.V, b.AX, b.AXs, b.AV, b.Yh, b.U, b.Gn, b.ell, b.tlast, b.steps_done, b.refl, b.bound,
-                  b.flags, b.nrej, b.ndeg, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid};
+                  b.flags, b.nrej, b.ndeg, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid, b.jlast, b.wM, b.wL, b.wS};
     for (void* p : ps)
         if (p) cudaFree(p);
     b = ChainBuf();
@@ -120,7 +126,11 @@ static int ensure_chains(spec_ctx* ctx, long long C) {
     ZA(X, cap * np) ZA(Xs, cap * np) ZA(V, cap * np) ZA(Gn, cap * np) ZA(AX, cap * mtp) ZA(AXs, cap * mtp)
     ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(tlast, cap) ZA(steps_done, cap) ZA(refl, cap)
     ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
-    ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap)
+    ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap) ZA(jlast, cap)
+    if (ctx->k2_split) {
+        const size_t mp = (size_t)roundup(ctx->m, 8);
+        ZA(wM, cap * mp * ctx->ld) ZA(wL, cap * mp * ctx->ld) ZA(wS, cap * (size_t)s_stride((int)mp))
+    }
 #undef ZA
     if (e != cudaSuccess) {
         free_chains(b);
@@ -251,6 +261,34 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
         ctx->smem_bytes = 0;
     }
+    // K2 split (chord3.cuh) for 64 < m <= 128 unless SPECWALK_K2_FUSED is set (for m <= 64 the
+    // fused kernel was measured faster: 1.9M vs 1.4M calls/s at m = 40; it does not spill there)
+    if ((ctx->k2_variant == 1 || ctx->k2_variant == 3) && !getenv("SPECWALK_K2_FUSED")) {
+        ctx->k2_split = 1;
+        ctx->f_smem = ctx->smem_bytes;
+        ctx->l_smem = ctx->smem_bytes;
+        ctx->t_smem = sizeof(double) * ((size_t)mp * ctx->ld + 5 * (size_t)(mp + 8) + 64);
+        int of = 0, ol = 0, ot = 0;
+#define SW_SPLIT_SETUP(NT_, KC_)                                                                                     \
+    CK(cudaFuncSetAttribute(factor_kernel<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->f_smem));     \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, factor_kernel<NT_>, NT_, ctx->f_smem));                     \
+    CK(cudaFuncSetAttribute(lanczos_kernel<NT_, KC_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->l_smem)); \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ol, lanczos_kernel<NT_, KC_>, NT_, ctx->l_smem));
+        if (ctx->k2_variant == 0) {
+            SW_SPLIT_SETUP(256, 8)
+        } else if (ctx->k2_variant == 1) {
+            SW_SPLIT_SETUP(512, 13)
+        } else {
+            SW_SPLIT_SETUP(512, 16)
+        }
+#undef SW_SPLIT_SETUP
+        CK(cudaFuncSetAttribute(tail_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->t_smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, tail_kernel<256>, 256, ctx->t_smem));
+        if (of < 1 || ol < 1 || ot < 1) return fail(SPEC_ECUDA, "K2 split kernels cannot be resident");
+        ctx->f_grid = of * ctx->num_sms;
+        ctx->l_grid = ol * ctx->num_sms;
+        ctx->t_grid = ot * ctx->num_sms;
+    }
     ctx->lsave_stride = (long long)mp * ctx->ld;
     CK(zalloc(&ctx->lsave, (size_t)ctx->lsave_stride * ctx->chord_grid_max));
     *out = ctx;
@@ -345,10 +383,32 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.Ac = ctx->Ac;
     P.cvec = ctx->c;
     P.tlast = b.tlast;
+    P.jlast = b.jlast;
+    P.wM = b.wM;
+    P.wL = b.wL;
+    P.wS = b.wS;
+    P.w_mstride = (long long)roundup(ctx->m, 8) * ctx->ld;
+    P.w_sstride = s_stride(roundup(ctx->m, 8));
     return P;
 }
 
 static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
+    if (ctx->k2_split) {
+        auto g = [&](int gmax) { return std::max(1, std::min(count_host, gmax)); };
+        if (ctx->k2_variant == 0) {
+            factor_kernel<256><<<g(ctx->f_grid), 256, ctx->f_smem, ctx->stream>>>(P);
+            lanczos_kernel<256, 8><<<g(ctx->l_grid), 256, ctx->l_smem, ctx->stream>>>(P);
+        } else if (ctx->k2_variant == 1) {
+            factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            lanczos_kernel<512, 13><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
+        } else {
+            factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            lanczos_kernel<512, 16><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
+        }
+        tail_kernel<256><<<g(ctx->t_grid), 256, ctx->t_smem, ctx->stream>>>(P);
+        ctx->launches += 3;
+        return;
+    }
     int grid = count_host < ctx->chord_grid_max ? count_host : ctx->chord_grid_max;
     if (grid < 1) grid = 1;
     if (ctx->k2_variant == 0)
@@ -556,6 +616,7 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     CK(cudaMemsetAsync(b.ndeg, 0, sizeof(int) * C, ctx->stream));
     CK(cudaMemsetAsync(b.calls, 0, sizeof(long long) * C, ctx->stream));
     CK(cudaMemsetAsync(b.nrefl, 0, sizeof(long long) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.jlast, 0, sizeof(int) * C, ctx->stream));
     {
         std::vector<int> bnd(C, SW_BIND_NONE_DEV);
         CK(cudaMemcpyAsync(b.bound, bnd.data(), sizeof(int) * C, cudaMemcpyHostToDevice, ctx->stream));
@@ -1075,6 +1136,9 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         X.assign((size_t)Cl * n, 0.0);
         spec_walk_stats st;
         rc2 = walk_entry(ctx, &p, X0.data(), 1, nullptr, nullptr, X.data(), &st, true);
+        if (getenv("SPECWALK_DEBUG_VOLUME"))
+            fprintf(stderr, "[volume] walk r=%.6g tag=%08x chains=%lld steps=%lld rc=%d calls=%lld failures=%lld\n", r,
+                    tag, Cl, steps, rc2, (long long)st.calls, (long long)st.failures);
         calls += st.calls;
         return rc2;
     };
