@@ -1,0 +1,186 @@
+// chol_inv.cuh -- blocked Cholesky that also keeps the inverses of its 8 x 8
+// diagonal blocks, and the two triangular solves of the congruence
+// M = -L^{-1} A(v) L^{-T} built on them, so that every
+// block operation is an FP64 tensor-core (DMMA m8n8k4) product:
+//   panel      L_ik   = A_ik L_kk^{-T}            (was: 8 x 8 substitution per row,
+//                                                  a 36-deep chain of 24-cycle FMAs)
+//   TRSM step  B_k    = L_kk^{-1} B_k             (was: 8 x 8 substitution per column)
+//   updates    A_ij  -= L_ik L_jk^T, B_i -= L_ik B_k  (DMMA, unchanged)
+// The 8 x 8 diagonal factor and its inverse are computed by warp 0 in registers
+// (lane r < 8 holds row r); the inverse is the forward substitution L X = I.
+// Same arithmetic as the substitution (up to rounding order) -- results agree
+// with the oracle's unblocked Cholesky and substitutions to ~1e-15.
+#pragma once
+#include "chord2.cuh"
+
+namespace sw {
+
+// acc(8x8) = A(8x8, row-major lda) * W^T, W 8x8 row-major (ldw): C[r][c] = sum_k A[r][k] W[c][k]
+__device__ __forceinline__ void tile_mul_wt(double (&acc)[2], const double* A, int lda, const double* W, int ldw,
+                                            int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    const double a0 = A[r * lda + q], a1 = A[r * lda + 4 + q];
+    const double b0 = W[r * ldw + q], b1 = W[r * ldw + 4 + q];
+    acc[0] = 0.0;
+    acc[1] = 0.0;
+    dmma_t(acc, a0, b0);
+    dmma_t(acc, a1, b1);
+}
+
+// acc(8x8) = W(8x8 row-major, ldw) * B(8x8 at Bp, row-major ldb): C[r][c] = sum_k W[r][k] B[k][c]
+__device__ __forceinline__ void tile_mul_w(double (&acc)[2], const double* W, int ldw, const double* Bp, int ldb,
+                                           int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    const double a0 = W[r * ldw + q], a1 = W[r * ldw + 4 + q];
+    const double b0 = Bp[q * ldb + r], b1 = Bp[(4 + q) * ldb + r];
+    acc[0] = 0.0;
+    acc[1] = 0.0;
+    dmma_t(acc, a0, b0);
+    dmma_t(acc, a1, b1);
+}
+
+// Blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8),
+// rdiag = 1 / diag(L), Lv = the inverses of the 8 x 8 diagonal blocks (row-major,
+// 64 doubles per block).  Returns false on a non-positive pivot (CTA-uniform).
+__device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, double* rdiag, double* Lv,
+                                     int* flag) {
+    const int TB = n >> 3;
+    for (int kb = 0; kb < TB; ++kb) {
+        const int k0 = kb * 8;
+        double* D = G + k0 * ld + k0;
+        double* Vk = Lv + kb * 64;
+        if (T.warp == 0) {
+            const int r = T.lane;
+            double a[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) a[c] = (r < 8 && c <= r) ? D[r * ld + c] : 0.0;
+            bool ok = true;
+            double rd = 1.0;  // 1 / L_rr of this lane's row
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const double d = __shfl_sync(0xffffffffu, a[c], c);
+                if (!(d > 0.0)) ok = false;
+                const double l = sqrt(fmax(d, 1e-300));
+                const double il = 1.0 / l;
+                if (r == c) { a[c] = l; rd = il; }
+                else if (r > c) a[c] *= il;
+#pragma unroll
+                for (int k = c + 1; k < 8; ++k) {
+                    const double lkc = __shfl_sync(0xffffffffu, a[c], k);
+                    if (r >= k) a[k] = fma(-a[c], lkc, a[k]);
+                }
+            }
+            // X = L_kk^{-1}: forward substitution on L X = I, lane r owns row r of X
+            double x[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                // row k final: x_k = (e_k - acc_k) / L_kk  (acc accumulated in x of lane k)
+                if (r == k) {
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) x[c] = ((c == k ? 1.0 : 0.0) - x[c]) * rd;
+                }
+#pragma unroll
+                for (int c = 0; c <= k; ++c) {
+                    const double xkc = __shfl_sync(0xffffffffu, x[c], k);
+                    if (r > k && r < 8) x[c] = fma(a[k], xkc, x[c]);
+                }
+            }
+            if (r < 8) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (c <= r) D[r * ld + c] = a[c];
+                    Vk[r * 8 + c] = (c <= r) ? x[c] : 0.0;
+                }
+                rdiag[k0 + r] = rd;
+            }
+            if (T.lane == 0) *flag = ok ? 0 : 1;
+        }
+        __syncthreads();
+        if (*flag) return false;
+        // panel: L_ib,kb = A_ib,kb L_kk^{-T}, one 8 x 8 tile per warp (DMMA)
+        for (int ib = kb + 1 + T.warp; ib < TB; ib += T.nwarps) {
+            double* Ct = G + ib * 8 * ld + k0;
+            double acc[2];
+            tile_mul_wt(acc, Ct, ld, Vk, 8, T.lane);
+            __syncwarp();
+            const int r = T.lane >> 2, q = T.lane & 3;
+            Ct[r * ld + 2 * q] = acc[0];
+            Ct[r * ld + 2 * q + 1] = acc[1];
+        }
+        __syncthreads();
+        // trailing SYRK on DMMA tiles: G_ij -= P_i P_j^T, kb < j <= i
+        const int Tr = TB - kb - 1;
+        const int ntile = Tr * (Tr + 1) / 2;
+        for (int t = T.warp; t < ntile; t += T.nwarps) {
+            int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+            while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
+            while (ii * (ii + 1) / 2 > t) --ii;
+            const int jj = t - ii * (ii + 1) / 2;
+            const int ib = kb + 1 + ii, jb = kb + 1 + jj;
+            double* C = G + ib * 8 * ld + jb * 8;
+            const int r = T.lane >> 2, q = T.lane & 3;
+            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+        }
+        __syncthreads();
+    }
+    return true;
+}
+
+// B <- L^{-1} B on all n columns, with the inverse diagonal blocks Lv.  TR =
+// true works on the transposed view W(r, c) = B[c*ld + r] (i.e. B <- B L^{-T}).
+template <bool TR>
+__device__ void trsm_inv_blocked(const Team& T, const double* G, const double* Lv, double* B, int n, int ld) {
+    const int TB = n >> 3;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    for (int kb = 0; kb < TB; ++kb) {
+        const int k0 = kb * 8;
+        const double* Vk = Lv + kb * 64;
+        // block row kb: W_kb = L_kk^{-1} W_kb (one tile per warp)
+        for (int cb = T.warp; cb < TB; cb += T.nwarps) {
+            double acc[2];
+            if (!TR) {
+                double* Bt = B + k0 * ld + cb * 8;  // W tile (kb, cb) = B rows k0.., cols cb*8..
+                tile_mul_w(acc, Vk, 8, Bt, ld, T.lane);
+                __syncwarp();
+                Bt[r * ld + 2 * q] = acc[0];
+                Bt[r * ld + 2 * q + 1] = acc[1];
+            } else {
+                double* Bt = B + cb * 8 * ld + k0;  // W tile (kb, cb) = (B rows cb*8.., cols k0..)^T
+                tile_mul_wt(acc, Bt, ld, Vk, 8, T.lane);
+                __syncwarp();
+                Bt[r * ld + 2 * q] = acc[0];
+                Bt[r * ld + 2 * q + 1] = acc[1];
+            }
+        }
+        __syncthreads();
+        const int nt = (TB - kb - 1) * TB;
+        for (int t = T.warp; t < nt; t += T.nwarps) {
+            const int ib = kb + 1 + t / TB, cb = t % TB;
+            const double* A = G + ib * 8 * ld + k0;
+            double acc[2];
+            if (!TR) {
+                double* C = B + ib * 8 * ld + cb * 8;
+                acc[0] = C[r * ld + 2 * q];
+                acc[1] = C[r * ld + 2 * q + 1];
+                tile_msub<false>(acc, A, ld, B + k0 * ld + cb * 8, ld, 8, T.lane);
+                C[r * ld + 2 * q] = acc[0];
+                C[r * ld + 2 * q + 1] = acc[1];
+            } else {
+                double* Ct = B + cb * 8 * ld + ib * 8;
+                acc[0] = Ct[(2 * q) * ld + r];
+                acc[1] = Ct[(2 * q + 1) * ld + r];
+                tile_msub<true>(acc, A, ld, B + cb * 8 * ld + k0, ld, 8, T.lane);
+                Ct[(2 * q) * ld + r] = acc[0];
+                Ct[(2 * q + 1) * ld + r] = acc[1];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace sw

@@ -18,6 +18,7 @@
 // chain-call at m = 100 (~3% of a round).
 #pragma once
 #include "chord2.cuh"
+#include "chol_inv.cuh"
 
 namespace sw {
 
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
     double* rdiag = vec + V_RDIAG * vl;
     double* yy = vec + V_YY * vl;
     double* bv = vec + V_BV * vl;
+    double* Lv = vec + NVEC2 * vl + 64;  // inverse diagonal blocks (8 mp doubles)
 
     const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
     for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
@@ -123,12 +125,12 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         __syncthreads();
         int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
         if (!outward && md >= 1) {
-            const bool okc = cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2]);
+            const bool okc = cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
             if (!okc) {
                 status |= ST_FAILED;
             } else {
-                trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
-                trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                trsm_inv_blocked<false>(T, G, Lv, B, mdp, ld);
+                trsm_inv_blocked<true>(T, G, Lv, B, mdp, ld);
                 // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
                 double* Mw = P.wM + (size_t)slot * P.w_mstride;
                 double* Lw = P.wL + (size_t)slot * P.w_mstride;

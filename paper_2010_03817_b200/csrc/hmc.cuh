@@ -350,6 +350,11 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
             }
             continue;
         }
+        // per-chain counters read by every thread BEFORE thread 0 updates them below
+        // (a read after the update would give threads different values: a race)
+        const int refl0 = P.refl[slot];
+        const int sdone0 = P.steps_done[slot];
+        const int trk0 = (P.max_trace > 0) ? P.tr_cnt[slot] : 0;
         const double el = P.ell[slot];
         const bool accept = (el <= tplus);
         const double th = accept ? el : tplus;
@@ -359,7 +364,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
         __syncthreads();
         bool end_step = accept, reject = false;
         if (!accept) {
-            int rf = P.refl[slot] + 1;
+            int rf = refl0 + 1;
             if (T.tid == 0) {
                 P.refl[slot] = rf;
                 P.ell[slot] = el - th;
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
             }
             if (P.max_trace > 0 && !reject) {
                 __syncthreads();
-                int k = P.tr_cnt[slot];
+                int k = trk0;
                 if (k < P.max_trace) {
                     size_t o = ((size_t)slot * P.max_trace + k);
                     for (int i = T.tid; i < n; i += T.nthr) {
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
                 for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] = axs[i];
             }
             __syncthreads();
-            int sd = P.steps_done[slot] + 1;
+            int sd = sdone0 + 1;
             if (T.tid == 0) {
                 P.steps_done[slot] = sd;
                 P.refl[slot] = 0;
