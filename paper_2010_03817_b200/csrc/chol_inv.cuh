@@ -6,8 +6,10 @@
 //                                                  a 36-deep chain of 24-cycle FMAs)
 //   TRSM step  B_k    = L_kk^{-1} B_k             (was: 8 x 8 substitution per column)
 //   updates    A_ij  -= L_ik L_jk^T, B_i -= L_ik B_k  (DMMA, unchanged)
-// The 8 x 8 diagonal factor and its inverse are computed by warp 0 in registers
-// (lane r < 8 holds row r); the inverse is the forward substitution L X = I.
+// Warp 0 computes the 8 x 8 diagonal factor (rsqrt: no division) and its
+// inverse in registers (lane r < 8 holds row r; the inverse is the forward
+// substitution L X = I).  (All warps factoring it redundantly, to drop a
+// barrier, was measured slower: 16x the shuffles.)
 // Same arithmetic as the substitution (up to rounding order) -- results agree
 // with the oracle's unblocked Cholesky and substitutions to ~1e-15.
 #pragma once
@@ -60,9 +62,8 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
             for (int c = 0; c < 8; ++c) {
                 const double d = __shfl_sync(0xffffffffu, a[c], c);
                 if (!(d > 0.0)) ok = false;
-                const double l = sqrt(fmax(d, 1e-300));
-                const double il = 1.0 / l;
-                if (r == c) { a[c] = l; rd = il; }
+                const double il = rsqrt(fmax(d, 1e-300));
+                if (r == c) { a[c] = d * il; rd = il; }
                 else if (r > c) a[c] *= il;
 #pragma unroll
                 for (int k = c + 1; k < 8; ++k) {
@@ -76,7 +77,6 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
             for (int c = 0; c < 8; ++c) x[c] = 0.0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
-                // row k final: x_k = (e_k - acc_k) / L_kk  (acc accumulated in x of lane k)
                 if (r == k) {
 #pragma unroll
                     for (int c = 0; c < 8; ++c) x[c] = ((c == k ? 1.0 : 0.0) - x[c]) * rd;
@@ -110,21 +110,21 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
             Ct[r * ld + 2 * q + 1] = acc[1];
         }
         __syncthreads();
-        // trailing SYRK on DMMA tiles: G_ij -= P_i P_j^T, kb < j <= i
+        // trailing SYRK on DMMA tiles: G_ij -= P_i P_j^T, kb < j <= i (tile index walked
+        // incrementally: no divisions / square roots)
         const int Tr = TB - kb - 1;
-        const int ntile = Tr * (Tr + 1) / 2;
-        for (int t = T.warp; t < ntile; t += T.nwarps) {
-            int ii = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-            while ((ii + 1) * (ii + 2) / 2 <= t) ++ii;
-            while (ii * (ii + 1) / 2 > t) --ii;
-            const int jj = t - ii * (ii + 1) / 2;
+        int ii = 0, jj = T.warp;
+        while (ii < Tr && jj > ii) { jj -= ii + 1; ++ii; }
+        while (ii < Tr) {
             const int ib = kb + 1 + ii, jb = kb + 1 + jj;
             double* C = G + ib * 8 * ld + jb * 8;
-            const int r = T.lane >> 2, q = T.lane & 3;
-            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            const int rr = T.lane >> 2, q = T.lane & 3;
+            double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
             tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
-            C[r * ld + 2 * q] = acc[0];
-            C[r * ld + 2 * q + 1] = acc[1];
+            C[rr * ld + 2 * q] = acc[0];
+            C[rr * ld + 2 * q + 1] = acc[1];
+            jj += T.nwarps;
+            while (ii < Tr && jj > ii) { jj -= ii + 1; ++ii; }
         }
         __syncthreads();
     }
@@ -158,9 +158,11 @@ __device__ void trsm_inv_blocked(const Team& T, const double* G, const double* L
             }
         }
         __syncthreads();
-        const int nt = (TB - kb - 1) * TB;
-        for (int t = T.warp; t < nt; t += T.nwarps) {
-            const int ib = kb + 1 + t / TB, cb = t % TB;
+        int ib = kb + 1, cb = T.warp;
+        while (cb >= TB) { cb -= TB; ++ib; }
+        for (; ib < TB; cb += T.nwarps) {
+            while (cb >= TB) { cb -= TB; ++ib; }
+            if (ib >= TB) break;
             const double* A = G + ib * 8 * ld + k0;
             double acc[2];
             if (!TR) {

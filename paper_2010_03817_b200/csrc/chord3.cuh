@@ -63,12 +63,14 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         double* S = P.wS + (size_t)slot * P.w_sstride;
         const int bnd = P.bound[slot];
         __syncthreads();
+        long long t_prof = clock64();
         unpack_sym(T, ax, G, m, ld);
         unpack_sym(T, av, B, m, ld);
         const bool defl = (bnd == 0);
         if (defl)
             for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
         __syncthreads();
+        PROF_MARK(0);
         int md = m;
         double a_schur = 0.0, beta_h = 0.0;
         bool outward = false;
@@ -124,13 +126,16 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
             }
         __syncthreads();
         int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
+        PROF_MARK(1);
         if (!outward && md >= 1) {
             const bool okc = cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
+            PROF_MARK(2);
             if (!okc) {
                 status |= ST_FAILED;
             } else {
                 trsm_inv_blocked<false>(T, G, Lv, B, mdp, ld);
                 trsm_inv_blocked<true>(T, G, Lv, B, mdp, ld);
+                PROF_MARK(3);
                 // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
                 double* Mw = P.wM + (size_t)slot * P.w_mstride;
                 double* Lw = P.wL + (size_t)slot * P.w_mstride;
@@ -153,6 +158,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
             S[S_VEC + vl + i] = bv[i];
             S[S_VEC + 2 * vl + i] = rdiag[i];
         }
+        PROF_MARK(4);
     }
 }
 
