@@ -1231,7 +1231,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
 }
 
 template <int NT, bool SMEM, int KC>
-__global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
+__global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
     T.tid = threadIdx.x;

@@ -216,7 +216,14 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     ctx->ld = mp + 4;
     // K2 variants: 0 = <256, smem, KC 8> (mp <= 64), 1 = <512, smem, KC 13> (mp <= 104),
     // 3 = <512, smem, KC 16> (mp <= 128), 2 = global scratch (larger m).
-    if (mp <= 64) {
+    // small m: smaller CTAs, more chains resident per SM (4 = <128, KC 4>, 5 = <192, KC 6>)
+    if (mp <= 32) {
+        ctx->k2_variant = 4;
+        ctx->chord_threads = 128;
+    } else if (mp <= 48) {
+        ctx->k2_variant = 5;
+        ctx->chord_threads = 192;
+    } else if (mp <= 64) {
         ctx->k2_variant = 0;
         ctx->chord_threads = 256;
     } else if (mp <= 104) {
@@ -239,7 +246,11 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     CK(cudaFuncSetAttribute(chord_kernel2<NT_, true, KC_>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                             (int)ctx->smem_bytes));                                                           \
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<NT_, true, KC_>, NT_, ctx->smem_bytes));
-        if (ctx->k2_variant == 0) {
+        if (ctx->k2_variant == 4) {
+            SW_K2_SETUP(128, 4)
+        } else if (ctx->k2_variant == 5) {
+            SW_K2_SETUP(192, 6)
+        } else if (ctx->k2_variant == 0) {
             SW_K2_SETUP(256, 8)
         } else if (ctx->k2_variant == 1) {
             SW_K2_SETUP(512, 13)
@@ -411,7 +422,11 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
     }
     int grid = count_host < ctx->chord_grid_max ? count_host : ctx->chord_grid_max;
     if (grid < 1) grid = 1;
-    if (ctx->k2_variant == 0)
+    if (ctx->k2_variant == 4)
+        chord_kernel2<128, true, 4><<<grid, 128, ctx->smem_bytes, ctx->stream>>>(P);
+    else if (ctx->k2_variant == 5)
+        chord_kernel2<192, true, 6><<<grid, 192, ctx->smem_bytes, ctx->stream>>>(P);
+    else if (ctx->k2_variant == 0)
         chord_kernel2<256, true, 8><<<grid, 256, ctx->smem_bytes, ctx->stream>>>(P);
     else if (ctx->k2_variant == 1)
         chord_kernel2<512, true, 13><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
