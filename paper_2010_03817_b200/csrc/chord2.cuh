@@ -949,7 +949,7 @@ __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, co
 // bookkeeping of lanczos_reg kept out of registers, and the decision.
 enum : int { CK_TTOP = 0, CK_RTOP = 1, CK_TBOT = 2, CK_RBOT = 3, CK_TNORM = 10 /* 2 slots (parity) */,
              CK_GHI = 12, CK_GLO = 13, CK_INTOP = 14, CK_INBOT = 15, CK_LRES = 16, CK_JPREV = 17, CK_NEXT = 18,
-             CK_DONE = 19 };
+             CK_DONE = 19, CK_HINTED = 20 };
 
 // Lanczos convergence check, run by warp 0 (lane 0 does the bookkeeping): Ritz
 // value(s) by the warp-parallel Laguerre between the inner bound (previous Ritz
@@ -963,11 +963,24 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     extern __shared__ __align__(16) double sm[];
     if ((tid >> 5) != 0) return;
     const int lane = tid & 31;
-    const double th = tri_laguerre_warp(oAl, oB2, J, sm[oShd + CK_INTOP], sm[oShd + CK_GHI] + 1e-13 * tnorm, true,
-                                        lane);
+    // Gershgorin bounds (outer) and max / min alpha (inner: Rayleigh quotients of T_J)
+    double ghi = -SW_INF, glo = SW_INF, ahi = -SW_INF, alo = SW_INF;
+    for (int i = lane; i < J; i += 32) {
+        const double a = sm[oAl + i];
+        const double rs = (i > 0 ? sm[oBe + i - 1] : 0.0) + (i + 1 < J ? sm[oBe + i] : beta);
+        ghi = fmax(ghi, a + rs);
+        glo = fmin(glo, a - rs);
+        ahi = fmax(ahi, a);
+        alo = fmin(alo, a);
+    }
+    ghi = warp_max(ghi);
+    glo = warp_min(glo);
+    ahi = warp_max(ahi);
+    alo = warp_min(alo);
+    const double in_top = fmax(ahi, sm[oShd + CK_INTOP]), in_bot = fmin(alo, sm[oShd + CK_INBOT]);
+    const double th = tri_laguerre_warp(oAl, oB2, J, in_top, ghi + 1e-13 * tnorm, true, lane);
     double thb = SW_INF;
-    if (need_bot)
-        thb = tri_laguerre_warp(oAl, oB2, J, sm[oShd + CK_INBOT], sm[oShd + CK_GLO] - 1e-13 * tnorm, false, lane);
+    if (need_bot) thb = tri_laguerre_warp(oAl, oB2, J, in_bot, glo - 1e-13 * tnorm, false, lane);
     if (lane != 0) return;
     const double res = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
     const double resb = need_bot ? beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, thb) : 0.0;
@@ -985,7 +998,7 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     const double lres = log(fmax(res, resb));
     const int jprev = (int)sm[oShd + CK_JPREV];
     const double lres_prev = sm[oShd + CK_LRES];
-    int step = 8;
+    int step = (sm[oShd + CK_HINTED] != 0.0) ? 2 : 8;  // a hinted first check is close to convergence
     if (jprev > 0 && lres < lres_prev) {
         const double rate = (lres_prev - lres) / (double)(J - jprev);
         step = (int)ceil((lres - log(tol)) / rate);
@@ -1056,20 +1069,22 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     for (int w = 0; w < NW; ++w) nn0 += sm[oRB + w];
     double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
     double bjm1 = 0.0;
+    // first check: 2 before the chain's previous iteration count (consecutive calls
+    // of a chain need similar J), else at 40% of md; later checks from the observed rate
+    // (a per-chain hint from the previous call was measured to RAISE J: consecutive calls of a
+    // chain differ too much; the first check stays at 40% of md)
+    (void)jhint;
     int next_check = max(min(md, 12), (md * 2) / 5);
-    (void)jhint;  // a per-chain hint was measured to raise J (consecutive calls differ): unused
     int J = 0;
+    double tnorm = 0.0;
     if (tid == 0) {  // bookkeeping of the checks lives in shared memory (register pressure)
-        sm[oShd + CK_TNORM] = 0.0;
-        sm[oShd + CK_TNORM + 1] = 0.0;
-        sm[oShd + CK_GHI] = -SW_INF;
-        sm[oShd + CK_GLO] = SW_INF;
         sm[oShd + CK_INTOP] = -SW_INF;
         sm[oShd + CK_INBOT] = SW_INF;
         sm[oShd + CK_JPREV] = 0.0;
         sm[oShd + CK_LRES] = 0.0;
         sm[oShd + CK_TTOP] = -SW_INF;
         sm[oShd + CK_TBOT] = SW_INF;
+        sm[oShd + CK_HINTED] = 0.0;
     }
 #if SW_PROF_LANCZOS
     long long c_mv = 0, c_dot = 0, c_upd = 0, c_chk = 0, c_t = clock64();
@@ -1176,23 +1191,16 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         }
         wr = wcur;
         const double beta = sqrt(nn);
+        const double rsb = 1.0 / beta;
         if (tid == 0) {
             sm[oAl + j] = alpha;
             sm[oBe + j] = beta;
             sm[oB2 + j] = nn;
-            sm[oRbe + j] = 1.0 / beta;
+            sm[oRbe + j] = rsb;
         }
-        // |T| bound: the previous iteration's value (parity slot) and this row
-        const double tnorm = fmax(j > 0 ? sm[oShd + CK_TNORM + ((j - 1) & 1)] : 0.0, fabs(alpha) + beta + bjm1);
-        if (tid == 0) {
-            sm[oShd + CK_TNORM + (j & 1)] = tnorm;
-            sm[oShd + CK_GHI] = fmax(sm[oShd + CK_GHI], alpha + beta + bjm1);
-            sm[oShd + CK_GLO] = fmin(sm[oShd + CK_GLO], alpha - beta - bjm1);
-            sm[oShd + CK_INTOP] = fmax(sm[oShd + CK_INTOP], alpha);  // Rayleigh quotients: inner bounds
-            sm[oShd + CK_INBOT] = fmin(sm[oShd + CK_INBOT], alpha);
-        }
+        tnorm = fmax(tnorm, fabs(alpha) + beta + bjm1);
         bjm1 = beta;
-        sj = 1.0 / beta;
+        sj = rsb;
         J = j + 1;
         const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
         SW_LZ_STAMP(c_upd)

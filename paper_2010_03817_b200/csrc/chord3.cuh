@@ -192,7 +192,10 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         }
         const int mdp = (md + 7) & ~7;
         const double* Mw = P.wM + (size_t)slot * P.w_mstride;
-        const int J = lanczos_reg<NT, KC, true>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, 0, P.prof, Mw, oQT);
+        const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
+        const int J = lanczos_reg<NT, KC, true>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, jhint, P.prof, Mw,
+                                                oQT);
+        if (P.jlast && tid == 0) P.jlast[slot] = J;
         const double theta_max = smem_dyn[oRed + 32 + 4];
         const double theta_min = smem_dyn[oRed + 32 + 5];
         const double* al = smem_dyn + oVec + V_AL * vl;
