@@ -51,7 +51,29 @@ def flops_per_call(n: int, m: int, k: int = LANCZOS_K) -> dict:
     """SURVEY 8(d).2 algorithmic flops of one line boundary-oracle call that reflects."""
     contr = 2 * n * m * (m + 1)  # A(v) and normal contractions (packed symmetric)
     k2 = m ** 3 / 3 + m ** 3 + 2 * k * m * m  # Cholesky + congruence + Lanczos matvecs
-    return dict(total=contr + k2, k2=k2, k1=n * m * (m + 1), k3=n * m * (m + 1))
+    return dict(total=contr + k2, k2=k2, k1=n * m * (m + 1), k3=n * m * (m + 1), lanczos=2 * k * m * m)
+
+
+def ncu_traffic_per_launch(tag: str):
+    """DRAM bytes (read + write) of one launch of the dominant kernel, from the latest
+    committed ncu --set full summary profiles/*<tag>.txt (tools/summarize_ncu.py), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"*{tag}*.txt")))
+    if not files:
+        return None
+    vals = {}
+    units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    for line in open(files[-1]):
+        parts = [p.strip() for p in line.split("|")]
+        if len(parts) == 4 and parts[0] == "raw" and parts[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                vals[parts[1]] = float(parts[3].replace(",", "")) * units.get(parts[2], 1.0)
+            except ValueError:
+                pass
+    if len(vals) != 2:
+        return None
+    return {"bytes": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"], "unit": "B/launch",
+            "source": os.path.relpath(files[-1], ROOT)}
 
 
 def fp64_peak_tflops() -> float:
@@ -272,16 +294,31 @@ def run_ours(args):
         ms_max, calls_tot = ms, float(calls)
     value = calls_tot / (ms_max * 1e-3)
 
-    # ---- roofline of the dominant kernel (K2 chord), from its own events
+    # ---- roofline of the dominant kernel, from its own events on the library stream:
+    # K2b lanczos_kernel when K2 is split (m = 100), else the whole K2
     f = flops_per_call(N_DIM, M_DIM)
     k2_ms = kt["ms"]["K2_chord"]
     k2_launches = kt["launches"]["K2_chord"]
     k2_items = kt["k2_items"]
     k2_avg_ms = k2_ms / max(k2_launches, 1)
-    k2_flops_per_launch = f["k2"] * (k2_items / max(k2_launches, 1))
-    achieved = k2_flops_per_launch / (k2_avg_ms * 1e-3) / 1e12
+    items_per_launch = k2_items / max(k2_launches, 1)
+    k2_flops_per_launch = f["k2"] * items_per_launch
+    k2_achieved = k2_flops_per_launch / (k2_avg_ms * 1e-3) / 1e12
     peak = fp64_peak_tflops()
+    phases = kt.get("k2_phases_ms", {})
     share = {k: v / max(sum(kt["ms"].values()), 1e-9) for k, v in kt["ms"].items()}
+    tot_ms = max(sum(kt["ms"].values()), 1e-9)
+    for k, v in phases.items():
+        share[k] = v / tot_ms
+    if phases.get("K2b_lanczos", 0.0) > 0.0:
+        dom, dom_ms = "K2b lanczos_kernel<512,13>", phases["K2b_lanczos"]
+        dom_flops = f["lanczos"]
+    else:
+        dom, dom_ms, dom_flops = "K2 chord_kernel2 (fused)", k2_ms, f["k2"]
+    dom_avg_ms = dom_ms / max(k2_launches, 1)
+    achieved = dom_flops * items_per_launch / (dom_avg_ms * 1e-3) / 1e12
+    tr = ncu_traffic_per_launch("lanczos_full_ncu") if dom.startswith("K2b") else None
+    traffic = tr["bytes"] if tr else None
 
     # ---- end-to-end through the public host API (walk_sample with host buffers)
     e2e = None
@@ -358,11 +395,18 @@ def run_ours(args):
                    "chains_per_gpu": local_chains,
                    "parallelism": f"{world} GPU(s) x {local_chains} chains, sharded by global chain id"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "K2 chord_kernel",
-                     "flops_per_chain_call": f["k2"], "chain_calls_per_launch": k2_items / max(k2_launches, 1),
-                     "avg_launch_ms": k2_avg_ms,
+                     "traffic": traffic, "kernel": dom,
+                     "flops_per_chain_call": dom_flops, "chain_calls_per_launch": items_per_launch,
+                     "avg_launch_ms": dom_avg_ms,
+                     "flop_model": "SURVEY 8(d).2: Lanczos 2 k m^2 (k = 55) for K2b; K2 total m^3/3 + m^3 + 2 k m^2",
+                     "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
+                                      f"capture {tr['source'] if tr else '-'} (one 65536-chain round); algorithmic "
+                                      f"bytes = M read once, {8 * M_DIM * M_DIM * items_per_launch:.3g} B/launch"),
                      "peak_note": "fp64 FMA pipe 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (derived; measured DFMA "
                                   "36.7, cuBLAS DGEMM 35.4 TF/s, tools/fp64_peak.py)"},
+        "roofline_k2_total": {"bound": "alu", "achieved": k2_achieved, "peak": peak, "unit": "TFLOP/s",
+                              "frac": k2_achieved / peak, "flops_per_chain_call": f["k2"],
+                              "avg_launch_ms": k2_avg_ms},
         "kernel_share": share,
         "path_tflops": value * f["total"] / 1e12,
         "clocks": clk.summary(),

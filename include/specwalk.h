@@ -175,6 +175,9 @@ int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st);
  * number of chain slots K2 processed (including finished ones not yet compacted). */
 int spec_kernel_timing(spec_ctx* ctx, int enable);
 int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items);
+/* With timing enabled and K2 split into factor / Lanczos / tail kernels (64 < m <= 128): the
+ * accumulated ms of each phase (ms3[0..2], host buffer); zeros for the fused K2 variants. */
+int spec_k2_phase_times(spec_ctx* ctx, double* ms3);
 
 /* ---- estimators ----
  * Multi-rank: spec_set_comm installs an allgather of equal HOST shards in rank

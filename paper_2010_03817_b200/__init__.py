@@ -34,7 +34,7 @@ EXPORTS = (
     "spec_last_error", "spec_create", "spec_destroy", "spec_set_objective", "spec_set_ball", "boundary_oracle",
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
-    "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation",
+    "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -122,6 +122,7 @@ def load(build_if_missing: bool = True):
     l.spec_walk_stats_now.argtypes = [C.c_void_p, C.POINTER(WalkStats)]
     l.spec_kernel_timing.argtypes = [C.c_void_p, C.c_int]
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
+    l.spec_k2_phase_times.argtypes = [C.c_void_p, _dp]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
     l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
@@ -336,8 +337,11 @@ class Spectrahedron:
         items = C.c_int64()
         _check(_lib.spec_kernel_times(self._h, ms, cnt, C.byref(items)))
         names = ("K1_av_gemm", "K2_chord", "K3_normal_gemm", "K4_reflect")
+        k2 = (C.c_double * 3)()
+        _check(_lib.spec_k2_phase_times(self._h, k2))
         return dict(ms={k: ms[i] for i, k in enumerate(names)}, launches={k: cnt[i] for i, k in enumerate(names)},
-                    k2_items=items.value)
+                    k2_items=items.value,
+                    k2_phases_ms=dict(K2a_factor=k2[0], K2b_lanczos=k2[1], K2c_tail=k2[2]))
 
     def walk_trace(self, chain_ids, steps: int, L: float, rho: int, seed: int, max_refl: int,
                    kind: int = BILLIARD, T: float = 1.0) -> list:

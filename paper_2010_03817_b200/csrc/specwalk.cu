@@ -403,19 +403,23 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     return P;
 }
 
-static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host) {
+static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cudaEvent_t* sub = nullptr) {
     if (ctx->k2_split) {
         auto g = [&](int gmax) { return std::max(1, std::min(count_host, gmax)); };
         if (ctx->k2_variant == 0) {
             factor_kernel<256><<<g(ctx->f_grid), 256, ctx->f_smem, ctx->stream>>>(P);
+            if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<256, 8><<<g(ctx->l_grid), 256, ctx->l_smem, ctx->stream>>>(P);
         } else if (ctx->k2_variant == 1) {
             factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<512, 13><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
         } else {
             factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<512, 16><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
         }
+        if (sub) cudaEventRecord(sub[1], ctx->stream);
         tail_kernel<256><<<g(ctx->t_grid), 256, ctx->t_smem, ctx->stream>>>(P);
         ctx->launches += 3;
         return;
@@ -612,6 +616,7 @@ struct WalkRun {
     double ms = 0.0;
     bool timing = false;        // per-kernel CUDA-event timing
     double kms[4] = {0, 0, 0, 0};  // K1, K2, K3, K4
+    double k2ms[3] = {0, 0, 0};    // K2 split phases: factor, Lanczos, tail
     long long kcount[4] = {0, 0, 0, 0};
     long long k2_items = 0;        // chain-calls processed by K2 launches (upper bound incl. done)
 };
@@ -657,6 +662,7 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     W.rounds = 0;
     W.ms = 0.0;
     for (int i = 0; i < 4; ++i) W.kms[i] = 0.0, W.kcount[i] = 0;
+    for (int i = 0; i < 3; ++i) W.k2ms[i] = 0.0;
     W.k2_items = 0;
     CK(cudaMemcpyAsync(b.counters, &W.count, sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     ChordParams& P = W.P;
@@ -699,8 +705,8 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
     int* lists[2] = {b.list, b.list2};
     const int check = 8;
     long long done_rounds = 0;
-    // per-kernel event pool: 5 events per round, read back at each compaction sync
-    const int pool = 5 * check;
+    // per-kernel event pool: 7 events per round (K1 | K2a | K2b | K2c | K3 | K4), read back at each sync
+    const int pool = 7 * check;
     std::vector<cudaEvent_t> ev;
     if (W.timing) {
         ev.resize(pool);
@@ -712,7 +718,7 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
         for (int k = 0; k < check && W.count > 0 && (max_rounds <= 0 || done_rounds < max_rounds); ++k) {
             int* list = lists[W.cur];
             const int count = W.count;
-            cudaEvent_t* e = W.timing ? &ev[5 * k] : nullptr;
+            cudaEvent_t* e = W.timing ? &ev[7 * k] : nullptr;
             CK(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));
             if (e) CK(cudaEventRecord(e[0], ctx->stream));
             launch_gemm_av(ctx, b.V, list, b.counters, count, b.AV, nullptr);  // K1
@@ -721,7 +727,7 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             P.count_dev = b.counters;
             P.count_host = count;
             if (W.p.kind == SPEC_WALK_HMC) launch_hmc(ctx, P, count);  // K5
-            else launch_chord(ctx, P, count);                         // K2
+            else launch_chord(ctx, P, count, (e && ctx->k2_split) ? &e[5] : nullptr);  // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
             launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
             if (e) CK(cudaEventRecord(e[3], ctx->stream));
@@ -747,13 +753,23 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
         CK(cudaStreamSynchronize(ctx->stream));
         CK(cudaGetLastError());
         if (W.timing) {
-            for (int k = 0; k < kr; ++k)
+            for (int k = 0; k < kr; ++k) {
                 for (int i = 0; i < 4; ++i) {
                     float t = 0.f;
-                    CK(cudaEventElapsedTime(&t, ev[5 * k + i], ev[5 * k + i + 1]));
+                    CK(cudaEventElapsedTime(&t, ev[7 * k + i], ev[7 * k + i + 1]));
                     W.kms[i] += t;
                     W.kcount[i] += 1;
                 }
+                if (ctx->k2_split && W.p.kind != SPEC_WALK_HMC) {
+                    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+                    CK(cudaEventElapsedTime(&t0, ev[7 * k + 1], ev[7 * k + 5]));
+                    CK(cudaEventElapsedTime(&t1, ev[7 * k + 5], ev[7 * k + 6]));
+                    CK(cudaEventElapsedTime(&t2, ev[7 * k + 6], ev[7 * k + 2]));
+                    W.k2ms[0] += t0;
+                    W.k2ms[1] += t1;
+                    W.k2ms[2] += t2;
+                }
+            }
         }
         W.cur ^= 1;
     }
@@ -1015,7 +1031,15 @@ extern "C" int spec_kernel_timing(spec_ctx* ctx, int enable) {
     WalkRun& W = walk_run(ctx);
     W.timing = enable != 0;
     for (int i = 0; i < 4; ++i) W.kms[i] = 0.0, W.kcount[i] = 0;
+    for (int i = 0; i < 3; ++i) W.k2ms[i] = 0.0;
     W.k2_items = 0;
+    return SPEC_OK;
+}
+
+extern "C" int spec_k2_phase_times(spec_ctx* ctx, double* ms3) {
+    if (!ctx || !ms3) return fail(SPEC_EINVAL, "null argument");
+    WalkRun& W = walk_run(ctx);
+    for (int i = 0; i < 3; ++i) ms3[i] = W.k2ms[i];
     return SPEC_OK;
 }
 
