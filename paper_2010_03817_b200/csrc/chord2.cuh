@@ -1074,7 +1074,9 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     // (a per-chain hint from the previous call was measured to RAISE J: consecutive calls of a
     // chain differ too much; the first check stays at 40% of md)
     (void)jhint;
-    int next_check = max(min(md, 12), (md * 2) / 5);
+    // first check by size: small problems need nearly the full dimension (m = 40: J ~ 0.85 md;
+    // m <= 24: J = md), larger ones about half (m = 100: J ~ 0.5 md)
+    int next_check = (md <= 24) ? md : (md <= 64) ? (md * 4) / 5 : max(12, (md * 2) / 5);
     int J = 0;
     double tnorm = 0.0;
     if (tid == 0) {  // bookkeeping of the checks lives in shared memory (register pressure)
