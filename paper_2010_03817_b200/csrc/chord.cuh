@@ -157,7 +157,7 @@ __device__ __forceinline__ void unpack_sym(const Team& T, const double* __restri
 // ax += th * av over the packed vector, loads issued before stores
 __device__ __forceinline__ void packed_axpy(const Team& T, double* ax, const double* __restrict__ av, double th,
                                             int mt) {
-    constexpr int K = 8;
+    constexpr int K = 20;  // m = 100: 5050 / 256 threads -> every load of a thread in flight at once
     for (int e0 = 0; e0 < mt; e0 += K * T.nthr) {
         double a[K], b[K];
 #pragma unroll

@@ -231,6 +231,70 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
     }
 }
 
+// closed-form cube / ball constraints and the selection with the fixed tie order
+// (R10) -- the same arithmetic as chord_tail.inc's block, as a function so that
+// the tail kernel can run it on its last warp while the others solve for y.
+__device__ __forceinline__ void select_bound_warp(const ChordParams& P, int lane, int n, const double* x,
+                                                  const double* v, double theta_max, double theta_min, bool defl,
+                                                  bool outward, int bnd, double* sh_d, int* sh_i) {
+    double tpl = (theta_max > 0.0) ? 1.0 / theta_max : SW_INF;
+    double tmi = defl ? 0.0 : ((theta_min < 0.0) ? 1.0 / theta_min : -SW_INF);
+    if (outward) { tpl = 0.0; tmi = 0.0; }
+    int bind = (tpl < SW_INF) ? 0 : SW_BIND_NONE_DEV;
+    if (P.lo) {
+        double bt = SW_INF;
+        int bi = 0x7fffffff;
+        double tm = -SW_INF;
+        for (int i = lane; i < n; i += 32) {
+            double vi = v[i], xi = x[i];
+            double t = SW_INF, tn = -SW_INF;
+            if (vi > 0.0) { t = (P.hi[i] - xi) / vi; tn = (P.lo[i] - xi) / vi; }
+            else if (vi < 0.0) { t = (P.lo[i] - xi) / vi; tn = (P.hi[i] - xi) / vi; }
+            if (t < bt) { bt = t; bi = i; }
+            tm = fmax(tm, tn);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ot = __shfl_xor_sync(0xffffffffu, bt, o);
+            int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ot < bt || (ot == bt && oi < bi)) { bt = ot; bi = oi; }
+        }
+        tm = warp_max(tm);
+        if (bt < tpl) {
+            tpl = bt;
+            bind = (v[bi] > 0.0) ? 1 + 2 * bi : 2 + 2 * bi;
+        }
+        tmi = fmax(tmi, tm);
+    }
+    if (P.has_ball) {
+        double dv = 0.0, dd2 = 0.0, vv = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            double di = x[i] - P.ball_c[i];
+            dv += di * v[i];
+            dd2 += di * di;
+            vv += v[i] * v[i];
+        }
+        dv = warp_sum(dv); dd2 = warp_sum(dd2); vv = warp_sum(vv);
+        double disc = dv * dv - vv * (dd2 - P.ball_r * P.ball_r);
+        double sq = sqrt(fmax(disc, 0.0));
+        double tb = (-dv + sq) / vv;
+        double tbm = (-dv - sq) / vv;
+        if (bnd == SW_BIND_BALL_DEV && tb <= 0.0) tb = SW_INF;
+        if (tb < tpl) { tpl = tb; bind = SW_BIND_BALL_DEV; }
+        tmi = fmax(tmi, fmin(tbm, 0.0));
+    }
+    if (lane == 0) {
+        sh_d[0] = tpl;
+        sh_d[1] = tmi;
+        sh_i[1] = bind;
+    }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
+
 // ---------------------------------------------------------------- K2c
 template <int NT>
 __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
@@ -276,11 +340,13 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
         const bool defl = (bnd == 0);
         long long t_prof = clock64();
         __syncthreads();
-        if (!outward && !failed && md >= 1 && theta_max > 0.0) {
+        const bool dense_y = !outward && !failed && md >= 1 && theta_max > 0.0;
+        if (dense_y) {
+            // L (lower rows, 16-byte segments [0, i+1]) into shared memory asynchronously
             const int mdp = (md + 7) & ~7;
             const double* Lw = P.wL + (size_t)slot * P.w_mstride;
             for (int i = T.warp; i < mdp; i += T.nwarps)
-                for (int jx = T.lane; jx <= i; jx += 32) G[i * ld + jx] = Lw[i * ld + jx];
+                for (int c2 = T.lane; 2 * c2 <= i; c2 += 32) cp_async16(G + i * ld + 2 * c2, Lw + i * ld + 2 * c2);
             for (int i = T.tid; i < mdp; i += T.nthr) {
                 zz[i] = S[S_VEC + 3 * vl + i];
                 rdiag[i] = S[S_VEC + 2 * vl + i];
@@ -290,6 +356,13 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
                     hh[i] = S[S_VEC + i];
                     bv[i] = S[S_VEC + vl + i];
                 }
+        }
+        // the last warp selects the binding constraint while L is in flight
+        if (T.warp == T.nwarps - 1)
+            select_bound_warp(P, T.lane, n, x, v, theta_max, theta_min, defl, outward, bnd, sh_d, sh_i);
+        if (dense_y) {
+            const int mdp = (md + 7) & ~7;
+            cp_async_wait_all();
             __syncthreads();
             // y = L^{-T} z, blocked backwards over 8-row blocks
             for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
@@ -343,7 +416,9 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
             }
             __syncthreads();
         }
+#define SW_SELECT_EARLY
 #include "chord_tail.inc"
+#undef SW_SELECT_EARLY
     }
 }
 
