@@ -27,6 +27,26 @@ enum : int { S_A = 0, S_BH = 1, S_MD = 2, S_ST = 3, S_TMAX = 4, S_TMIN = 5, S_DE
 enum : int { ST_OUTWARD = 1, ST_FAILED = 2, ST_DEFL = 4 };
 __host__ __device__ __forceinline__ long long s_stride(int mp) { return S_VEC + 4LL * (mp + 8); }
 
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+
+// packed lower P (row-major packing, pk(i, j) = i(i+1)/2 + j) -> rows of M (lower
+// triangle) by 8-byte cp.async, one warp per row (no index arithmetic per element);
+// the caller waits (cp.async.wait_all + barrier) and mirrors the upper triangle.
+__device__ __forceinline__ void unpack_lower_async(const Team& T, const double* __restrict__ P, double* M, int m,
+                                                   int ld) {
+    for (int i = T.warp; i < m; i += T.nwarps) {
+        const double* src = P + (size_t)i * (i + 1) / 2;
+        for (int j = T.lane; j <= i; j += 32) cp_async8(M + i * ld + j, src + j);
+    }
+}
+__device__ __forceinline__ void mirror_upper(const Team& T, double* M, int m, int ld) {
+    for (int i = T.warp; i < m; i += T.nwarps)
+        for (int j = T.lane; j < i; j += 32) M[j * ld + i] = M[i * ld + j];
+}
+
 // ---------------------------------------------------------------- K2a
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
@@ -64,11 +84,15 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         const int bnd = P.bound[slot];
         __syncthreads();
         long long t_prof = clock64();
-        unpack_sym(T, ax, G, m, ld);
-        unpack_sym(T, av, B, m, ld);
+        unpack_lower_async(T, ax, G, m, ld);
+        unpack_lower_async(T, av, B, m, ld);
         const bool defl = (bnd == 0);
         if (defl)
             for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+        mirror_upper(T, G, m, ld);
+        mirror_upper(T, B, m, ld);
         __syncthreads();
         PROF_MARK(0);
         int md = m;
