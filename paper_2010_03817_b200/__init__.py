@@ -94,11 +94,15 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing and _build.needs_build():
-        _build.build()
-    if not os.path.exists(_build.LIB):
-        raise ImportError(f"libspecwalk.so not built at {_build.LIB}")
-    l = C.CDLL(_build.LIB)
+    alt = os.environ.get("SPECWALK_LIB")  # A/B measurements: an alternative in-tree build of the same ABI
+    if alt:
+        l = C.CDLL(alt)
+    else:
+        if build_if_missing and _build.needs_build():
+            _build.build()
+        if not os.path.exists(_build.LIB):
+            raise ImportError(f"libspecwalk.so not built at {_build.LIB}")
+        l = C.CDLL(_build.LIB)
     l.spec_last_error.restype = C.c_char_p
     l.spec_create.argtypes = [C.c_int, C.c_int, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_void_p)]
     l.spec_destroy.argtypes = [C.c_void_p]
