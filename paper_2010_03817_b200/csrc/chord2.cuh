@@ -1013,7 +1013,7 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
 
-template <int NT, int KC, bool GM = false>
+template <int NT, int KC, bool GM = false, bool USEQT = true>
 __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
                                            const bool need_bot, const int oVec, const int vl, const int oRed,
                                            const int jhint, unsigned long long* prof, const double* __restrict__ Mg = nullptr,
@@ -1123,8 +1123,10 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         if (owner) {
             const double q = wr * sj;  // q_j (wr = u_j[r])
             sm[oQ + j * ld + r] = q;
-            sm[oQT + r * ld + j] = q;
-            sm[oQT + r * ld + j + 1] = 0.0;  // the update reads pairs (i, i + 1): never stale (NaN) data
+            if (USEQT) {
+                sm[oQT + r * ld + j] = q;
+                sm[oQT + r * ld + j + 1] = 0.0;  // the update reads pairs (i, i + 1): never stale (NaN) data
+            }
             sm[oWp + r] = wpr;
         }
         __syncthreads();
@@ -1165,12 +1167,21 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             // (3) w -= Q h (row r: lane g takes the pairs i = 2 g + 8 k)
             double acc0 = 0.0, acc1 = 0.0;
             if (r < mdp) {
-                const int oQr = oQT + r * ld;
-                for (int i = 2 * g; i <= j; i += 8) {
-                    const double2 h2 = *reinterpret_cast<const double2*>(sm + oHb + i);
-                    const double2 q2 = *reinterpret_cast<const double2*>(sm + oQr + i);
-                    acc0 = fma(h2.x, q2.x, acc0);
-                    acc1 = fma(h2.y, q2.y, acc1);
+                if (USEQT) {
+                    const int oQr = oQT + r * ld;
+                    for (int i = 2 * g; i <= j; i += 8) {
+                        const double2 h2 = *reinterpret_cast<const double2*>(sm + oHb + i);
+                        const double2 q2 = *reinterpret_cast<const double2*>(sm + oQr + i);
+                        acc0 = fma(h2.x, q2.x, acc0);
+                        acc1 = fma(h2.y, q2.y, acc1);
+                    }
+                } else {  // column access of the row-major basis (lane g takes i = g mod 4)
+                    int i = g;
+                    for (; i + 4 <= j; i += 8) {
+                        acc0 = fma(sm[oHb + i], sm[oQ + i * ld + r], acc0);
+                        acc1 = fma(sm[oHb + i + 4], sm[oQ + (i + 4) * ld + r], acc1);
+                    }
+                    if (i <= j) acc0 = fma(sm[oHb + i], sm[oQ + i * ld + r], acc0);
                 }
             }
             double qh = acc0 + acc1;

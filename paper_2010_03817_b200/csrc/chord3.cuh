@@ -193,8 +193,9 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
     const int m = P.m, ld = P.ld;
     const int mp = (m + 7) & ~7;
     const int vl = mp + 8;
-    // Q (rows of ld), QT (rows of ld), vector area (NVEC2 slots) + 64 slack
-    const int oQ = 0, oQT = mp * ld, oVec = 2 * mp * ld, oRed = oVec + NVEC2 * vl;
+    // Q (rows of ld), vector area (NVEC2 slots) + 64 slack; no transposed basis (the smaller
+    // shared-memory footprint leaves more L1 for the M loads)
+    const int oQ = 0, oVec = mp * ld, oRed = oVec + NVEC2 * vl;
     const int tid = threadIdx.x;
     __shared__ int sh_deg;
     const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
@@ -217,8 +218,8 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         const int mdp = (md + 7) & ~7;
         const double* Mw = P.wM + (size_t)slot * P.w_mstride;
         const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
-        const int J = lanczos_reg<NT, KC, true>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, jhint, P.prof, Mw,
-                                                oQT);
+        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, jhint,
+                                                       P.prof, Mw, 0);
         if (P.jlast && tid == 0) P.jlast[slot] = J;
         const double theta_max = smem_dyn[oRed + 32 + 4];
         const double theta_min = smem_dyn[oRed + 32 + 5];

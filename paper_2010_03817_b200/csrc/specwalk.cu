@@ -277,7 +277,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     if ((ctx->k2_variant == 1 || ctx->k2_variant == 3) && !getenv("SPECWALK_K2_FUSED")) {
         ctx->k2_split = 1;
         ctx->f_smem = ctx->smem_bytes + sizeof(double) * 8 * (size_t)mp;  // + inverse diagonal blocks
-        ctx->l_smem = ctx->smem_bytes;
+        ctx->l_smem = sizeof(double) * ((size_t)mp * ctx->ld + (size_t)NVEC2 * (mp + 8) + 64);  // Q + vectors
         ctx->t_smem = sizeof(double) * ((size_t)mp * ctx->ld + 5 * (size_t)(mp + 8) + 64);
         int of = 0, ol = 0, ot = 0;
 #define SW_SPLIT_SETUP(NT_, KC_)                                                                                     \
