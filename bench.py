@@ -432,7 +432,7 @@ def main():
     ap.add_argument("--chains", type=int, default=CHAINS, help="chains per GPU")
     ap.add_argument("--e2e-chains", type=int, default=2048)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--volume-seeds", type=int, default=1)
+    ap.add_argument("--volume-seeds", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -206,7 +206,7 @@ int spec_set_comm(spec_ctx* ctx, const spec_comm* comm);
 #define SPEC_MAX_PHASES 64
 typedef struct spec_volume_opts {
     int64_t walk_len; /* billiard steps per phase [10] */
-    int64_t burn;     /* phase-0 burn-in steps from c0 [40] */
+    int64_t burn;     /* phase-0 burn-in steps from c0 [20] (R25) */
     double L;         /* billiard tau [2 sqrt(n)] */
     int64_t rho;      /* reflection bound [10 n] */
     double rho_star;  /* pilot quantile level [0.325] */

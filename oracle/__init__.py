@@ -351,7 +351,7 @@ def ball_samples(seed: int, tag: int, begin: int, count: int, n: int, c0, r: flo
     return X
 
 
-def volume(inst, eps: float, seed: int, N: int, W: int = 10, burn: int = 40, L: float = None, rho: int = None,
+def volume(inst, eps: float, seed: int, N: int, W: int = 10, burn: int = 20, L: float = None, rho: int = None,
            rho_star: float = 0.325, q_stop: float = 0.25, max_phases: int = 64, max_growth: int = 16,
            nthreads: int = 0) -> dict:
     """Ball-phase multiphase Monte Carlo volume (eq:mmc_vol P:1291-1300, telescoping

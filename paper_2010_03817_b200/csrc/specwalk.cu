@@ -1141,7 +1141,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
     if (!(eps > 0.0 && eps < 1.0)) return fail(SPEC_EINVAL, "eps must be in (0,1)");
     const int n = ctx->n;
     spec_volume_opts opt;
-    opt.walk_len = 10; opt.burn = 40; opt.L = 2.0 * std::sqrt((double)n); opt.rho = 10 * n;
+    opt.walk_len = 10; opt.burn = 20; opt.L = 2.0 * std::sqrt((double)n); opt.rho = 10 * n;  // burn: R25
     opt.rho_star = 0.325; opt.q_stop = 0.25; opt.max_phases = 64; opt.max_growth = 16;
     if (o) {
         if (o->walk_len > 0) opt.walk_len = o->walk_len;
