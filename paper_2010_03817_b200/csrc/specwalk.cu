@@ -111,6 +111,10 @@ template <typename T>
 static cudaError_t zalloc(T** p, size_t count) {
     cudaError_t e = cudaMalloc((void**)p, sizeof(T) * (count ? count : 1));
     if (e == cudaSuccess) e = cudaMemset(*p, 0, sizeof(T) * (count ? count : 1));
+    // cudaMemset runs on the legacy default stream, which the library's non-blocking stream
+    // does not wait for: without this the zero fill could land after the first kernels
+    // writing the buffer (seen as intermittently zeroed chain state)
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     return e;
 }
 
@@ -196,13 +200,17 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     ctx->amax = amax;
     CK(zalloc(&ctx->Ahat, Ah.size()));
     CK(zalloc(&ctx->a0, a0.size()));
-    CK(cudaMemcpy(ctx->Ahat, Ah.data(), sizeof(double) * Ah.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->a0, a0.data(), sizeof(double) * a0.size(), cudaMemcpyHostToDevice));
+    // stream-ordered uploads (a pageable cudaMemcpy may return before its DMA completes, and
+    // the library's stream does not wait for the legacy default stream)
+    CK(cudaMemcpyAsync(ctx->Ahat, Ah.data(), sizeof(double) * Ah.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->a0, a0.data(), sizeof(double) * a0.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     if (cube_lo) {
         CK(zalloc(&ctx->lo, n));
         CK(zalloc(&ctx->hi, n));
-        CK(cudaMemcpy(ctx->lo, cube_lo, sizeof(double) * n, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(ctx->hi, cube_hi, sizeof(double) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(ctx->lo, cube_lo, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->hi, cube_hi, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
         ctx->has_cube = 1;
     }
     CK(zalloc(&ctx->c, ctx->np));
@@ -337,7 +345,7 @@ extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
     for (int i = 0; i < ctx->n; ++i) s += c[i] * c[i];
     if (!(s > 0.0) || !std::isfinite(s)) return fail(SPEC_EINVAL, "|c| must be finite and > 0");
     CK(cudaSetDevice(ctx->dev));
-    CK(cudaMemcpy(ctx->c, c, sizeof(double) * ctx->n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->c, c, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
     // A(c) = sum_i c_i A_i (packed), the t^2 coefficient of the HMC pencil up to -1/(2T)
     launch_gemm_av(ctx, ctx->c, nullptr, nullptr, 1, ctx->Ac, nullptr);
     CK(cudaStreamSynchronize(ctx->stream));
@@ -353,7 +361,8 @@ extern "C" int spec_set_ball(spec_ctx* ctx, const double* center, double radius)
         return SPEC_OK;
     }
     if (!center) return fail(SPEC_EINVAL, "center is NULL");
-    CK(cudaMemcpy(ctx->ball_c, center, sizeof(double) * ctx->n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(ctx->ball_c, center, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     ctx->ball_r = radius;
     ctx->has_ball = 1;
     return SPEC_OK;
@@ -807,6 +816,7 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         unsigned long long ph[32];
         CK(cudaMemcpy(ph, ctx->prof, sizeof(ph), cudaMemcpyDeviceToHost));
         CK(cudaMemset(ctx->prof, 0, sizeof(ph)));
+        CK(cudaStreamSynchronize(0));
         const char* names[] = {"unpack", "deflate", "cholesky", "congruence", "eigen", "extreme", "eigvec",
                                "backtransform+y", "select+advance"};
         double tot = 0;
@@ -901,8 +911,9 @@ static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0
         for (size_t k = 1; k < allp.size() / stride; ++k)
             for (int q = 0; q < stride; ++q) acc[q] += allp[k * stride + q];
         cudaMemcpyKind kk = host ? cudaMemcpyHostToHost : cudaMemcpyHostToDevice;
-        if (sum_x) CK(cudaMemcpy(sum_x, acc.data(), sizeof(double) * n, kk));
-        if (sum_xx) CK(cudaMemcpy(sum_xx, acc.data() + n, sizeof(double) * nxx, kk));
+        if (sum_x) CK(cudaMemcpyAsync(sum_x, acc.data(), sizeof(double) * n, kk, ctx->stream));
+        if (sum_xx) CK(cudaMemcpyAsync(sum_xx, acc.data() + n, sizeof(double) * nxx, kk, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     if (final_x) {
         if (host) {
