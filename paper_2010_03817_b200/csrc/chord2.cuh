@@ -657,7 +657,9 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
             for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
             if (pass == 0) tl3 = clock64();
             if (prof && T.tid == 0 && pass == 1) atomicAdd(&prof[15], 1ull);
-            if (!(nn < 0.5 * nn_before)) break;
+            // second (DGKS) pass only on severe cancellation, as in lanczos_reg (one CGS pass
+            // keeps theta_max within ~20 eps |M|; the 0.5 criterion fired on 2/3 of the iterations)
+            if (!(nn < 1e-12 * nn_before)) break;
         }
         const double beta = sqrt(nn);
         if (T.tid == 0) {
