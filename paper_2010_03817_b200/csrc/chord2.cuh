@@ -1253,6 +1253,10 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     return J;
 }
 
+}  // namespace sw
+#include "chol_inv.cuh"
+namespace sw {
+
 template <int NT, bool SMEM, int KC>
 __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
@@ -1376,13 +1380,22 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
         bool degenerate = false, failed = false;
         int lanczos_J = 0;
         if (!outward && md >= 1) {
-            bool okc = cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2]);
+            // global-scratch variant (m > 128): the inverse-diagonal-block DMMA factorisations
+            // (measured +1% there; the shared-memory variants keep the substitution versions)
+            double* Lv = vec + NVEC2 * vl + 64;
+            bool okc = SMEM ? cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2])
+                            : cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
             PROF_MARK(2);
             if (!okc) {
                 failed = true;
             } else {
-                trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
-                trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                if (SMEM) {
+                    trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
+                    trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                } else {
+                    trsm_inv_blocked<false>(T, G, Lv, B, mdp, ld);
+                    trsm_inv_blocked<true>(T, G, Lv, B, mdp, ld);
+                }
                 PROF_MARK(3);
                 // ---- M = -(B + B^T)/2 in place; park L (lower, with rdiag) in global
                 // scratch so that the Lanczos basis can use its shared memory.

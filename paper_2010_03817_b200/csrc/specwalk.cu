@@ -275,7 +275,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         if (occ < 1) occ = 1;
         if (occ > 2) occ = 2;
         ctx->chord_grid_max = occ * ctx->num_sms;
-        ctx->scratch_stride = (long long)roundup((int)per_cta, 32);
+        ctx->scratch_stride = (long long)roundup((int)(per_cta + 8 * (size_t)mp), 32);  // + inverse diagonal blocks
         ctx->scratch_ctas = ctx->chord_grid_max;
         CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
         ctx->smem_bytes = 0;
