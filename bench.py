@@ -167,19 +167,23 @@ def cpu_oracle_sample(seconds: float = 15.0, nthreads: int = 0) -> dict:
 
     def one(c):
         tr = oracle.trace(lmi, oracle.BILLIARD, SEED, c, 1000, L_TAU, RHO, max_refl)
-        return len(tr["t"])
+        return tr["calls"]  # every oracle call made (the walk completes the last step)
 
     t0 = time.time()
     with ThreadPoolExecutor(nthreads) as ex:
         recs = list(ex.map(one, range(nthreads)))
     wall = time.time() - t0
-    calls = int(sum(recs))  # every recorded reflection is one oracle call (+ accepted segments not counted)
+    calls = int(sum(recs))
     return {"value": calls / wall, "unit": "calls/s", "cores": nthreads, "kind": "oracle",
-            "sample": f"{nthreads} chains x first {max_refl} reflections of the M100 walk (seed {SEED}), "
-                      f"{calls} oracle calls in {wall:.1f} s"}
+            "sample": f"{nthreads} chains x the steps holding their first {max_refl} reflections of the M100 walk "
+                      f"(seed {SEED}), {calls} oracle calls in {wall:.1f} s"}
 
 
 def run_reference(args):
+    """The oracle (plain C, Jacobi) as it stands, on the host cores: each step runs one M100
+    billiard chain per core (global chain ids step*cores + t, seed 4) for a bounded number of
+    boundary-oracle calls (the first REF_CALLS reflections), so that --steps K --warmup W
+    finishes in minutes.  Rank 0 only under torchrun."""
     world, rank, _ = _dist()
     if rank != 0:
         return 0
@@ -190,47 +194,35 @@ def run_reference(args):
     nthreads = os.cpu_count() or 1
     inst = specgen.config_instance(3)
     lmi = oracle.Lmi(inst)
-    calls_per_step = nthreads  # one oracle call per host core per step
+    ref_calls = int(os.environ.get("SPECWALK_REF_CALLS", "16"))
 
-    def draw(step):
-        # x on the M100 walk's typical radius (uniform scaling of the chord), v a random unit
-        us = specgen.unit_vectors(calls_per_step, N_DIM, 100 + step)
-        vs = specgen.unit_vectors(calls_per_step, N_DIM, 200 + step)
-        lam = specgen.uniforms(calls_per_step, 300 + step, 0.0, 0.9)
-        return us, vs, lam
-
-    def call(args_):
-        u, v, lam = args_
-        r = oracle.chord(lmi, np.zeros(N_DIM), u)
-        x = lam * r["t_plus"] * u
-        r2 = oracle.chord(lmi, x, v)
-        oracle.normal(lmi, r2["block"], r2["y"])
-        return 2
+    def one(chain):
+        # exactly ref_calls boundary-oracle calls of chain `chain` of the M100 walk (oracle.replay)
+        _, calls = oracle.replay(lmi, oracle.BILLIARD, SEED, chain, STEPS_PER_CHAIN, L_TAU, RHO, ref_calls)
+        return calls
 
     ex = ThreadPoolExecutor(nthreads)
     for s in range(args.warmup):
-        us, vs, lam = draw(s)
-        list(ex.map(call, zip(us, vs, lam)))
+        list(ex.map(one, range(s * nthreads, (s + 1) * nthreads)))
     t0 = time.time()
     total = 0
     for s in range(args.steps):
-        us, vs, lam = draw(1000 + s)
-        total += sum(ex.map(call, zip(us, vs, lam)))
+        base = (args.warmup + s) * nthreads
+        total += sum(ex.map(one, range(base, base + nthreads)))
     wall = time.time() - t0
     value = total / wall
     line = {
         "impl": "reference", "metric": "boundary-oracle calls/s (billiard walk, n=m=100)", "value": value,
         "unit": "calls/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": wall * 1e3 / max(args.steps, 1), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": wall * 1e3 / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "n": N_DIM, "m": M_DIM,
-                   "reference_step": f"{calls_per_step} interior boundary-oracle calls + normals on the M100 "
-                                     f"instance (one per host core; Jacobi oracle)"},
+                   "reference_step": f"{nthreads} M100 billiard chains (one per host core), the first {ref_calls} "
+                                     f"boundary-oracle calls of each (oracle/: plain C, Jacobi)"},
         "cpu_baseline": {"value": value, "unit": "calls/s", "cores": nthreads, "kind": "oracle",
-                         "sample": f"{args.steps} steps x {calls_per_step} x 2 chords"},
+                         "sample": f"{args.steps} steps x {nthreads} chains x {ref_calls} calls = {total} calls"},
         "e2e": {"value": value, "unit": "calls/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    line["scaling"] = "weak"
     print(json.dumps(line), flush=True)
     return 0
 

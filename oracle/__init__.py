@@ -106,6 +106,8 @@ def lib():
                                C.POINTER(_Stats), C.c_int]
         l.orc_trace.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp, _dp, _dp,
                                 _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        l.orc_trace_stats.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp, _dp,
+                                      _dp, _dp, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(_Stats)]
         l.orc_replay.argtypes = [C.c_void_p, C.POINTER(_WalkParams), C.c_int64, _dp, C.c_int64, _dp,
                                  C.POINTER(C.c_int64)]
         l.orc_qep_root.argtypes = [C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]
@@ -302,12 +304,14 @@ def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho:
     va = np.zeros((max_refl, n))
     bind = np.zeros(max_refl, dtype=np.int32)
     nrec = C.c_int64()
-    rc = lib().orc_trace(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
-                         bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec))
+    st = _Stats()
+    rc = lib().orc_trace_stats(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
+                               bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec), C.byref(st))
     if rc:
         raise ValueError(f"orc_trace rc={rc}")
     k = nrec.value
-    return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k])
+    # calls: every boundary-oracle call of the walk (it finishes the step of the last record)
+    return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k], calls=int(st.calls))
 
 
 def replay(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_calls: int,

@@ -1182,6 +1182,15 @@ int orc_replay(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const 
 int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
               int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
               int32_t* binding, int64_t* nrec) {
+    return orc_trace_stats(L, p, chain, x0, max_refl, hit_x, t, w, v_after, binding, nrec, NULL);
+}
+
+/* as orc_trace; st_out (may be NULL) receives the walk statistics: the walk always
+   completes the step in which the max_refl-th reflection falls, so st_out->calls
+   counts every boundary-oracle call made (>= the recorded reflections) */
+int orc_trace_stats(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
+                    int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
+                    int32_t* binding, int64_t* nrec, orc_stats* st_out) {
     int n = L->n;
     walk_ws W;
     ws_init(&W, L);
@@ -1195,6 +1204,7 @@ int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const d
         if (rc) break;
     }
     *nrec = tr.nrec;
+    if (st_out) *st_out = st;
     ws_free(&W);
     return rc;
 }

@@ -117,6 +117,9 @@ int orc_replay(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const 
 int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
               int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
               int32_t* binding, int64_t* nrec);
+int orc_trace_stats(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
+                    int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
+                    int32_t* binding, int64_t* nrec, orc_stats* st_out);
 
 /* HMC-r first positive root of det(F(p) + t F1(v) - t^2 F1(c)/(2T)) for one block
  * via the mu-companion + Hessenberg + Francis QR. */
