@@ -32,6 +32,8 @@ def make_allgather(group=None, device: Optional[str] = None) -> Callable[[np.nda
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
+    if device is None and dist.get_backend(group) == "nccl":
+        device = f"cuda:{torch.cuda.current_device()}"  # NCCL moves CUDA tensors only
 
     def allgather(local: np.ndarray) -> np.ndarray:
         t = torch.from_numpy(np.ascontiguousarray(local, dtype=np.float64))
