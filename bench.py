@@ -233,10 +233,20 @@ def run_ours(args):
     world, rank, local = _dist()
     if world > 1:
         import torch.distributed as dist
+        # SPECWALK_DIST_TEST=1: logic test of the N > 1 path on a 1-GPU box (every rank on
+        # cuda:0, gloo collectives; ranks are independent until the final reductions)
+        test1 = os.environ.get("SPECWALK_DIST_TEST") == "1"
+        if test1:
+            local = 0
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if test1:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        coll_dev = "cpu" if test1 else "cuda"
     else:
         dist = None
+        coll_dev = "cuda"
         torch.cuda.set_device(0)
     import paper_2010_03817_b200 as sw
     import specgen
@@ -276,7 +286,7 @@ def run_ours(args):
     S.kernel_timing(False)
     S.walk_end()
     calls = st1["calls"] - st0["calls"]
-    t = torch.tensor([ms, float(calls)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, float(calls)], dtype=torch.float64, device=coll_dev)
     if dist is not None:
         tmax = t.clone()
         dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
@@ -327,7 +337,7 @@ def run_ours(args):
         te1.synchronize()
         barrier()
         ems = te0.elapsed_time(te1)
-        et = torch.tensor([ems, float(out["stats"]["calls"])], dtype=torch.float64, device="cuda")
+        et = torch.tensor([ems, float(out["stats"]["calls"])], dtype=torch.float64, device=coll_dev)
         if dist is not None:
             emax = et.clone()
             dist.all_reduce(emax[:1], op=dist.ReduceOp.MAX)
