@@ -865,14 +865,15 @@ __device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB
 // flip); its value is returned to all lanes.  lo must be an inner bound (a Ritz
 // value of a smaller T or max/min alpha), hi an outer (Gershgorin) bound.
 __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, const double lo, const double hi,
-                                    const bool top, const int lane) {
+                                    const bool top, const int lane, int* it_out = nullptr,
+                                    const double hsafe = 0.0) {
     extern __shared__ __align__(16) double sm[];
     const double eps = 2.220446049250313e-16;
     if (J == 1) return sm[oA];
     const double n = (double)J;
     double x = lo + (hi - lo) * exp2(-0.5 * (double)lane);
     if (lane == 0) x = hi;
-    bool valid = true, done = false, has_step = false;
+    bool valid = true, done = false, has_step = false, restarted = (hsafe == 0.0);
     double last_step = 0.0;
     for (int it = 0; it < 40; ++it) {
         double p0 = 1.0, d0 = 0.0, s0 = 0.0;
@@ -938,8 +939,18 @@ __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, co
         // the valid lane with the innermost start converges first and is the answer
         const unsigned vmask = __ballot_sync(0xffffffffu, valid);
         const int best = top ? 31 - __clz(vmask) : 31 - __clz(vmask);  // highest lane = innermost start
-        if (vmask == 0u) break;
+        if (vmask == 0u) {
+            if (restarted) break;
+            // the (warm) outer bound was inside the spectrum: restart from the safe bound
+            restarted = true;
+            x = lo + (hsafe - lo) * exp2(-0.5 * (double)lane);
+            if (lane == 0) x = hsafe;
+            valid = true; done = false; has_step = false; last_step = 0.0;
+            it = -1;
+            continue;
+        }
         const bool bdone = __shfl_sync(0xffffffffu, done ? 1 : 0, best) != 0;
+        if (it_out) *it_out = it + 1;
         if (bdone) return __shfl_sync(0xffffffffu, x, best);
     }
     const unsigned vmask = __ballot_sync(0xffffffffu, valid);
@@ -961,10 +972,12 @@ enum : int { CK_TTOP = 0, CK_RTOP = 1, CK_TBOT = 2, CK_RBOT = 3, CK_TNORM = 10 /
 // Out of line: one warp works while the CTA waits.
 __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const int oBe, const int oB2, const int oRbe,
                                            const int J, const double beta, const double tnorm, const bool need_bot,
-                                           const bool exhausted, const int md, const int oShd) {
+                                           const bool exhausted, const int md, const int oShd,
+                                           unsigned long long* prof = nullptr) {
     extern __shared__ __align__(16) double sm[];
     if ((tid >> 5) != 0) return;
     const int lane = tid & 31;
+    long long ck0 = clock64();
     // Gershgorin bounds (outer) and max / min alpha (inner: Rayleigh quotients of T_J)
     double ghi = -SW_INF, glo = SW_INF, ahi = -SW_INF, alo = SW_INF;
     for (int i = lane; i < J; i += 32) {
@@ -980,11 +993,35 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     ahi = warp_max(ahi);
     alo = warp_min(alo);
     const double in_top = fmax(ahi, sm[oShd + CK_INTOP]), in_bot = fmin(alo, sm[oShd + CK_INBOT]);
-    const double th = tri_laguerre_warp(oAl, oB2, J, in_top, ghi + 1e-13 * tnorm, true, lane);
+    // outer start: Gershgorin, or -- after a first check -- the previous Ritz value plus its
+    // residual (an eigenvalue of M lies within the residual of a Ritz value; the top one when
+    // the residual is below the gap).  tri_laguerre_warp restarts at Gershgorin if the Sturm
+    // signs show the bound is inside the spectrum.
+    const double th_prev = sm[oShd + CK_TTOP];
+    double hi_top = ghi + 1e-13 * tnorm;
+    if (th_prev > -SW_INF) hi_top = fmin(hi_top, th_prev + 1.01 * sm[oShd + CK_RTOP] + 1e-13 * tnorm);
+    long long ck1 = clock64();
+    int lits = 0;
+    const double th = tri_laguerre_warp(oAl, oB2, J, fmin(in_top, hi_top), hi_top, true, lane, &lits,
+                                        ghi + 1e-13 * tnorm);
     double thb = SW_INF;
     if (need_bot) thb = tri_laguerre_warp(oAl, oB2, J, in_bot, glo - 1e-13 * tnorm, false, lane);
+    long long ck2 = clock64();
     if (lane != 0) return;
     const double res = beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, th);
+#if SW_PROF_LANCZOS
+    if (prof) {
+        long long ck3 = clock64();
+        const bool first = !(sm[oShd + CK_INTOP] > -SW_INF);
+        atomicAdd(&prof[first ? 20 : 24], 1ull);
+        atomicAdd(&prof[first ? 21 : 25], (unsigned long long)lits);
+        atomicAdd(&prof[first ? 22 : 26], (unsigned long long)(ck2 - ck1));
+        atomicAdd(&prof[23], (unsigned long long)(ck3 - ck2));
+        atomicAdd(&prof[27], (unsigned long long)(ck1 - ck0));
+    }
+#else
+    (void)ck0; (void)ck1; (void)ck2; (void)prof;
+#endif
     const double resb = need_bot ? beta * tri_back_lastcomp_sm(oAl, oBe, oRbe, J, thb) : 0.0;
     sm[oShd + CK_TTOP] = th;
     sm[oShd + CK_RTOP] = res;
@@ -1221,7 +1258,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         SW_LZ_STAMP(c_upd)
         if (exhausted || J >= next_check) {
             __syncthreads();  // al / be / b2 / rbe and the bookkeeping of this step visible
-            lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, tnorm, need_bot, exhausted, md, oShd);
+            lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, tnorm, need_bot, exhausted, md, oShd, prof);
             __syncthreads();
             SW_LZ_STAMP(c_chk)
             if (sm[oShd + CK_DONE] != 0.0) break;

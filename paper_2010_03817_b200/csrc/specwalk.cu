@@ -829,6 +829,13 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         fprintf(stderr, "[specwalk prof] lanczos_reg per iteration: matvec=%.0f dots=%.0f update=%.0f | check/call=%.0f\n",
                 (double)ph[12] / fmax((double)ph[10], 1.0), (double)ph[13] / fmax((double)ph[10], 1.0),
                 (double)ph[14] / fmax((double)ph[10], 1.0), (double)ph[9] / (double)hs[0]);
+        if (ph[20] + ph[24] > 0)
+            fprintf(stderr, "[specwalk prof] checks/call: first=%.2f later=%.2f | laguerre its: first=%.2f later=%.2f | "
+                            "cycles: laguerre first=%.0f later=%.0f back=%.0f bounds=%.0f (per check)\n",
+                    (double)ph[20] / hs[0], (double)ph[24] / hs[0], (double)ph[21] / fmax(1.0, (double)ph[20]),
+                    (double)ph[25] / fmax(1.0, (double)ph[24]), (double)ph[22] / fmax(1.0, (double)ph[20]),
+                    (double)ph[26] / fmax(1.0, (double)ph[24]), (double)ph[23] / fmax(1.0, (double)(ph[20] + ph[24])),
+                    (double)ph[27] / fmax(1.0, (double)(ph[20] + ph[24])));
         double it = (double)ph[10];
         fprintf(stderr, "[specwalk prof] per lanczos iteration: matvec=%.0f dots=%.0f axpy+norm(+pass2)=%.0f qwrite=%.0f pass2_frac=%.3f\n",
                 ph[12] / it, ph[13] / it, ph[14] / it, ph[16] / it, ph[15] / it);
