@@ -66,9 +66,20 @@ CASES = [
     ("paper_example", specgen.paper_example),
     ("rand_3_1", lambda: specgen.rand_cube(3, 1, 9)),
 ]
+# one instance per K2 launch variant (csrc/specwalk.cu): 128-thread fused (m <= 32), 192-thread
+# fused (m <= 48), 256-thread fused (m <= 64), split with 13 column pairs (m <= 104, here with
+# mp = 72 < 104: padded columns), split with 16 pairs (104 < m <= 128), global scratch (m > 128)
+VARIANTS = [
+    ("v4_rand_8_30", lambda: specgen.rand_cube(8, 30, 11)),
+    ("v5_rand_12_44", lambda: specgen.rand_cube(12, 44, 12)),
+    ("v0_rand_16_60", lambda: specgen.rand_cube(16, 60, 13)),
+    ("v1_rand_20_72", lambda: specgen.rand_cube(20, 72, 14)),
+    ("v3_rand_24_120", lambda: specgen.rand_cube(24, 120, 15)),
+    ("v2_rand_10_136", lambda: specgen.rand_cube(10, 136, 16)),
+]
 
 
-@pytest.mark.parametrize("name,make", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("name,make", CASES + VARIANTS, ids=[c[0] for c in CASES + VARIANTS])
 def test_boundary_oracle_interior_parity(name, make):
     import paper_2010_03817_b200 as sw
     inst = make()
@@ -88,7 +99,7 @@ def test_boundary_oracle_interior_parity(name, make):
             assert abs(np.linalg.eigvalsh(F)[0]) <= 1e-12 * scale
 
 
-@pytest.mark.parametrize("name,make", CASES[:6], ids=[c[0] for c in CASES[:6]])
+@pytest.mark.parametrize("name,make", CASES[:6] + VARIANTS, ids=[c[0] for c in CASES[:6] + VARIANTS])
 def test_boundary_oracle_boundary_start_parity(name, make):
     """Segments that start on the dense boundary (after a reflection): Schur deflation (R6)."""
     import paper_2010_03817_b200 as sw
