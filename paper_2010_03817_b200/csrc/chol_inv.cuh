@@ -7,9 +7,9 @@
 //   TRSM step  B_k    = L_kk^{-1} B_k             (was: 8 x 8 substitution per column)
 //   updates    A_ij  -= L_ik L_jk^T, B_i -= L_ik B_k  (DMMA, unchanged)
 // Warp 0 computes the 8 x 8 diagonal factor (rsqrt: no division) and its
-// inverse in registers (lane r < 8 holds row r; the inverse is the forward
-// substitution L X = I).  (All warps factoring it redundantly, to drop a
-// barrier, was measured slower: 16x the shuffles.)
+// inverse in registers, with a one-block lookahead over the trailing update.
+// (All warps factoring it redundantly, to drop a barrier, was measured slower:
+// 16x the shuffles.)
 // Same arithmetic as the substitution (up to rounding order) -- results agree
 // with the oracle's unblocked Cholesky and substitutions to ~1e-15.
 #pragma once
@@ -44,6 +44,122 @@ __device__ __forceinline__ void tile_mul_w(double (&acc)[2], const double* W, in
 // Blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8),
 // rdiag = 1 / diag(L), Lv = the inverses of the 8 x 8 diagonal blocks (row-major,
 // 64 doubles per block).  Returns false on a non-positive pivot (CTA-uniform).
+// 8 x 8 diagonal factor of D (lower, leading dimension ld) and its inverse, by one
+// warp in registers (lane r < 8 holds row r; rsqrt: no division; the inverse is the
+// forward substitution L X = I).  Stores L_kk into D, 1/diag into rd8, X into V (row-major
+// 8 x 8).  Returns the pivot test (warp-uniform).
+__device__ __forceinline__ bool diag_factor_inv(double* D, int ld, double* rd8, double* V, int lane) {
+    const int r = lane;
+    double a[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[c] = (r < 8 && c <= r) ? D[r * ld + c] : 0.0;
+    bool ok = true;
+    double rd = 1.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const double d = __shfl_sync(0xffffffffu, a[c], c);
+        if (!(d > 0.0)) ok = false;
+        const double il = rsqrt(fmax(d, 1e-300));
+        if (r == c) { a[c] = d * il; rd = il; }
+        else if (r > c) a[c] *= il;
+#pragma unroll
+        for (int k = c + 1; k < 8; ++k) {
+            const double lkc = __shfl_sync(0xffffffffu, a[c], k);
+            if (r >= k) a[k] = fma(-a[c], lkc, a[k]);
+        }
+    }
+    double x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        if (r == k) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) x[c] = ((c == k ? 1.0 : 0.0) - x[c]) * rd;
+        }
+#pragma unroll
+        for (int c = 0; c <= k; ++c) {
+            const double xkc = __shfl_sync(0xffffffffu, x[c], k);
+            if (r > k && r < 8) x[c] = fma(a[k], xkc, x[c]);
+        }
+    }
+    if (r < 8) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (c <= r) D[r * ld + c] = a[c];
+            V[r * 8 + c] = (c <= r) ? x[c] : 0.0;
+        }
+        rd8[r] = rd;
+    }
+    return ok;
+}
+
+// Blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8),
+// rdiag = 1 / diag(L), Lv = the inverses of the 8 x 8 diagonal blocks (row-major,
+// 64 doubles per block).  Returns false on a non-positive pivot (CTA-uniform).
+// Lookahead: in step kb warp 0 updates tile (kb+1, kb+1) first and factors it
+// right away, while the other warps do the rest of the trailing update, so the
+// diagonal factor (the critical path) overlaps the SYRK; two barriers per step.
+__device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld, double* rdiag, double* Lv,
+                                        int* flag) {
+    const int TB = n >> 3;
+    const int rr = T.lane >> 2, q = T.lane & 3;
+    if (T.warp == 0) {
+        const bool ok = diag_factor_inv(G, ld, rdiag, Lv, T.lane);
+        if (T.lane == 0) *flag = ok ? 0 : 1;
+    }
+    __syncthreads();
+    if (*flag) return false;
+    for (int kb = 0; kb < TB; ++kb) {
+        const int k0 = kb * 8;
+        const double* Vk = Lv + kb * 64;
+        // panel: L_ib,kb = A_ib,kb L_kk^{-T}, one 8 x 8 tile per warp (DMMA)
+        for (int ib = kb + 1 + T.warp; ib < TB; ib += T.nwarps) {
+            double* Ct = G + ib * 8 * ld + k0;
+            double acc[2];
+            tile_mul_wt(acc, Ct, ld, Vk, 8, T.lane);
+            __syncwarp();
+            Ct[rr * ld + 2 * q] = acc[0];
+            Ct[rr * ld + 2 * q + 1] = acc[1];
+        }
+        __syncthreads();
+        const int Tr = TB - kb - 1;
+        if (Tr == 0) break;
+        if (T.warp == 0) {
+            // tile (kb+1, kb+1) of the trailing update, then its factor and inverse
+            double* C = G + (kb + 1) * 8 * ld + (kb + 1) * 8;
+            double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
+            tile_msub<true>(acc, G + (kb + 1) * 8 * ld + k0, ld, G + (kb + 1) * 8 * ld + k0, ld, 8, T.lane);
+            C[rr * ld + 2 * q] = acc[0];
+            C[rr * ld + 2 * q + 1] = acc[1];
+            __syncwarp();
+            const bool ok = diag_factor_inv(C, ld, rdiag + (kb + 1) * 8, Lv + (kb + 1) * 64, T.lane);
+            if (T.lane == 0) *flag = ok ? 0 : 1;
+        } else {
+            // the rest of the trailing SYRK: G_ij -= P_i P_j^T, kb < j <= i, (i, j) != (kb+1, kb+1),
+            // tiles walked incrementally over the warps 1..nwarps-1
+            int ii = 0, jj = 0, t = T.warp;  // tile 0 = (0, 0) belongs to warp 0
+            while (ii < Tr && jj + t > ii) { t -= ii + 1 - jj; jj = 0; ++ii; }
+            jj += t;
+            while (ii < Tr) {
+                const int ib = kb + 1 + ii, jb = kb + 1 + jj;
+                double* C = G + ib * 8 * ld + jb * 8;
+                double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
+                tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
+                C[rr * ld + 2 * q] = acc[0];
+                C[rr * ld + 2 * q + 1] = acc[1];
+                jj += T.nwarps - 1;
+                while (ii < Tr && jj > ii) { jj -= ii + 1; ++ii; }
+            }
+        }
+        __syncthreads();
+        if (*flag) return false;
+    }
+    return true;
+}
+
+// Without lookahead (three barriers per step): used on the global-scratch variant (m > 128),
+// where the lookahead was measured 3% slower.
 __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, double* rdiag, double* Lv,
                                      int* flag) {
     const int TB = n >> 3;

@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
         PROF_MARK(1);
         if (!outward && md >= 1) {
-            const bool okc = cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
+            const bool okc = cholesky_inv_blocked_la(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
             PROF_MARK(2);
             if (!okc) {
                 status |= ST_FAILED;
