@@ -301,4 +301,73 @@ __device__ void trsm_inv_blocked(const Team& T, const double* G, const double* L
     }
 }
 
+// As trsm_inv_blocked with a one-row lookahead: the warp that updates a tile of block
+// row kb+1 in step kb also multiplies it by L_{kb+1,kb+1}^{-1} right away, so the row
+// multiply needs no phase (and barrier) of its own -- one barrier per block step.
+template <bool TR>
+__device__ void trsm_inv_blocked_la(const Team& T, const double* G, const double* Lv, double* B, int n, int ld) {
+    const int TB = n >> 3;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    // block row 0
+    for (int cb = T.warp; cb < TB; cb += T.nwarps) {
+        double acc[2];
+        if (!TR) {
+            double* Bt = B + cb * 8;
+            tile_mul_w(acc, Lv, 8, Bt, ld, T.lane);
+            __syncwarp();
+            Bt[r * ld + 2 * q] = acc[0];
+            Bt[r * ld + 2 * q + 1] = acc[1];
+        } else {
+            double* Bt = B + cb * 8 * ld;
+            tile_mul_wt(acc, Bt, ld, Lv, 8, T.lane);
+            __syncwarp();
+            Bt[r * ld + 2 * q] = acc[0];
+            Bt[r * ld + 2 * q + 1] = acc[1];
+        }
+    }
+    __syncthreads();
+    for (int kb = 0; kb + 1 < TB; ++kb) {
+        const int k0 = kb * 8;
+        const double* Vn = Lv + (kb + 1) * 64;
+        int ib = kb + 1, cb = T.warp;
+        while (cb >= TB) { cb -= TB; ++ib; }
+        for (; ib < TB; cb += T.nwarps) {
+            while (cb >= TB) { cb -= TB; ++ib; }
+            if (ib >= TB) break;
+            const double* A = G + ib * 8 * ld + k0;
+            double acc[2];
+            if (!TR) {
+                double* C = B + ib * 8 * ld + cb * 8;
+                acc[0] = C[r * ld + 2 * q];
+                acc[1] = C[r * ld + 2 * q + 1];
+                tile_msub<false>(acc, A, ld, B + k0 * ld + cb * 8, ld, 8, T.lane);
+                C[r * ld + 2 * q] = acc[0];
+                C[r * ld + 2 * q + 1] = acc[1];
+                if (ib == kb + 1) {  // finish block row kb+1: W = L^{-1} W for this tile
+                    __syncwarp();
+                    tile_mul_w(acc, Vn, 8, C, ld, T.lane);
+                    __syncwarp();
+                    C[r * ld + 2 * q] = acc[0];
+                    C[r * ld + 2 * q + 1] = acc[1];
+                }
+            } else {
+                double* Ct = B + cb * 8 * ld + ib * 8;
+                acc[0] = Ct[(2 * q) * ld + r];
+                acc[1] = Ct[(2 * q + 1) * ld + r];
+                tile_msub<true>(acc, A, ld, B + cb * 8 * ld + k0, ld, 8, T.lane);
+                Ct[(2 * q) * ld + r] = acc[0];
+                Ct[(2 * q + 1) * ld + r] = acc[1];
+                if (ib == kb + 1) {
+                    __syncwarp();
+                    tile_mul_wt(acc, Ct, ld, Vn, 8, T.lane);
+                    __syncwarp();
+                    Ct[r * ld + 2 * q] = acc[0];
+                    Ct[r * ld + 2 * q + 1] = acc[1];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 }  // namespace sw
