@@ -19,6 +19,11 @@
 namespace sw {
 
 constexpr int NVEC2 = 20;
+#ifndef SW_LANCZOS_TOL
+// Lanczos convergence: residual of the top Ritz pair <= SW_LANCZOS_TOL |T_J|.  The Ritz value
+// error is ~res^2 / gap; the Ritz vector (the kernel vector y, the normal) error ~res / gap.
+#define SW_LANCZOS_TOL 1e-13
+#endif
 #ifndef SW_PROF_LANCZOS
 #define SW_PROF_LANCZOS 0  // per-stage clock64 counters of lanczos_reg (build with -DSW_PROF_LANCZOS=1)
 #endif
@@ -1027,7 +1032,7 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     sm[oShd + CK_RTOP] = res;
     sm[oShd + CK_TBOT] = thb;
     sm[oShd + CK_RBOT] = resb;
-    const double tol = 1e-14 * tnorm;
+    const double tol = SW_LANCZOS_TOL * tnorm;
     const bool done = exhausted || (res <= tol && resb <= tol);
     sm[oShd + CK_DONE] = done ? 1.0 : 0.0;
     if (done) return;
