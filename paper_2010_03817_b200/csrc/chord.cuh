@@ -91,6 +91,12 @@ struct ChordParams {
     double* wL;     // L (lower incl. diagonal, rows of leading dimension ld)
     double* wS;     // scalars + vectors (chord3.cuh: S_*)
     long long w_mstride, w_sstride;
+    // K5 split (hmc2.cuh): per-slot Weyl-stepping state, Householder rank-2 vectors
+    double* wH;       // H_* scalars per slot
+    double* wQ;       // q_0, q_1, q_2 (3 x (mp + 8) per slot)
+    int* nxt_list;    // slots still stepping after this iteration
+    int* nxt_count;
+    int zall;         // lanczos_kernel: z = Q s whatever the sign of theta_max
 };
 
 // ---------------------------------------------------------------- team helpers

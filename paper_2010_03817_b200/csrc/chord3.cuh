@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         const int mdp = (md + 7) & ~7;
         const double* Mw = P.wM + (size_t)slot * P.w_mstride;
         const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
-        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1, oVec, vl, oRed, jhint,
+        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1 && !P.zall, oVec, vl, oRed, jhint,
                                                        P.prof, Mw, 0);
         if (P.jlast && tid == 0) P.jlast[slot] = J;
         const double theta_max = smem_dyn[oRed + 32 + 4];
@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         }
         // z = Q s (rows of Q are the normalised Lanczos vectors)
         double* zg = S + S_VEC + 3 * vl;
-        if (theta_max > 0.0) {
+        if (theta_max > 0.0 || P.zall) {
             for (int e = tid; e < mdp; e += NT) {
                 double s0 = 0.0, s1 = 0.0;
                 int i = 0;
@@ -320,6 +320,35 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::); }
 
+// y = L^{-T} z with L lower in G (rows of ld), rdiag = 1 / diag(L); blocked backwards
+// over 8-row blocks (warp 0 solves the diagonal block, all threads update).  zz is
+// overwritten.
+__device__ __forceinline__ void back_solve_lt(const Team& T, const double* G, int ld, int mdp, double* zz, double* yy,
+                                              const double* rdiag) {
+    for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
+        const int k0 = kb * 8;
+        if (T.warp == 0) {
+            const int r = T.lane;
+            double zr = (r < 8) ? zz[k0 + r] : 0.0;
+#pragma unroll
+            for (int c = 7; c >= 0; --c) {
+                const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
+                if (r == c) zr = yc;
+                else if (r < c) zr -= G[(k0 + c) * ld + k0 + r] * yc;
+            }
+            if (r < 8) yy[k0 + r] = zr;
+        }
+        __syncthreads();
+        for (int i = T.tid; i < k0; i += T.nthr) {
+            double acc = zz[i];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc -= G[(k0 + c) * ld + i] * yy[k0 + c];
+            zz[i] = acc;
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- K2c
 template <int NT>
 __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
@@ -389,29 +418,7 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
             const int mdp = (md + 7) & ~7;
             cp_async_wait_all();
             __syncthreads();
-            // y = L^{-T} z, blocked backwards over 8-row blocks
-            for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
-                const int k0 = kb * 8;
-                if (T.warp == 0) {
-                    const int r = T.lane;
-                    double zr = (r < 8) ? zz[k0 + r] : 0.0;
-#pragma unroll
-                    for (int c = 7; c >= 0; --c) {
-                        const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
-                        if (r == c) zr = yc;
-                        else if (r < c) zr -= G[(k0 + c) * ld + k0 + r] * yc;
-                    }
-                    if (r < 8) yy[k0 + r] = zr;
-                }
-                __syncthreads();
-                for (int i = T.tid; i < k0; i += T.nthr) {
-                    double acc = zz[i];
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) acc -= G[(k0 + c) * ld + i] * yy[k0 + c];
-                    zz[i] = acc;
-                }
-                __syncthreads();
-            }
+            back_solve_lt(T, G, ld, mdp, zz, yy, rdiag);  // y = L^{-T} z
             if (T.warp == 0) {
                 if (defl) {  // y = H [ -b^T yh / a ; yh ]
                     double s = 0.0;

@@ -73,6 +73,168 @@ __device__ double weyl_step(double a, const double* c, int d) {
     return lo;
 }
 
+// Cube faces, selection, the oracle outputs (mode 1) or the HMC advance, reflection
+// and step logic (Alg. 6) for one slot, given the dense chord t_dense and the unit
+// kernel vector yy (shared memory) -- shared by hmc_kernel and the split tail.
+__device__ __forceinline__ void hmc_finish(const Team& T, const ChordParams& P, int slot, long long gidv, double* x,
+                                           double* v, const double* av, double* ax, int bnd, const double* yy,
+                                           double t_dense, bool failed, bool outward, double* red, double* sh_d,
+                                           int* sh_i) {
+    const int m = P.m, n = P.n;
+    const double Tinv = 1.0 / P.Temp;
+    {
+
+        // ---- cube faces: per-coordinate quadratic x_i(t) = x_i + v_i t - c_i t^2 / 2T
+        if (T.warp == 0) {
+            double tpl = t_dense;
+            int bind = (tpl < SW_INF) ? 0 : SW_BIND_NONE_DEV;
+            if (P.lo) {
+                double bt = SW_INF;
+                int bi = 0x7fffffff, bcode = 0;
+                for (int i = T.lane; i < n; i += 32) {
+                    const double g = 0.5 * P.cvec[i] * Tinv;
+                    double tu = first_pos_root2(P.hi[i] - x[i], -v[i], g, bnd == 1 + 2 * i);
+                    double tl = first_pos_root2(x[i] - P.lo[i], v[i], -g, bnd == 2 + 2 * i);
+                    if (tu < bt) { bt = tu; bi = i; bcode = 1 + 2 * i; }
+                    if (tl < bt) { bt = tl; bi = i; bcode = 2 + 2 * i; }
+                }
+                for (int o = 16; o > 0; o >>= 1) {
+                    double ot = __shfl_xor_sync(0xffffffffu, bt, o);
+                    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                    int oc = __shfl_xor_sync(0xffffffffu, bcode, o);
+                    if (ot < bt || (ot == bt && oi < bi)) { bt = ot; bi = oi; bcode = oc; }
+                }
+                if (bt < tpl) { tpl = bt; bind = bcode; }
+            }
+            if (T.lane == 0) {
+                sh_d[0] = tpl;
+                sh_i[1] = bind;
+            }
+        }
+        __syncthreads();
+        const double tplus = sh_d[0];
+        const int bind = sh_i[1];
+        if (P.mode == 1) {
+            if (T.tid == 0) {
+                P.o_tplus[slot] = tplus;
+                P.o_tminus[slot] = 0.0;
+                P.o_binding[slot] = bind;
+                P.o_status[slot] = failed ? 2 : 0;
+                P.flags[slot] = (bind == 0 && !failed) ? CF_NEED_NORMAL : 0;
+            }
+            if (P.o_kernel)
+                for (int i = T.tid; i < m; i += T.nthr) P.o_kernel[(size_t)slot * m + i] = (bind == 0) ? yy[i] : 0.0;
+            if (bind == 0 && !failed) {
+                double* yh = P.Yh + (size_t)slot * P.mtp;
+                for (int i = T.warp; i < m; i += T.nwarps)
+                    for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
+            }
+            return;
+        }
+        // ---- HMC advance (Alg. 6): p <- p(t^), A(p) <- A(p) + t^ A(v) + t^2 C2
+        if (failed) {
+            if (T.tid == 0) {
+                P.flags[slot] |= CF_DONE | CF_FAILED;
+                P.calls[slot] += 1;
+            }
+            return;
+        }
+        // per-chain counters read by every thread BEFORE thread 0 updates them below
+        // (a read after the update would give threads different values: a race)
+        const int refl0 = P.refl[slot];
+        const int sdone0 = P.steps_done[slot];
+        const int trk0 = (P.max_trace > 0) ? P.tr_cnt[slot] : 0;
+        const double el = P.ell[slot];
+        const bool accept = (el <= tplus);
+        const double th = accept ? el : tplus;
+        const double qa = -0.5 * th * th * Tinv;
+        for (int i = T.tid; i < n; i += T.nthr) x[i] += th * v[i] + qa * P.cvec[i];
+        for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] += th * av[i] + qa * P.Ac[i];
+        __syncthreads();
+        bool end_step = accept, reject = false;
+        if (!accept) {
+            int rf = refl0 + 1;
+            if (T.tid == 0) {
+                P.refl[slot] = rf;
+                P.ell[slot] = el - th;
+                P.nrefl[slot] += 1;
+                P.tlast[slot] = th;
+            }
+            if (rf > P.rho) {
+                reject = end_step = true;
+                if (T.tid == 0) P.nrej[slot] += 1;
+            } else if (bind == 0) {
+                if (outward) {
+                    reject = end_step = true;
+                    if (T.tid == 0) P.ndeg[slot] += 1;
+                } else {
+                    double* yh = P.Yh + (size_t)slot * P.mtp;
+                    for (int i = T.warp; i < m; i += T.nwarps)
+                        for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
+                    for (int i = T.tid; i < m; i += T.nthr) P.U[(size_t)slot * m + i] = yy[i];
+                    if (T.tid == 0) {
+                        P.bound[slot] = 0;
+                        P.flags[slot] |= CF_NEED_NORMAL;
+                        int q = atomicAdd(P.ncount, 1);
+                        P.nlist[q] = slot;
+                    }
+                }
+            } else if (bind > 0) {
+                // velocity at the hit u = v - (c/T) t, reflected at the face (w = +-e_i)
+                const int f = (bind - 1) >> 1;
+                for (int i = T.tid; i < n; i += T.nthr) {
+                    double u = v[i] - P.cvec[i] * Tinv * th;
+                    v[i] = (i == f) ? -u : u;
+                }
+                if (T.tid == 0) P.bound[slot] = bind;
+            }
+            if (P.max_trace > 0 && !reject) {
+                __syncthreads();
+                int k = trk0;
+                if (k < P.max_trace) {
+                    size_t o = ((size_t)slot * P.max_trace + k);
+                    for (int i = T.tid; i < n; i += T.nthr) {
+                        P.tr_hit[o * n + i] = x[i];
+                        if (bind > 0) {
+                            P.tr_v[o * n + i] = v[i];
+                            P.tr_w[o * n + i] = (i == ((bind - 1) >> 1)) ? ((bind & 1) ? 1.0 : -1.0) : 0.0;
+                        }
+                    }
+                    if (T.tid == 0) {
+                        P.tr_t[o] = th;
+                        P.tr_bind[o] = bind;
+                        P.tr_cnt[slot] = k + 1;
+                        if (k + 1 >= P.max_trace && bind != 0) P.flags[slot] |= CF_DONE;
+                    }
+                }
+            }
+        }
+        if (T.tid == 0) P.calls[slot] += 1;
+        __syncthreads();
+        if (end_step) {
+            if (reject) {
+                const double* xs = P.Xs + (size_t)slot * P.np;
+                const double* axs = P.AXs + (size_t)slot * P.mtp;
+                for (int i = T.tid; i < n; i += T.nthr) x[i] = xs[i];
+                for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] = axs[i];
+            }
+            __syncthreads();
+            int sd = sdone0 + 1;
+            if (T.tid == 0) {
+                P.steps_done[slot] = sd;
+                P.refl[slot] = 0;
+                P.bound[slot] = SW_BIND_NONE_DEV;
+            }
+            if (sd >= P.steps_total) {
+                if (T.tid == 0) P.flags[slot] |= CF_DONE;
+            } else {
+                step_start<true>(T, slot, gidv, sd, n, P.np, P.mt, P.mtp, P.V, P.X, P.Xs, P.AX, P.AXs, P.ell, P.Lpar,
+                                 P.seed, P.tag, 1, red);
+            }
+        }
+    }
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
     Team T;
@@ -86,7 +248,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
     __shared__ double sh_d[16];
     extern __shared__ __align__(16) double smem_dyn[];
 
-    const int m = P.m, n = P.n, ld = P.ld;
+    const int m = P.m, ld = P.ld;
     const int mp = (m + 7) & ~7;
     const size_t MS = (size_t)mp * ld;
     double* base = P.scratch + (size_t)blockIdx.x * P.scratch_stride;
@@ -293,156 +455,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
         }
         __syncthreads();
         double t_dense = outward ? 0.0 : (hit ? (d == 4 ? s * s : s) : SW_INF);
-
-        // ---- cube faces: per-coordinate quadratic x_i(t) = x_i + v_i t - c_i t^2 / 2T
-        if (T.warp == 0) {
-            double tpl = t_dense;
-            int bind = (tpl < SW_INF) ? 0 : SW_BIND_NONE_DEV;
-            if (P.lo) {
-                double bt = SW_INF;
-                int bi = 0x7fffffff, bcode = 0;
-                for (int i = T.lane; i < n; i += 32) {
-                    const double g = 0.5 * P.cvec[i] * Tinv;
-                    double tu = first_pos_root2(P.hi[i] - x[i], -v[i], g, bnd == 1 + 2 * i);
-                    double tl = first_pos_root2(x[i] - P.lo[i], v[i], -g, bnd == 2 + 2 * i);
-                    if (tu < bt) { bt = tu; bi = i; bcode = 1 + 2 * i; }
-                    if (tl < bt) { bt = tl; bi = i; bcode = 2 + 2 * i; }
-                }
-                for (int o = 16; o > 0; o >>= 1) {
-                    double ot = __shfl_xor_sync(0xffffffffu, bt, o);
-                    int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    int oc = __shfl_xor_sync(0xffffffffu, bcode, o);
-                    if (ot < bt || (ot == bt && oi < bi)) { bt = ot; bi = oi; bcode = oc; }
-                }
-                if (bt < tpl) { tpl = bt; bind = bcode; }
-            }
-            if (T.lane == 0) {
-                sh_d[0] = tpl;
-                sh_i[1] = bind;
-            }
-        }
-        __syncthreads();
-        const double tplus = sh_d[0];
-        const int bind = sh_i[1];
-        PROF_MARK(7);
-        if (P.mode == 1) {
-            if (T.tid == 0) {
-                P.o_tplus[slot] = tplus;
-                P.o_tminus[slot] = 0.0;
-                P.o_binding[slot] = bind;
-                P.o_status[slot] = failed ? 2 : 0;
-                P.flags[slot] = (bind == 0 && !failed) ? CF_NEED_NORMAL : 0;
-            }
-            if (P.o_kernel)
-                for (int i = T.tid; i < m; i += T.nthr) P.o_kernel[(size_t)slot * m + i] = (bind == 0) ? yy[i] : 0.0;
-            if (bind == 0 && !failed) {
-                double* yh = P.Yh + (size_t)slot * P.mtp;
-                for (int i = T.warp; i < m; i += T.nwarps)
-                    for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
-            }
-            continue;
-        }
-        // ---- HMC advance (Alg. 6): p <- p(t^), A(p) <- A(p) + t^ A(v) + t^2 C2
-        if (failed) {
-            if (T.tid == 0) {
-                P.flags[slot] |= CF_DONE | CF_FAILED;
-                P.calls[slot] += 1;
-            }
-            continue;
-        }
-        // per-chain counters read by every thread BEFORE thread 0 updates them below
-        // (a read after the update would give threads different values: a race)
-        const int refl0 = P.refl[slot];
-        const int sdone0 = P.steps_done[slot];
-        const int trk0 = (P.max_trace > 0) ? P.tr_cnt[slot] : 0;
-        const double el = P.ell[slot];
-        const bool accept = (el <= tplus);
-        const double th = accept ? el : tplus;
-        const double qa = -0.5 * th * th * Tinv;
-        for (int i = T.tid; i < n; i += T.nthr) x[i] += th * v[i] + qa * P.cvec[i];
-        for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] += th * av[i] + qa * P.Ac[i];
-        __syncthreads();
-        bool end_step = accept, reject = false;
-        if (!accept) {
-            int rf = refl0 + 1;
-            if (T.tid == 0) {
-                P.refl[slot] = rf;
-                P.ell[slot] = el - th;
-                P.nrefl[slot] += 1;
-                P.tlast[slot] = th;
-            }
-            if (rf > P.rho) {
-                reject = end_step = true;
-                if (T.tid == 0) P.nrej[slot] += 1;
-            } else if (bind == 0) {
-                if (outward) {
-                    reject = end_step = true;
-                    if (T.tid == 0) P.ndeg[slot] += 1;
-                } else {
-                    double* yh = P.Yh + (size_t)slot * P.mtp;
-                    for (int i = T.warp; i < m; i += T.nwarps)
-                        for (int j = T.lane; j <= i; j += 32) yh[pk(i, j)] = (i == j ? 1.0 : 2.0) * yy[i] * yy[j];
-                    for (int i = T.tid; i < m; i += T.nthr) P.U[(size_t)slot * m + i] = yy[i];
-                    if (T.tid == 0) {
-                        P.bound[slot] = 0;
-                        P.flags[slot] |= CF_NEED_NORMAL;
-                        int q = atomicAdd(P.ncount, 1);
-                        P.nlist[q] = slot;
-                    }
-                }
-            } else if (bind > 0) {
-                // velocity at the hit u = v - (c/T) t, reflected at the face (w = +-e_i)
-                const int f = (bind - 1) >> 1;
-                for (int i = T.tid; i < n; i += T.nthr) {
-                    double u = v[i] - P.cvec[i] * Tinv * th;
-                    v[i] = (i == f) ? -u : u;
-                }
-                if (T.tid == 0) P.bound[slot] = bind;
-            }
-            if (P.max_trace > 0 && !reject) {
-                __syncthreads();
-                int k = trk0;
-                if (k < P.max_trace) {
-                    size_t o = ((size_t)slot * P.max_trace + k);
-                    for (int i = T.tid; i < n; i += T.nthr) {
-                        P.tr_hit[o * n + i] = x[i];
-                        if (bind > 0) {
-                            P.tr_v[o * n + i] = v[i];
-                            P.tr_w[o * n + i] = (i == ((bind - 1) >> 1)) ? ((bind & 1) ? 1.0 : -1.0) : 0.0;
-                        }
-                    }
-                    if (T.tid == 0) {
-                        P.tr_t[o] = th;
-                        P.tr_bind[o] = bind;
-                        P.tr_cnt[slot] = k + 1;
-                        if (k + 1 >= P.max_trace && bind != 0) P.flags[slot] |= CF_DONE;
-                    }
-                }
-            }
-        }
-        if (T.tid == 0) P.calls[slot] += 1;
-        __syncthreads();
-        if (end_step) {
-            if (reject) {
-                const double* xs = P.Xs + (size_t)slot * P.np;
-                const double* axs = P.AXs + (size_t)slot * P.mtp;
-                for (int i = T.tid; i < n; i += T.nthr) x[i] = xs[i];
-                for (int i = T.tid; i < P.mt; i += T.nthr) ax[i] = axs[i];
-            }
-            __syncthreads();
-            int sd = sdone0 + 1;
-            if (T.tid == 0) {
-                P.steps_done[slot] = sd;
-                P.refl[slot] = 0;
-                P.bound[slot] = SW_BIND_NONE_DEV;
-            }
-            if (sd >= P.steps_total) {
-                if (T.tid == 0) P.flags[slot] |= CF_DONE;
-            } else {
-                step_start<true>(T, slot, gidv, sd, n, P.np, P.mt, P.mtp, P.V, P.X, P.Xs, P.AX, P.AXs, P.ell, P.Lpar,
-                                 P.seed, P.tag, 1, red);
-            }
-        }
+        hmc_finish(T, P, slot, gidv, x, v, av, ax, bnd, yy, t_dense, failed, outward, red, sh_d, sh_i);
         PROF_MARK(8);
     }
 }

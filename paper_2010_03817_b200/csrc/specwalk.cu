@@ -21,6 +21,7 @@
 #include "chord2.cuh"
 #include "chord3.cuh"
 #include "hmc.cuh"
+#include "hmc2.cuh"
 #include "estimators.cuh"
 #include <algorithm>
 
@@ -56,6 +57,14 @@ struct ChainBuf {
     long long* gid = nullptr;
 };
 
+// K5 split work buffers (hmc2.cuh), grown with the chain capacity on first HMC use
+struct HmcBuf {
+    long long cap = 0;
+    double *wH = nullptr, *wQ = nullptr;
+    double *wM = nullptr, *wL = nullptr, *wS = nullptr;  // own copies when the K2 split is off
+    int *il0 = nullptr, *il1 = nullptr, *cnt = nullptr;
+};
+
 struct spec_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -71,6 +80,11 @@ struct spec_ctx {
     long long hmc_stride = 0;
     int hmc_grid = 0;
     size_t hmc_smem = 0;
+    int hmc_split = 0;   // K5 as setup / (factor, Lanczos, Weyl)^k / tail (hmc2.cuh), m <= 128
+    int hmc_nt = 512, hmc_kc = 13;
+    int hf_grid = 0, hl_grid = 0, ht_grid = 0, hs_grid = 0;
+    size_t hf_smem = 0, hl_smem = 0, ht_smem = 0;
+    HmcBuf hb;
     double* ball_c = nullptr;
     double ball_r = 0.0;
     int has_ball = 0;
@@ -282,9 +296,12 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     }
     // K2 split (chord3.cuh) for 64 < m <= 128 unless SPECWALK_K2_FUSED is set (for m <= 64 the
     // fused kernel was measured faster: 1.9M vs 1.4M calls/s at m = 40; it does not spill there)
-    if ((ctx->k2_variant == 1 || ctx->k2_variant == 3) && !getenv("SPECWALK_K2_FUSED")) {
+    // (and only where the factor kernel's G, B and inverse diagonal blocks fit: mp <= 104;
+    // 104 < mp <= 112 keeps the fused variant 3)
+    const size_t f_smem = ctx->smem_bytes + sizeof(double) * 8 * (size_t)mp;  // + inverse diagonal blocks
+    if ((ctx->k2_variant == 1 || ctx->k2_variant == 3) && f_smem <= 227 * 1024 && !getenv("SPECWALK_K2_FUSED")) {
         ctx->k2_split = 1;
-        ctx->f_smem = ctx->smem_bytes + sizeof(double) * 8 * (size_t)mp;  // + inverse diagonal blocks
+        ctx->f_smem = f_smem;
         ctx->l_smem = sizeof(double) * ((size_t)mp * ctx->ld + (size_t)NVEC2 * (mp + 8) + 64);  // Q + vectors
         ctx->t_smem = sizeof(double) * ((size_t)mp * ctx->ld + 5 * (size_t)(mp + 8) + 64);
         int of = 0, ol = 0, ot = 0;
@@ -315,11 +332,13 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
 }
 
 static void free_walk(spec_ctx* ctx);
+static void free_hmc_bufs(HmcBuf& h);
 extern "C" int spec_destroy(spec_ctx* ctx) {
     if (!ctx) return SPEC_OK;
     free_walk(ctx);
     cudaSetDevice(ctx->dev);
     free_chains(ctx->cb);
+    free_hmc_bufs(ctx->hb);
     void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
     for (void* p : ps)
         if (p) cudaFree(p);
@@ -450,10 +469,45 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
     ctx->launches++;
 }
 
-// K5 (HMC-r) resources: 8 matrices of mp x ld per CTA in global scratch
+// K5 (HMC-r) resources.  G and one operand in shared memory (m <= 112): the split kernels of
+// hmc2.cuh (per-slot work buffers, allocated with the chain capacity by ensure_hmc_bufs); larger m: hmc_kernel with
+// 8 matrices of mp x ld per CTA in global scratch.
 static int ensure_hmc(spec_ctx* ctx) {
-    if (ctx->hmc_scratch) return SPEC_OK;
+    if (ctx->hmc_split || ctx->hmc_scratch) return SPEC_OK;
     const int mp = roundup(ctx->m, 8);
+    const size_t hf_smem = sizeof(double) * ((size_t)2 * mp * ctx->ld + (size_t)8 * (mp + 8) + 8 * (size_t)mp);
+    if (mp <= 128 && hf_smem <= 227 * 1024 && !getenv("SPECWALK_HMC_FUSED")) {
+        const int vl = mp + 8;
+        ctx->hmc_nt = (mp <= 64) ? 256 : 512;
+        ctx->hmc_kc = (mp <= 64) ? 8 : (mp <= 104) ? 13 : 16;
+        ctx->hf_smem = hf_smem;
+        ctx->hl_smem = sizeof(double) * ((size_t)mp * ctx->ld + (size_t)NVEC2 * vl + 64);
+        ctx->ht_smem = sizeof(double) * ((size_t)mp * ctx->ld + 4 * (size_t)vl);
+        int of = 0, ol = 0, ot = 0, os = 0;
+#define SW_HMC_SETUP(NT_, KC_)                                                                                     \
+    CK(cudaFuncSetAttribute(hmc_factor_kernel<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->hf_smem)); \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&of, hmc_factor_kernel<NT_>, NT_, ctx->hf_smem));                \
+    CK(cudaFuncSetAttribute(lanczos_kernel<NT_, KC_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->hl_smem)); \
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ol, lanczos_kernel<NT_, KC_>, NT_, ctx->hl_smem));
+        if (ctx->hmc_kc == 8) {
+            SW_HMC_SETUP(256, 8)
+        } else if (ctx->hmc_kc == 13) {
+            SW_HMC_SETUP(512, 13)
+        } else {
+            SW_HMC_SETUP(512, 16)
+        }
+#undef SW_HMC_SETUP
+        CK(cudaFuncSetAttribute(hmc_tail_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->ht_smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, hmc_tail_kernel<256>, 256, ctx->ht_smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&os, hmc_setup_kernel<256>, 256, 0));
+        if (of < 1 || ol < 1 || ot < 1 || os < 1) return fail(SPEC_ECUDA, "K5 split kernels cannot be resident");
+        ctx->hf_grid = of * ctx->num_sms;
+        ctx->hl_grid = ol * ctx->num_sms;
+        ctx->ht_grid = ot * ctx->num_sms;
+        ctx->hs_grid = os * ctx->num_sms;
+        ctx->hmc_split = 1;
+        return SPEC_OK;
+    }
     ctx->hmc_stride = (long long)8 * mp * ctx->ld;
     ctx->hmc_smem = sizeof(double) * (size_t)16 * (mp + 8);
     CK(cudaFuncSetAttribute(hmc_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->hmc_smem));
@@ -466,13 +520,96 @@ static int ensure_hmc(spec_ctx* ctx) {
     return SPEC_OK;
 }
 
-static void launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
-    int grid = count_host < ctx->hmc_grid ? count_host : ctx->hmc_grid;
-    if (grid < 1) grid = 1;
-    P.scratch = ctx->hmc_scratch;
-    P.scratch_stride = ctx->hmc_stride;
-    hmc_kernel<512><<<grid, 512, ctx->hmc_smem, ctx->stream>>>(P);
+static void free_hmc_bufs(HmcBuf& h) {
+    void* ps[] = {h.wH, h.wQ, h.wM, h.wL, h.wS, h.il0, h.il1, h.cnt};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    h = HmcBuf();
+}
+
+static int ensure_hmc_bufs(spec_ctx* ctx) {
+    HmcBuf& h = ctx->hb;
+    const long long cap = ctx->cb.cap;
+    if (cap <= h.cap) return SPEC_OK;
+    free_hmc_bufs(h);
+    const size_t mp = (size_t)roundup(ctx->m, 8), vl = mp + 8;
+    cudaError_t e = cudaSuccess;
+#define ZA(ptr, cnt) \
+    if (e == cudaSuccess) e = zalloc(&h.ptr, (size_t)(cnt));
+    ZA(wH, cap * H_NS) ZA(wQ, cap * 3 * vl) ZA(il0, cap) ZA(il1, cap) ZA(cnt, 2)
+    if (!ctx->k2_split) {
+        ZA(wM, cap * mp * ctx->ld) ZA(wL, cap * mp * ctx->ld) ZA(wS, cap * (size_t)s_stride((int)mp))
+    }
+#undef ZA
+    if (e != cudaSuccess) {
+        free_hmc_bufs(h);
+        cudaGetLastError();
+        return fail(SPEC_ENOMEM, std::string("HMC buffers: ") + cudaGetErrorString(e));
+    }
+    h.cap = cap;
+    return SPEC_OK;
+}
+
+// One HMC-r boundary-oracle call for every slot of the list (P.list / P.count_dev).
+static int launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
+    if (!ctx->hmc_split) {
+        int grid = count_host < ctx->hmc_grid ? count_host : ctx->hmc_grid;
+        if (grid < 1) grid = 1;
+        P.scratch = ctx->hmc_scratch;
+        P.scratch_stride = ctx->hmc_stride;
+        hmc_kernel<512><<<grid, 512, ctx->hmc_smem, ctx->stream>>>(P);
+        ctx->launches++;
+        return SPEC_OK;
+    }
+    int rc = ensure_hmc_bufs(ctx);
+    if (rc) return rc;
+    HmcBuf& h = ctx->hb;
+    P.wH = h.wH;
+    P.wQ = h.wQ;
+    if (!ctx->k2_split) {
+        P.wM = h.wM;
+        P.wL = h.wL;
+        P.wS = h.wS;
+    }
+    P.zall = 1;
+    auto g = [&](int gmax) { return std::max(1, std::min(count_host, gmax)); };
+    int* il[2] = {h.il0, h.il1};
+    CK(cudaMemsetAsync(h.cnt, 0, 2 * sizeof(int), ctx->stream));
+    ChordParams Ps = P;
+    Ps.nxt_list = il[0];
+    Ps.nxt_count = h.cnt;
+    hmc_setup_kernel<256><<<g(ctx->hs_grid), 256, 0, ctx->stream>>>(Ps);
     ctx->launches++;
+    const int wblocks = std::max(1, std::min((count_host + 255) / 256, 4096));
+    for (int k = 0; k < HMC_MAX_IT; ++k) {
+        ChordParams Pk = P;
+        Pk.list = il[k & 1];
+        Pk.count_dev = h.cnt + (k & 1);
+        Pk.nxt_list = il[(k + 1) & 1];
+        Pk.nxt_count = h.cnt + ((k + 1) & 1);
+        CK(cudaMemsetAsync(Pk.nxt_count, 0, sizeof(int), ctx->stream));
+        if (ctx->hmc_kc == 8) {
+            hmc_factor_kernel<256><<<g(ctx->hf_grid), 256, ctx->hf_smem, ctx->stream>>>(Pk);
+            lanczos_kernel<256, 8><<<g(ctx->hl_grid), 256, ctx->hl_smem, ctx->stream>>>(Pk);
+        } else if (ctx->hmc_kc == 13) {
+            hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
+            lanczos_kernel<512, 13><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
+        } else {
+            hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
+            lanczos_kernel<512, 16><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
+        }
+        hmc_weyl_kernel<<<wblocks, 256, 0, ctx->stream>>>(Pk);
+        ctx->launches += 3;
+        if ((k & 3) == 3) {  // most chains stop after ~4 steps: look at the list every 4 iterations
+            int left = 0;
+            CK(cudaMemcpyAsync(&left, Pk.nxt_count, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            if (left == 0) break;
+        }
+    }
+    hmc_tail_kernel<256><<<g(ctx->ht_grid), 256, ctx->ht_smem, ctx->stream>>>(P);
+    ctx->launches++;
+    return SPEC_OK;
 }
 
 static NormalParams normal_params(spec_ctx* ctx, int mode) {
@@ -521,7 +658,8 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     P.o_tminus = o_tm; P.o_tplus = o_tp; P.o_kernel = o_ker; P.o_binding = o_bind; P.o_status = o_stat;
     if (hmcT > 0.0) {
         P.Temp = hmcT;
-        launch_hmc(ctx, P, B);
+        int rc = launch_hmc(ctx, P, B);
+        if (rc) return rc;
     } else {
         launch_chord(ctx, P, B);
     }
@@ -735,8 +873,10 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             P.list = list;
             P.count_dev = b.counters;
             P.count_host = count;
-            if (W.p.kind == SPEC_WALK_HMC) launch_hmc(ctx, P, count);  // K5
-            else launch_chord(ctx, P, count, (e && ctx->k2_split) ? &e[5] : nullptr);  // K2
+            if (W.p.kind == SPEC_WALK_HMC) {  // K5
+                int rc = launch_hmc(ctx, P, count);
+                if (rc) return rc;
+            } else launch_chord(ctx, P, count, (e && ctx->k2_split) ? &e[5] : nullptr);  // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
             launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
             if (e) CK(cudaEventRecord(e[3], ctx->stream));

@@ -36,6 +36,10 @@ CASES = [
     ("rand_100_100", lambda: specgen.rand_cube(100, 100, 3), 1.0, 1.0),
     ("mixed_12_30", lambda: specgen.rand_cube(12, 30, 5, scale=1 / np.sqrt(12)), 0.5, 0.3),
     ("cube_only_6", lambda: specgen.cube_only(6), 1.0, 0.2),
+    # K5 split variants: <256, KC 8> (m <= 64), <512, 13> (m <= 104), <512, 16> (m <= 112);
+    # larger m runs the fused global-scratch hmc_kernel
+    ("rand_16_110", lambda: specgen.rand_cube(16, 110, 7), 1.0, 1.0),
+    ("rand_10_136", lambda: specgen.rand_cube(10, 136, 8), 1.0, 1.0),
 ]
 
 
@@ -54,7 +58,10 @@ def test_hmc_oracle_interior_parity(name, make, vscale, T):
     _cmp(res, refs, lmi)
 
 
-@pytest.mark.parametrize("name,make,vscale,T", CASES[:4], ids=[c[0] for c in CASES[:4]])
+BCASES = CASES[:4] + CASES[5:]
+
+
+@pytest.mark.parametrize("name,make,vscale,T", BCASES, ids=[c[0] for c in BCASES])
 def test_hmc_oracle_boundary_start_parity(name, make, vscale, T):
     """After a dense reflection the segment starts on the boundary: sqrt(t) deflation (SURVEY a-10)."""
     import paper_2010_03817_b200 as sw
@@ -105,6 +112,31 @@ def test_hmc_trajectory_parity():
             good &= g[i]["binding"][j] == o["binding"][j]
         ok += bool(good)
     assert ok >= 0.9 * len(chains), ok
+
+
+def test_hmc_trajectory_parity_m40():
+    """Trajectories on the K5 split path with the <256, KC 8> kernels (m = 40): many Weyl
+    iterations per call over compacted lists, boundary starts after every dense hit."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.rand_cube(12, 40, 4, scale=1 / np.sqrt(12))
+    lmi = oracle.Lmi(inst)
+    c = specgen.objective(12, 4)
+    T, L, rho = 0.5, 2.0, 100
+    S = sw.Spectrahedron.from_instance(inst)
+    S.set_objective(c)
+    chains = list(range(8))
+    g = S.walk_trace(chains, steps=10, L=L, rho=rho, seed=6, max_refl=10, kind=sw.HMC, T=T)
+    ok = 0
+    for i, ch in enumerate(chains):
+        o = oracle.trace(lmi, oracle.HMC, 6, ch, 10, L, rho, 10, T=T, c=c)
+        k = min(len(o["t"]), len(g[i]["t"]))
+        good = k == len(o["t"]) and k > 0
+        for j in range(k):
+            good &= np.linalg.norm(g[i]["hit_x"][j] - o["hit_x"][j]) <= 1e-8 * max(np.linalg.norm(o["hit_x"][j]), .1)
+            good &= np.linalg.norm(g[i]["v_after"][j] - o["v_after"][j]) <= 1e-8 * max(np.linalg.norm(o["v_after"][j]), 1)
+            good &= g[i]["binding"][j] == o["binding"][j]
+        ok += bool(good)
+    assert ok >= 0.75 * len(chains), ok
 
 
 def test_hmc_boltzmann_cube_moments_gpu():
