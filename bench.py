@@ -41,6 +41,7 @@ SEED = 4
 INSTANCE_SEED = 3  # BASELINE.json configs[3] instance (SURVEY 8(d).1 "M100")
 L_TAU = 2.0 * math.sqrt(N_DIM)
 RHO = 10 * N_DIM
+HMC_L = 1.09  # configs[3] HMC trajectory length: the diameter estimate
 LANCZOS_K = 55  # Lanczos iterations at m = 100 in the algorithmic flop model
 
 WORKLOAD = (f"M100: billiard walk (Alg. 5) on the BASELINE.json configs[3] instance (rand-cube n=m={N_DIM}, "
@@ -351,6 +352,41 @@ def run_ours(args):
                            f"the M100 instance (H2D x0, D2H end points + moments inside the region; includes the "
                            f"reflection-count tail of the step)"}
 
+    # ---- configs[3]'s own workload (reflective HMC, T = 1, c ~ N(0, I) normalised) on the same
+    # instance: HMC-r boundary-oracle calls/s over scheduler rounds (K5 split kernels)
+    hmc = None
+    if args.hmc_rounds > 0:
+        c3 = specgen.objective(N_DIM, 3)
+        S.set_objective(c3)
+        S.walk_begin(local_chains, 200, HMC_L, RHO, 3, kind=sw.HMC, T=1.0, chain_begin=begin)
+        S.walk_rounds(2)
+        h0 = S.walk_stats_now()
+        hl0 = S.kernel_launches()
+        barrier()
+        he0 = torch.cuda.Event(enable_timing=True)
+        he1 = torch.cuda.Event(enable_timing=True)
+        he0.record(stream)
+        S.walk_rounds(args.hmc_rounds)
+        he1.record(stream)
+        he1.synchronize()
+        barrier()
+        hms = he0.elapsed_time(he1)
+        h1 = S.walk_stats_now()
+        S.walk_end()
+        ht = torch.tensor([hms, float(h1["calls"] - h0["calls"])], dtype=torch.float64, device=coll_dev)
+        if dist is not None:
+            hmax = ht.clone()
+            dist.all_reduce(hmax[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(ht[1:], op=dist.ReduceOp.SUM)
+            hms, hcalls = float(hmax[0]), float(ht[1])
+        else:
+            hcalls = float(ht[1])
+        hmc = {"metric": "HMC-r boundary-oracle calls/s (configs[3]: n=m=100, T=1, c~N(0,I) normalised)",
+               "value": hcalls / (hms * 1e-3), "unit": "calls/s", "chains": chains, "rounds": args.hmc_rounds,
+               "ms": hms, "calls": hcalls, "L": HMC_L, "gpu_launches": int(S.kernel_launches() - hl0),
+               "note": "one quadratic-pencil chord per chain per round (Weyl stepping, ~5 Cholesky + Lanczos "
+                       "iterations per call); device events on the library stream, max over ranks"}
+
     # ---- BASELINE metric, second half: volume time at n = m = 40 (configs[2], eps 0.1, 4096 chains/phase)
     vol = None
     if args.volume_seeds > 0:
@@ -418,6 +454,7 @@ def run_ours(args):
         "e2e": e2e,
         "cpu_baseline": cpu,
         "volume_n40": vol,
+        "hmc_configs3": hmc,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -435,6 +472,7 @@ def main():
     ap.add_argument("--e2e-chains", type=int, default=2048)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--volume-seeds", type=int, default=3)
+    ap.add_argument("--hmc-rounds", type=int, default=4)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -370,4 +370,97 @@ __device__ void trsm_inv_blocked_la(const Team& T, const double* G, const double
     }
 }
 
+// acc -= A(8 x K) * B(K x 8) as tile_msub, with two accumulator chains (even / odd k-steps)
+// so that consecutive DMMAs do not wait on each other.
+template <bool BNK>
+__device__ __forceinline__ void tile_msub2(double (&acc)[2], const double* A, int lda, const double* Bp, int ldb,
+                                           int K, int lane) {
+    const int r = lane >> 2, q = lane & 3;
+    double acc2[2] = {0.0, 0.0};
+    int k0 = 0;
+#pragma unroll 2
+    for (; k0 + 8 <= K; k0 += 8) {
+        const double a0 = -A[r * lda + k0 + q];
+        const double a1 = -A[r * lda + k0 + 4 + q];
+        const double b0 = BNK ? Bp[r * ldb + k0 + q] : Bp[(k0 + q) * ldb + r];
+        const double b1 = BNK ? Bp[r * ldb + k0 + 4 + q] : Bp[(k0 + 4 + q) * ldb + r];
+        dmma_t(acc, a0, b0);
+        dmma_t(acc2, a1, b1);
+    }
+    if (k0 < K) {
+        const double a0 = -A[r * lda + k0 + q];
+        const double b0 = BNK ? Bp[r * ldb + k0 + q] : Bp[(k0 + q) * ldb + r];
+        dmma_t(acc, a0, b0);
+    }
+    acc[0] += acc2[0];
+    acc[1] += acc2[1];
+}
+
+// B <- L^{-1} B, left-looking with one warp per 8-column block: for each block row i,
+// acc = B_ic - L_i,0:i X_0:i,c (one DMMA chain over all earlier blocks, accumulator in
+// registers), X_ic = L_ii^{-1} acc.  Column blocks are independent, so there is no CTA
+// barrier inside (the right-looking trsm_inv_blocked_la needs one per block step and
+// re-loads / stores every trailing tile at each step).  Ends with a barrier.
+__device__ void trsm_ll_cols(const Team& T, const double* G, const double* Lv, double* B, int n, int ld) {
+    const int TB = n >> 3;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    for (int cb = T.warp; cb < TB; cb += T.nwarps) {
+        double* Bc = B + cb * 8;
+        for (int ib = 0; ib < TB; ++ib) {
+            double* C = Bc + ib * 8 * ld;
+            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            if (ib > 0) tile_msub2<false>(acc, G + ib * 8 * ld, ld, Bc, ld, 8 * ib, T.lane);
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+            __syncwarp();
+            tile_mul_w(acc, Lv + ib * 64, 8, C, ld, T.lane);
+            __syncwarp();
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
+// B <- B L^{-T}, left-looking with one warp per 8-row block: M_rj = (B_rj - M_r,0:j L_j,0:j^T)
+// L_jj^{-T}, j ascending (each block row only reads itself and L).  Ends with a barrier.
+__device__ void trsm_ll_rows(const Team& T, const double* G, const double* Lv, double* B, int n, int ld) {
+    const int TB = n >> 3;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    for (int rb = T.warp; rb < TB; rb += T.nwarps) {
+        double* Br = B + rb * 8 * ld;
+        for (int jb = 0; jb < TB; ++jb) {
+            double* C = Br + jb * 8;
+            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            if (jb > 0) tile_msub2<true>(acc, Br, ld, G + jb * 8 * ld, ld, 8 * jb, T.lane);
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+            __syncwarp();
+            tile_mul_wt(acc, C, ld, Lv + jb * 64, 8, T.lane);
+            __syncwarp();
+            C[r * ld + 2 * q] = acc[0];
+            C[r * ld + 2 * q + 1] = acc[1];
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
+// the congruence B <- L^{-1} B L^{-T} of the split factor kernels (SW_TRSM_LL = 0: the
+// right-looking pair)
+#ifndef SW_TRSM_LL
+#define SW_TRSM_LL 1
+#endif
+__device__ __forceinline__ void congruence_inv(const Team& T, const double* G, const double* Lv, double* B, int n,
+                                               int ld) {
+#if SW_TRSM_LL
+    trsm_ll_cols(T, G, Lv, B, n, ld);
+    trsm_ll_rows(T, G, Lv, B, n, ld);
+#else
+    trsm_inv_blocked_la<false>(T, G, Lv, B, n, ld);
+    trsm_inv_blocked_la<true>(T, G, Lv, B, n, ld);
+#endif
+}
+
 }  // namespace sw

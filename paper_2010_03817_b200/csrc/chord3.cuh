@@ -157,8 +157,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
             if (!okc) {
                 status |= ST_FAILED;
             } else {
-                trsm_inv_blocked_la<false>(T, G, Lv, B, mdp, ld);
-                trsm_inv_blocked_la<true>(T, G, Lv, B, mdp, ld);
+                congruence_inv(T, G, Lv, B, mdp, ld);
                 PROF_MARK(3);
                 // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
                 double* Mw = P.wM + (size_t)slot * P.w_mstride;

@@ -254,13 +254,13 @@ __global__ void __launch_bounds__(NT, 1) hmc_factor_kernel(ChordParams P) {
             }
             continue;
         }
-        trsm_inv_blocked_la<false>(T, G, Lv, B, mp, ld);
-        trsm_inv_blocked_la<true>(T, G, Lv, B, mp, ld);
+        congruence_inv(T, G, Lv, B, mp, ld);
         // N~_first (symmetrised) parked in the Lanczos buffer
         double* Mw = P.wM + (size_t)slot * P.w_mstride;
         for (int i = T.warp; i < mp; i += T.nwarps)
             for (int j = T.lane; j < mp; j += 32) Mw[i * ld + j] = 0.5 * (B[i * ld + j] + B[j * ld + i]);
         __syncthreads();
+        PROF_MARK(3);
         // second operand: C_1 = A(v) (quadratic) or C_2 = inner(g1) + corner g2 (quartic)
         for (int i = T.warp; i < mp; i += T.nwarps)
             for (int j = T.lane; j <= i; j += 32) {
@@ -289,11 +289,12 @@ __global__ void __launch_bounds__(NT, 1) hmc_factor_kernel(ChordParams P) {
         __syncthreads();
         mirror_upper(T, B, mp, ld);
         __syncthreads();
-        trsm_inv_blocked_la<false>(T, G, Lv, B, mp, ld);
-        trsm_inv_blocked_la<true>(T, G, Lv, B, mp, ld);
+        PROF_MARK(5);
+        congruence_inv(T, G, Lv, B, mp, ld);
+        PROF_MARK(6);
         if (d == 4) fwd_solve_vecs(T, G, Lv, X, 3, vl, mp, ld);
         __syncthreads();
-        PROF_MARK(3);
+        PROF_MARK(7);
         // N_1 -> -N_1 (Lanczos operand, in place over N~_first), |N_j|_F^2 for j >= 2
         double f2 = 0.0, f3 = 0.0, f4 = 0.0;
         const double* pv = X;

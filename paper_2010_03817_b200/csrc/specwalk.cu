@@ -976,6 +976,8 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
                     (double)ph[25] / fmax(1.0, (double)ph[24]), (double)ph[22] / fmax(1.0, (double)ph[20]),
                     (double)ph[26] / fmax(1.0, (double)ph[24]), (double)ph[23] / fmax(1.0, (double)(ph[20] + ph[24])),
                     (double)ph[27] / fmax(1.0, (double)(ph[20] + ph[24])));
+        if (ph[17] > 0)
+            fprintf(stderr, "[specwalk prof] hmc: Weyl iterations/call=%.2f\n", (double)ph[17] / (double)hs[0]);
         double it = (double)ph[10];
         fprintf(stderr, "[specwalk prof] per lanczos iteration: matvec=%.0f dots=%.0f axpy+norm(+pass2)=%.0f qwrite=%.0f pass2_frac=%.3f\n",
                 ph[12] / it, ph[13] / it, ph[14] / it, ph[16] / it, ph[15] / it);
