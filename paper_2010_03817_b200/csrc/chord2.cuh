@@ -19,6 +19,9 @@
 namespace sw {
 
 constexpr int NVEC2 = 20;
+#ifndef SW_GLOBAL_LL
+#define SW_GLOBAL_LL 1  // global-scratch variant (m > 112): left-looking congruence
+#endif
 #ifndef SW_LANCZOS_TOL
 // Lanczos convergence: residual of the top Ritz pair <= SW_LANCZOS_TOL |T_J|.  The Ritz value
 // error is ~res^2 / gap; the Ritz vector (the kernel vector y, the normal) error ~res / gap.
@@ -1424,6 +1427,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
         if (!outward && md >= 1) {
             // global-scratch variant (m > 128): the inverse-diagonal-block DMMA factorisations
             // (measured +1% there; the shared-memory variants keep the substitution versions)
+            // (the shared-memory variants with cholesky_inv_blocked_la + the left-looking
+            // congruence were measured 3-7% slower at m = 10..60)
             double* Lv = vec + NVEC2 * vl + 64;
             bool okc = SMEM ? cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2])
                             : cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
@@ -1431,7 +1436,9 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
             if (!okc) {
                 failed = true;
             } else {
-                if (SMEM) {
+                if (!SMEM && SW_GLOBAL_LL) {  // m > 112: +11% at m = 200
+                    congruence_inv(T, G, Lv, B, mdp, ld);
+                } else if (SMEM) {
                     trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
                     trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
                 } else {
