@@ -970,7 +970,10 @@ __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, co
 // bookkeeping of lanczos_reg kept out of registers, and the decision.
 enum : int { CK_TTOP = 0, CK_RTOP = 1, CK_TBOT = 2, CK_RBOT = 3, CK_TNORM = 10 /* 2 slots (parity) */,
              CK_GHI = 12, CK_GLO = 13, CK_INTOP = 14, CK_INBOT = 15, CK_LRES = 16, CK_JPREV = 17, CK_NEXT = 18,
-             CK_DONE = 19, CK_HINTED = 20 };
+             CK_DONE = 19, CK_HINTED = 20,
+             // asynchronous checks (lanczos_reg with a spare warp): J available to check, first
+             // converged J (0 = none yet), J of exhaustion, the stop decision for the compute warps
+             CK_JAV = 21, CK_STOPJ = 22, CK_EXH = 23, CK_DEC = 24 };
 
 // Lanczos convergence check, run by warp 0 (lane 0 does the bookkeeping): Ritz
 // value(s) by the warp-parallel Laguerre between the inner bound (previous Ritz
@@ -1060,6 +1063,73 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
 
+#ifndef SW_ASYNC_CHECK
+// measured 3% slower at m = 100: a check takes ~33k cycles next to the iterating warps, so
+// convergence is seen ~8 iterations late (56 run for 48 used), which costs more than the
+// synchronous checks' idle time
+#define SW_ASYNC_CHECK 0
+#endif
+// sum over the row-owner lanes (g = lane & 3 == 0) of a warp: the other lanes hold zeros, so
+// the xor-1 / xor-2 levels of a full warp_sum add exact zeros and can be skipped (same value)
+__device__ __forceinline__ double owner_sum(double v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 16);  // warp_sum's order
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 4);
+    return v;
+}
+// balanced pairwise sum of the N per-warp partials (depth log2 N instead of N)
+template <int N>
+__device__ __forceinline__ double tree_sum(const double* p) {
+    if constexpr (N == 1) return p[0];
+    else return tree_sum<N / 2>(p) + tree_sum<N - N / 2>(p + N / 2);
+}
+__device__ __forceinline__ double vload(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
+__device__ __forceinline__ void vstore(double* p, double v) { *reinterpret_cast<volatile double*>(p) = v; }
+
+// The checker warp of lanczos_reg's asynchronous mode: checks T_J at the same J sequence as the
+// synchronous mode (first check by size, later ones predicted from the residual rate), each as
+// soon as the compute warps have published alpha / beta up to J, while they keep iterating.
+// Stops at the first converged J (CK_STOPJ), which makes the result independent of timing.
+__device__ __noinline__ void lanczos_checker(const int lane, const int oAl, const int oBe, const int oB2,
+                                             const int oRbe, const bool need_bot, const int md, const int oShd,
+                                             int next, unsigned long long* prof) {
+    extern __shared__ __align__(16) double sm[];
+    while (true) {
+        int target = next;
+        const int exh = (int)vload(sm + oShd + CK_EXH);
+        if (exh > 0 && exh < target) target = exh;
+        if ((int)vload(sm + oShd + CK_JAV) < target) {
+            __nanosleep(64);
+            continue;
+        }
+        __threadfence_block();
+        const int J = target;
+        // |T_J| and beta_{J-1} exactly as the compute warps form them (max is exact)
+        double tn = 0.0;
+        for (int i = lane; i < J; i += 32)
+            tn = fmax(tn, fabs(sm[oAl + i]) + sm[oBe + i] + (i > 0 ? sm[oBe + i - 1] : 0.0));
+        tn = warp_max(tn);
+        const double beta = sm[oBe + J - 1];
+        const bool exhausted = (J == md) || !(beta > 1e-15 * tn);
+        const long long t0 = clock64();
+        lanczos_check(lane, oAl, oBe, oB2, oRbe, J, beta, tn, need_bot, exhausted, md, oShd, prof);
+        __syncwarp();
+        if (prof && lane == 0) {
+            atomicAdd(&prof[19], (unsigned long long)(clock64() - t0));
+            atomicAdd(&prof[28], 1ull);
+        }
+        const bool done = sm[oShd + CK_DONE] != 0.0;
+        if (done) {
+            if (lane == 0) {
+                __threadfence_block();
+                vstore(sm + oShd + CK_STOPJ, (double)J);
+            }
+            return;
+        }
+        next = (int)sm[oShd + CK_NEXT];
+    }
+}
+
 template <int NT, int KC, bool GM = false, bool USEQT = true>
 __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
                                            const bool need_bot, const int oVec, const int vl, const int oRed,
@@ -1070,12 +1140,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     static_assert(KC <= NT / 32, "M row segment of a thread: 8 KC columns <= NT / 4 rows");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
+    // asynchronous checks when a whole warp has no M rows (m = 65..104 on 512 threads): the
+    // last warp runs the convergence checks while the others iterate (named barrier 1)
+    constexpr bool ASYNC = SW_ASYNC_CHECK && (NT - 32 >= 32 * KC);
+    constexpr int NWC = ASYNC ? NW - 1 : NW;  // compute warps
     const int oAl = oVec + V_AL * vl, oBe = oVec + V_BE * vl, oRbe = oVec + V_RBE * vl, oHb = oVec + V_HB * vl;
     const int oB2 = oVec + V_B2 * vl;
     const int oWu = oVec + V_LZ * vl;  // wu0, wu1 (ping-pong), wp: 3 x (mdp + 8)
     const int oWp = oWu + 2 * (mdp + 8);
     const int oRB = oRed + 16;         // per-warp partial norms
     const int oShd = oRed + 32;        // check results (4) and thetas (2)
+    auto csync = [&]() {
+        if (ASYNC) asm volatile("bar.sync 1, %0;\n" ::"n"(NT - 32) : "memory");
+        else __syncthreads();
+    };
     // transposed basis: in M's shared space once M is in registers, or a given region
     const int oQT = (oQTin >= 0) ? oQTin : oM;
     const int r = tid >> 2, g = tid & 3;
@@ -1108,12 +1186,24 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     }
     if (owner) sm[oWu + r] = wr;
     double p0 = (g == 0) ? wr * wr : 0.0;
-    p0 = warp_sum(p0);
+    p0 = owner_sum(p0);
     if (lane == 0) sm[oRB + warp] = p0;
+    if (tid == 0) {  // bookkeeping of the checks lives in shared memory (register pressure)
+        sm[oShd + CK_INTOP] = -SW_INF;
+        sm[oShd + CK_INBOT] = SW_INF;
+        sm[oShd + CK_JPREV] = 0.0;
+        sm[oShd + CK_LRES] = 0.0;
+        sm[oShd + CK_TTOP] = -SW_INF;
+        sm[oShd + CK_TBOT] = SW_INF;
+        sm[oShd + CK_HINTED] = 0.0;
+        sm[oShd + CK_JAV] = 0.0;
+        sm[oShd + CK_STOPJ] = 0.0;
+        sm[oShd + CK_EXH] = 0.0;
+        sm[oShd + CK_DEC] = 0.0;
+    }
     __syncthreads();  // also: every thread has its M row in registers (QT may overwrite M)
     double nn0 = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) nn0 += sm[oRB + w];
+    nn0 = tree_sum<NW>(sm + oRB);
     double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
     double bjm1 = 0.0;
     // first check: 2 before the chain's previous iteration count (consecutive calls
@@ -1126,15 +1216,9 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     int next_check = (md <= 24) ? md : (md <= 64) ? (md * 4) / 5 : max(12, (md * 2) / 5);
     int J = 0;
     double tnorm = 0.0;
-    if (tid == 0) {  // bookkeeping of the checks lives in shared memory (register pressure)
-        sm[oShd + CK_INTOP] = -SW_INF;
-        sm[oShd + CK_INBOT] = SW_INF;
-        sm[oShd + CK_JPREV] = 0.0;
-        sm[oShd + CK_LRES] = 0.0;
-        sm[oShd + CK_TTOP] = -SW_INF;
-        sm[oShd + CK_TBOT] = SW_INF;
-        sm[oShd + CK_HINTED] = 0.0;
-    }
+    if (ASYNC && warp == NW - 1) {
+        lanczos_checker(lane, oAl, oBe, oB2, oRbe, need_bot, md, oShd, next_check, prof);
+    } else {
 #if SW_PROF_LANCZOS
     long long c_mv = 0, c_dot = 0, c_upd = 0, c_chk = 0, c_t = clock64();
 #define SW_LZ_STAMP(acc) if (prof) { long long c = clock64(); acc += c - c_t; c_t = c; }
@@ -1176,14 +1260,22 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             }
             sm[oWp + r] = wpr;
         }
-        __syncthreads();
+        csync();
         SW_LZ_STAMP(c_mv)
+        if (ASYNC) {  // a check has converged at an earlier J: stop (this matvec is discarded)
+            const int dec = (int)sm[oShd + CK_DEC];
+            if (dec > 0) {
+                if (prof && tid == 0) atomicAdd(&prof[18], (unsigned long long)j);
+                J = dec;
+                break;
+            }
+        }
         // ---- (2)+(3) classical Gram-Schmidt of w' against q_0..q_j; a second pass
         // (DGKS) only on severe cancellation (|w| < 1e-6 |w'|, e.g. an invariant subspace)
         double wcur = wpr, alpha = 0.0, nnb = 0.0, nn = 0.0;
         for (int pass = 0; pass < 2; ++pass) {
             // (2) h_i = q_i . w for i <= j, and |w|^2 (slot j + 1): 8 lanes per dot, 4 dots per warp
-            for (int ib = 4 * warp; ib <= j + 1; ib += 4 * NW) {
+            for (int ib = 4 * warp; ib <= j + 1; ib += 4 * NWC) {
                 const int i = ib + du;
                 double sacc = 0.0;
                 if (i <= j + 1) {
@@ -1209,7 +1301,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
                     if (i == j + 1) sm[oShd + 8] = sacc;
                 }
             }
-            __syncthreads();
+            csync();
             SW_LZ_STAMP(c_dot)
             // (3) w -= Q h (row r: lane g takes the pairs i = 2 g + 8 k)
             double acc0 = 0.0, acc1 = 0.0;
@@ -1238,16 +1330,15 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             alpha += sm[oHb + j];
             if (pass == 0) nnb = sm[oShd + 8];
             double pb = (g == 0) ? wcur * wcur : 0.0;
-            pb = warp_sum(pb);
+            pb = owner_sum(pb);
             if (lane == 0) sm[oRB + warp] = pb;
             if (owner) sm[oUn + r] = wcur;
-            __syncthreads();
+            csync();
             nn = 0.0;
-#pragma unroll
-            for (int ww = 0; ww < NW; ++ww) nn += sm[oRB + ww];
+            nn = tree_sum<NWC>(sm + oRB);
             if (nn >= 1e-12 * nnb) break;
             if (owner) sm[oWp + r] = wcur;  // second pass on w
-            __syncthreads();
+            csync();
         }
         wr = wcur;
         const double beta = sqrt(nn);
@@ -1257,6 +1348,11 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             sm[oBe + j] = beta;
             sm[oB2 + j] = nn;
             sm[oRbe + j] = rsb;
+            if (ASYNC) {  // publish T_{j+1}; pick up a converged check for the next iteration
+                __threadfence_block();
+                vstore(sm + oShd + CK_JAV, (double)(j + 1));
+                sm[oShd + CK_DEC] = vload(sm + oShd + CK_STOPJ);
+            }
         }
         tnorm = fmax(tnorm, fabs(alpha) + beta + bjm1);
         bjm1 = beta;
@@ -1264,7 +1360,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         J = j + 1;
         const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
         SW_LZ_STAMP(c_upd)
-        if (exhausted || J >= next_check) {
+        if (ASYNC) {
+            if (exhausted) {  // nothing left to iterate: wait for the checker (it checks here at the latest)
+                if (tid == 0) {
+                    vstore(sm + oShd + CK_EXH, (double)J);
+                    double st;
+                    while ((st = vload(sm + oShd + CK_STOPJ)) == 0.0) __nanosleep(64);
+                    sm[oShd + CK_DEC] = st;
+                }
+                csync();
+                if (prof && tid == 0) atomicAdd(&prof[18], (unsigned long long)J);
+                J = (int)sm[oShd + CK_DEC];
+                break;
+            }
+        } else if (exhausted || J >= next_check) {
             __syncthreads();  // al / be / b2 / rbe and the bookkeeping of this step visible
             lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, tnorm, need_bot, exhausted, md, oShd, prof);
             __syncthreads();
@@ -1281,6 +1390,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         atomicAdd(&prof[9], (unsigned long long)c_chk);
     }
 #endif
+    }  // compute warps
 #undef SW_LZ_STAMP
     (void)prof;
     __syncthreads();
