@@ -864,6 +864,61 @@ __device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB
     return sJ / sqrt(nn);
 }
 
+// p_J(x), p_J'(x), p_J''(x) of T_J by the three-term recurrence (one lane, its own x), in
+// groups of 4 steps with a 2^+-400 rescale after each group; SIGNS also tracks whether every
+// p_i has the sign of "x outside the spectrum" (Sturm: above all for top, below all for bottom).
+// Full groups run without per-step predicates (no divergence bookkeeping in the chain).
+template <bool SIGNS>
+__device__ __forceinline__ bool tri_charpoly3(const int oA, const int oB2, const int J, const double x, const bool top,
+                                              double& p1, double& d1, double& s1) {
+    extern __shared__ __align__(16) double sm[];
+    double p0 = 1.0, d0 = 0.0, s0 = 0.0;
+    p1 = x - sm[oA];
+    d1 = 1.0;
+    s1 = 0.0;
+    bool outside = top ? (p1 > 0.0) : (p1 < 0.0);
+    auto step = [&](const double a, const double b2, const int i) {
+        const double t = x - a;
+        const double qp = -b2 * p0, qd = fma(-b2, d0, p1), qs = fma(-b2, s0, 2.0 * d1);
+        p0 = p1; d0 = d1; s0 = s1;
+        p1 = fma(t, p0, qp);
+        d1 = fma(t, d0, qd);
+        s1 = fma(t, s0, qs);
+        if (SIGNS) outside = outside && (top ? (p1 > 0.0) : ((i & 1) ? (p1 > 0.0) : (p1 < 0.0)));
+    };
+    auto rescale = [&]() {
+        const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
+        if (ap > 0x1p+400) {
+            p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
+            p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
+        } else if (ap < 0x1p-400) {
+            p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
+            p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
+        }
+    };
+    int i0 = 1;
+    double an[4], bn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { an[u] = sm[oA + 1 + u]; bn[u] = sm[oB2 + u]; }
+    for (; i0 + 3 < J; i0 += 4) {  // full groups (reads up to 7 slots past J: values unused)
+        double ac[4], bc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { ac[u] = an[u]; bc[u] = bn[u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { an[u] = sm[oA + i0 + 4 + u]; bn[u] = sm[oB2 + i0 + 3 + u]; }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) step(ac[u], bc[u], i0 + u);
+        rescale();
+    }
+    if (i0 < J) {  // the last, partial group
+        step(an[0], bn[0], i0);
+        if (i0 + 1 < J) step(an[1], bn[1], i0 + 1);
+        if (i0 + 2 < J) step(an[2], bn[2], i0 + 2);
+        rescale();
+    }
+    return outside;
+}
+
 // Warp-parallel extreme Ritz value of T_J: every lane runs Laguerre (one
 // recurrence sweep per iteration) from its own start x_l = lo + (hi - lo) 2^(-l/2)
 // (top; mirrored for the bottom).  A start is valid if its first sweep shows it
@@ -884,42 +939,10 @@ __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, co
     bool valid = true, done = false, has_step = false, restarted = (hsafe == 0.0);
     double last_step = 0.0;
     for (int it = 0; it < 40; ++it) {
-        double p0 = 1.0, d0 = 0.0, s0 = 0.0;
-        double p1 = x - sm[oA], d1 = 1.0, s1 = 0.0;
-        bool outside = top ? (p1 > 0.0) : (p1 < 0.0);
-        // steps i = 1 .. J-1 in groups of 4, the next group's a / b2 loaded ahead
-        // (reads up to 7 slots past J: inside the vector slot, values unused)
-        double an[4], bn[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { an[u] = sm[oA + 1 + u]; bn[u] = sm[oB2 + u]; }
-        for (int i0 = 1; i0 < J; i0 += 4) {
-            double ac[4], bc[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { ac[u] = an[u]; bc[u] = bn[u]; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) { an[u] = sm[oA + i0 + 4 + u]; bn[u] = sm[oB2 + i0 + 3 + u]; }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u;
-                if (i < J) {
-                    const double t = x - ac[u], b2 = bc[u];
-                    const double qp = -b2 * p0, qd = fma(-b2, d0, p1), qs = fma(-b2, s0, 2.0 * d1);
-                    p0 = p1; d0 = d1; s0 = s1;
-                    p1 = fma(t, p0, qp);
-                    d1 = fma(t, d0, qd);
-                    s1 = fma(t, s0, qs);
-                    if (it == 0) outside = outside && (top ? (p1 > 0.0) : ((i & 1) ? (p1 > 0.0) : (p1 < 0.0)));
-                }
-            }
-            const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
-            if (ap > 0x1p+400) {
-                p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
-                p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
-            } else if (ap < 0x1p-400) {
-                p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
-                p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
-            }
-        }
+        double p1, d1, s1;
+        bool outside = false;
+        if (it == 0) outside = tri_charpoly3<true>(oA, oB2, J, x, top, p1, d1, s1);
+        else tri_charpoly3<false>(oA, oB2, J, x, top, p1, d1, s1);
         if (it == 0) valid = outside;
         if (!done) {
             if (p1 == 0.0) {
