@@ -446,13 +446,20 @@ __device__ __noinline__ double tri_twisted_vec(const Team& T, const double* al, 
     }
     __syncthreads();
     const int r = *sh_r;
+    // the quotients of the two eigenvector recurrences do not depend on the recurrence:
+    // all threads form them first (one division each), the chains are then multiplications
+    for (int i = T.tid; i < J; i += T.nthr) {
+        if (i == r) continue;
+        double piv = (i < r) ? dp[i] : dm[i];
+        if (fabs(piv) < tiny) piv = (piv < 0.0 ? -tiny : tiny);
+        s[i] = ((i < r) ? be[i] : be[i - 1]) / piv;
+    }
+    __syncthreads();
     if (T.tid == 0) {
         s[r] = 1.0;
         double prev = 1.0;
         for (int i = r - 1; i >= 0; --i) {
-            double piv = dp[i];
-            if (fabs(piv) < tiny) piv = (piv < 0.0 ? -tiny : tiny);
-            double v = -(be[i] / piv) * prev;
+            double v = -s[i] * prev;
             if (fabs(v) > 1e200) v = copysign(1e200, v);
             s[i] = v;
             prev = v;
@@ -460,9 +467,7 @@ __device__ __noinline__ double tri_twisted_vec(const Team& T, const double* al, 
     } else if (T.tid == 32 || (T.nthr <= 32 && T.tid == 1)) {
         double prev = 1.0;
         for (int i = r + 1; i < J; ++i) {
-            double piv = dm[i];
-            if (fabs(piv) < tiny) piv = (piv < 0.0 ? -tiny : tiny);
-            double v = -(be[i - 1] / piv) * prev;
+            double v = -s[i] * prev;
             if (fabs(v) > 1e200) v = copysign(1e200, v);
             s[i] = v;
             prev = v;

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         const double* al = smem_dyn + oVec + V_AL * vl;
         const double* be = smem_dyn + oVec + V_BE * vl;
         const double* sv = smem_dyn + oVec + V_SV * vl;
-        if (tid == 0) {
+        if (tid == NT - 1) {  // a thread without z = Q s work when mdp < NT
             const double th2 = theta_max - 1e-12 * fabs(theta_max);
             const int c = sturm_below(al, be, J, th2);
             sh_deg = (md >= 2 && J >= 2 && c <= J - 2) ? 1 : 0;
