@@ -843,24 +843,34 @@ __device__ double tri_back_lastcomp_sm(const int oA, const int oB, const int oRB
     double s0 = (th - sm[oA + J - 1]) * sm[oRB + J - 2];
     double nn = 1.0 + s0 * s0;
     // i = J-2 .. 1 in groups of 4: the coefficients of a group (loads, products)
-    // are formed before its chain, so the chain itself is one FMA per step
-    for (int i0 = J - 2; i0 >= 1; i0 -= 4) {
+    // are formed before its chain, so the chain itself is one FMA per step; full
+    // groups run without per-step predicates
+    auto step = [&](const double c, const double d) {
+        const double sm_ = fma(c, s0, d * s1);
+        s1 = s0;
+        s0 = sm_;
+        nn = fma(sm_, sm_, nn);
+    };
+    int i0 = J - 2;
+    for (; i0 - 3 >= 1; i0 -= 4) {
         double c[4], d[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int ii = max(i0 - u, 1);
+            const int ii = i0 - u;
             const double rb = sm[oRB + ii - 1];
             c[u] = (th - sm[oA + ii]) * rb;
             d[u] = -sm[oB + ii] * rb;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (i0 - u >= 1) {
-                const double sm_ = fma(c[u], s0, d[u] * s1);
-                s1 = s0;
-                s0 = sm_;
-                nn = fma(sm_, sm_, nn);
-            }
+        for (int u = 0; u < 4; ++u) step(c[u], d[u]);
+        if (nn > 0x1p+600) {
+            s0 *= 0x1p-300; s1 *= 0x1p-300; sJ *= 0x1p-300; nn *= 0x1p-600;
+        }
+    }
+    if (i0 >= 1) {  // the last, partial group (1..3 steps)
+        for (int ii = i0; ii >= 1; --ii) {
+            const double rb = sm[oRB + ii - 1];
+            step((th - sm[oA + ii]) * rb, -sm[oB + ii] * rb);
         }
         if (nn > 0x1p+600) {
             s0 *= 0x1p-300; s1 *= 0x1p-300; sJ *= 0x1p-300; nn *= 0x1p-600;
