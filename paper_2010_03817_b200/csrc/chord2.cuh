@@ -1101,6 +1101,18 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
 
+#ifndef SW_PRO
+// partial reorthogonalisation: correct (82% of the iterations plain at m = 100, parity green) but
+// measured 0.7% slower: a plain iteration's two barrier stages cost about what the three of the
+// full Gram-Schmidt iteration do (the loop is bound by per-stage latency, not by the O(j) work)
+#define SW_PRO 0
+#endif
+#ifndef SW_RSQRT_BETA
+#define SW_RSQRT_BETA 1
+#endif
+#ifndef SW_PRO_TAU
+#define SW_PRO_TAU 1e-10  // reorthogonalise once an omega estimate exceeds this (sqrt(eps) ~ 1.5e-8)
+#endif
 #ifndef SW_ASYNC_CHECK
 // measured 3% slower at m = 100: a check takes ~33k cycles next to the iterating warps, so
 // convergence is seen ~8 iterations late (56 run for 48 used), which costs more than the
@@ -1182,12 +1194,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     // last warp runs the convergence checks while the others iterate (named barrier 1)
     constexpr bool ASYNC = SW_ASYNC_CHECK && (NT - 32 >= 32 * KC);
     constexpr int NWC = ASYNC ? NW - 1 : NW;  // compute warps
+    // partial reorthogonalisation (Simon's omega recurrence) for m > 64: most iterations are the
+    // plain three-term recurrence (2 barrier stages instead of 3, no O(j) dots / updates)
+    constexpr bool PRO = SW_PRO && (KC >= 13) && !ASYNC;
     const int oAl = oVec + V_AL * vl, oBe = oVec + V_BE * vl, oRbe = oVec + V_RBE * vl, oHb = oVec + V_HB * vl;
     const int oB2 = oVec + V_B2 * vl;
     const int oWu = oVec + V_LZ * vl;  // wu0, wu1 (ping-pong), wp: 3 x (mdp + 8)
     const int oWp = oWu + 2 * (mdp + 8);
     const int oRB = oRed + 16;         // per-warp partial norms
     const int oShd = oRed + 32;        // check results (4) and thetas (2)
+    // PRO scratch in vector slots the callers leave free during the Lanczos run: omega rows
+    // (ring of 3) and the per-warp partials of alpha, |y'|^2 and max |omega|
+    const int oPart = oVec + V_UU * vl;
+    auto orow = [&](int i) { const int q = i % 3; return oVec + (q == 0 ? V_WV : q == 1 ? V_WV + 1 : V_PW) * vl; };
+    const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
     auto csync = [&]() {
         if (ASYNC) asm volatile("bar.sync 1, %0;\n" ::"n"(NT - 32) : "memory");
         else __syncthreads();
@@ -1238,12 +1258,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         sm[oShd + CK_STOPJ] = 0.0;
         sm[oShd + CK_EXH] = 0.0;
         sm[oShd + CK_DEC] = 0.0;
+        if (PRO) {
+            sm[orow(0)] = 1.0;  // omega_{0,0}
+            sm[oPart + 40] = 0.0;
+            sm[oPart + 41] = 0.0;
+        }
     }
     __syncthreads();  // also: every thread has its M row in registers (QT may overwrite M)
     double nn0 = 0.0;
     nn0 = tree_sum<NW>(sm + oRB);
     double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
     double bjm1 = 0.0;
+    double qprev = 0.0;      // q_{j-1}[r] (PRO)
+    int reorth_left = 0;     // PRO: further iterations to reorthogonalise fully
+    bool was_full = true;    // PRO: the previous w was fully orthogonalised (omega row reset)
     // first check: 2 before the chain's previous iteration count (consecutive calls
     // of a chain need similar J), else at 40% of md; later checks from the observed rate
     // (a per-chain hint from the previous call was measured to RAISE J: consecutive calls of a
@@ -1289,8 +1317,39 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         y += __shfl_xor_sync(0xffffffffu, y, 1);
         y += __shfl_xor_sync(0xffffffffu, y, 2);
         const double wpr = rowok ? y * sj : 0.0;
+        const double qj = rowok ? wr * sj : 0.0;  // q_j[r] (all 4 lanes of the row)
+        double ypr = 0.0;                          // PRO: y' = M q_j - beta_{j-1} q_{j-1}
+        if (PRO) {
+            ypr = rowok ? wpr - bjm1 * qprev : 0.0;
+            double ap = (g == 0) ? qj * ypr : 0.0;
+            ap = owner_sum(ap);
+            if (lane == 0) sm[oPart + warp] = ap;
+            if (tid == 0) sm[oPart + 40 + ((j + 1) & 1)] = 0.0;  // next iteration's trigger flag
+            // omega_{j,k} = q_j . q_k estimates (Simon 1984) by the last 3 warps (no M rows for
+            // m <= 104): recurrence from the rows j-1, j-2, or the rounding level after a full
+            // orthogonalisation of w_{j-1}; any estimate above tau raises this iteration's flag
+            if (j >= 1) {
+                const int t = tid - (NT - 96);
+                for (int k = (t >= 0) ? t : md; k <= j; k += 96) {
+                    double v;
+                    if (k == j) v = 1.0;
+                    else if (k == j - 1) v = eps1 * tnorm * sj;
+                    else if (was_full) v = eps1;
+                    else {
+                        const int oP = orow(j - 1), oQq = orow(j - 2);
+                        const double bk = sm[oBe + k], bkm = (k > 0) ? sm[oBe + k - 1] : 0.0;
+                        double num = bk * sm[oP + k + 1] + (sm[oAl + k] - sm[oAl + j - 1]) * sm[oP + k] +
+                                     ((k > 0) ? bkm * sm[oP + k - 1] : 0.0) - sm[oBe + j - 2] * sm[oQq + k];
+                        num += copysign(eps1 * (bk + bjm1), num);
+                        v = num * sj;  // / beta_{j-1}
+                        if (fabs(v) > SW_PRO_TAU) sm[oPart + 40 + (j & 1)] = 1.0;
+                    }
+                    sm[orow(j) + k] = v;
+                }
+            }
+        }
         if (owner) {
-            const double q = wr * sj;  // q_j (wr = u_j[r])
+            const double q = qj;  // q_j (wr = u_j[r])
             sm[oQ + j * ld + r] = q;
             if (USEQT) {
                 sm[oQT + r * ld + j] = q;
@@ -1309,9 +1368,39 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             }
         }
         // ---- (2)+(3) classical Gram-Schmidt of w' against q_0..q_j; a second pass
-        // (DGKS) only on severe cancellation (|w| < 1e-6 |w'|, e.g. an invariant subspace)
+        // (DGKS) only on severe cancellation (|w| < 1e-6 |w'|, e.g. an invariant subspace).
+        // PRO (j >= 1): the three-term recurrence w = y' - alpha q_j; once an omega estimate of
+        // q_j exceeds tau, w_j and w_{j+1} also get one Gram-Schmidt pass against all q (after the
+        // recurrence removed the large local components, so the pass leaves w orthogonal to
+        // working precision and the omega row restarts at the rounding level).  q_j itself, already
+        // multiplied, stays semi-orthogonal (tau << sqrt(eps)).
         double wcur = wpr, alpha = 0.0, nnb = 0.0, nn = 0.0;
-        for (int pass = 0; pass < 2; ++pass) {
+        int pass0 = 0;
+        bool full = true;
+        if (PRO && j >= 1) {
+            bool reorth;
+            if (reorth_left > 0) { reorth = true; --reorth_left; }
+            else if (sm[oPart + 40 + (j & 1)] != 0.0) { reorth = true; reorth_left = 1; }
+            else reorth = false;
+            alpha = tree_sum<NW>(sm + oPart);
+            wcur = rowok ? ypr - alpha * qj : 0.0;
+            double pb = (g == 0) ? wcur * wcur : 0.0;
+            pb = owner_sum(pb);
+            if (lane == 0) sm[oRB + warp] = pb;
+            if (owner) sm[oUn + r] = wcur;
+            csync();
+            nn = tree_sum<NWC>(sm + oRB);
+            nnb = alpha * alpha + nn;  // |y'|^2 (y' = alpha q_j + w)
+            if (!reorth && nn >= 1e-12 * nnb) {
+                pass0 = 2;  // done: no Gram-Schmidt pass
+                full = false;
+            } else {
+                if (owner) sm[oWp + r] = wcur;  // one full pass on w (reorthogonalisation / cancellation)
+                csync();
+                pass0 = 1;
+            }
+        }
+        for (int pass = pass0; pass < 2; ++pass) {
             // (2) h_i = q_i . w for i <= j, and |w|^2 (slot j + 1): 8 lanes per dot, 4 dots per warp
             for (int ib = 4 * warp; ib <= j + 1; ib += 4 * NWC) {
                 const int i = ib + du;
@@ -1379,8 +1468,20 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             csync();
         }
         wr = wcur;
+        if (PRO) {
+            qprev = qj;
+            was_full = full;
+            if (prof && full && tid == 0) atomicAdd(&prof[29], 1ull);
+        }
+#if SW_RSQRT_BETA
+        // 1/beta by the hardware reciprocal square root (+ Newton, ~1 ulp) and beta = nn / beta:
+        // no correctly-rounded sqrt and division sequences on the iteration's critical path
+        const double rsb = (nn > 0.0) ? rsqrt(nn) : SW_INF;
+        const double beta = (nn > 0.0) ? nn * rsb : 0.0;
+#else
         const double beta = sqrt(nn);
         const double rsb = 1.0 / beta;
+#endif
         if (tid == 0) {
             sm[oAl + j] = alpha;
             sm[oBe + j] = beta;

@@ -976,6 +976,9 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
                     (double)ph[25] / fmax(1.0, (double)ph[24]), (double)ph[22] / fmax(1.0, (double)ph[20]),
                     (double)ph[26] / fmax(1.0, (double)ph[24]), (double)ph[23] / fmax(1.0, (double)(ph[20] + ph[24])),
                     (double)ph[27] / fmax(1.0, (double)(ph[20] + ph[24])));
+        if (ph[29] > 0)
+            fprintf(stderr, "[specwalk prof] PRO: fully orthogonalised iterations/call=%.2f of %.2f\n",
+                    (double)ph[29] / hs[0], (double)ph[10] / hs[0]);
         if (ph[18] > 0)
             fprintf(stderr, "[specwalk prof] async lanczos: iterations run/call=%.2f (J used %.2f) checks/call=%.2f "
                             "check cycles=%.0f\n", (double)ph[18] / hs[0], (double)ph[10] / hs[0],
