@@ -387,6 +387,49 @@ def run_ours(args):
                "note": "one quadratic-pencil chord per chain per round (Weyl stepping, ~5 Cholesky + Lanczos "
                        "iterations per call); device events on the library stream, max over ranks"}
 
+    # ---- north_star's second size: configs[4] (n = m = 200, 65536 billiard chains, seed 4), calls/s
+    # over scheduler rounds on the global-scratch K2 variant, with the K2 roofline fraction
+    m200 = None
+    if args.m200_rounds > 0:
+        inst4 = specgen.config_instance(4)
+        S4 = sw.Spectrahedron.from_instance(inst4, device=dev)
+        stream4 = torch.cuda.ExternalStream(S4.stream(), device=dev)
+        S4.walk_begin(local_chains, 100, 2.0 * math.sqrt(200), 2000, SEED, chain_begin=begin)
+        S4.walk_rounds(2)
+        g0 = S4.walk_stats_now()
+        S4.kernel_timing(True)
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream4)
+        S4.walk_rounds(args.m200_rounds)
+        f1.record(stream4)
+        f1.synchronize()
+        barrier()
+        fms = f0.elapsed_time(f1)
+        g1 = S4.walk_stats_now()
+        kt4 = S4.kernel_times()
+        S4.walk_end()
+        del S4
+        ft = torch.tensor([fms, float(g1["calls"] - g0["calls"])], dtype=torch.float64, device=coll_dev)
+        if dist is not None:
+            fmax_ = ft.clone()
+            dist.all_reduce(fmax_[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(ft[1:], op=dist.ReduceOp.SUM)
+            fms, fcalls = float(fmax_[0]), float(ft[1])
+        else:
+            fcalls = float(ft[1])
+        f4 = flops_per_call(200, 200, 68)
+        k2ms4 = kt4["ms"]["K2_chord"]
+        k2_ach4 = f4["k2"] * (kt4["k2_items"] / max(k2ms4 * 1e-3, 1e-12)) / 1e12
+        m200 = {"metric": "boundary-oracle calls/s (billiard walk, n=m=200, configs[4])",
+                "value": fcalls / (fms * 1e-3), "unit": "calls/s", "chains": chains, "rounds": args.m200_rounds,
+                "ms": fms, "calls": fcalls,
+                "roofline_k2": {"bound": "alu", "achieved": k2_ach4, "peak": fp64_peak_tflops(), "unit": "TFLOP/s",
+                                "frac": k2_ach4 / fp64_peak_tflops(), "flops_per_chain_call": f4["k2"],
+                                "flop_model": "SURVEY 8(d).2: m^3/3 + m^3 + 2 k m^2, k = 68 (V9)"},
+                "kernel_share": {k: v / max(sum(kt4["ms"].values()), 1e-9) for k, v in kt4["ms"].items()}}
+
     # ---- BASELINE metric, second half: volume time at n = m = 40 (configs[2], eps 0.1, 4096 chains/phase)
     vol = None
     if args.volume_seeds > 0:
@@ -455,6 +498,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "volume_n40": vol,
         "hmc_configs3": hmc,
+        "m200_configs4": m200,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -473,6 +517,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--volume-seeds", type=int, default=3)
     ap.add_argument("--hmc-rounds", type=int, default=4)
+    ap.add_argument("--m200-rounds", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
