@@ -94,6 +94,66 @@ __device__ __forceinline__ bool diag_factor_inv(double* D, int ld, double* rd8, 
     return ok;
 }
 
+// The same factor and inverse with the whole 8 x 8 block in every lane's registers (36
+// broadcast loads): the column steps need no shuffles (rsqrt -> scale -> update is the whole
+// chain), and lane c < 8 forms column c of the inverse by its own forward substitution.  Same
+// operations in the same order as diag_factor_inv (bit-identical L, 1/diag and inverse).
+__device__ __forceinline__ bool diag_factor_inv_reg(double* D, int ld, double* rd8, double* V, int lane) {
+    double a[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c <= r; ++c) a[r][c] = D[r * ld + c];
+    bool ok = true;
+    double rd[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const double d = a[c][c];
+        if (!(d > 0.0)) ok = false;
+        const double il = rsqrt(fmax(d, 1e-300));
+        a[c][c] = d * il;
+        rd[c] = il;
+#pragma unroll
+        for (int r = c + 1; r < 8; ++r) a[r][c] *= il;
+#pragma unroll
+        for (int k = c + 1; k < 8; ++k)
+#pragma unroll
+            for (int r = k; r < 8; ++r) a[r][k] = fma(-a[r][c], a[k][c], a[r][k]);
+    }
+    // column `lane` of X = L^{-1}: X[r][c] = (delta_rc - sum_{k<r} L[r][k] X[k][c]) / L[r][r]
+    const int c = lane & 7;
+    double x[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < r; ++k) acc = fma(a[r][k], x[k], acc);
+        x[r] = ((r == c ? 1.0 : 0.0) - acc) * rd[r];
+    }
+    __syncwarp();  // every lane has read D
+    if (lane < 8) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            V[r * 8 + c] = (r >= c) ? x[r] : 0.0;
+            if (r == lane) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    if (k <= r) D[r * ld + k] = a[r][k];
+                rd8[r] = rd[r];
+            }
+        }
+    }
+    return ok;
+}
+#ifndef SW_DIAG_REG
+#define SW_DIAG_REG 1
+#endif
+#if SW_DIAG_REG
+#define SW_DIAG_FACTOR diag_factor_inv_reg
+#else
+#define SW_DIAG_FACTOR diag_factor_inv
+#endif
+
 // Blocked right-looking Cholesky of the lower triangle of G (n = multiple of 8),
 // rdiag = 1 / diag(L), Lv = the inverses of the 8 x 8 diagonal blocks (row-major,
 // 64 doubles per block).  Returns false on a non-positive pivot (CTA-uniform).
@@ -105,7 +165,7 @@ __device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld,
     const int TB = n >> 3;
     const int rr = T.lane >> 2, q = T.lane & 3;
     if (T.warp == 0) {
-        const bool ok = diag_factor_inv(G, ld, rdiag, Lv, T.lane);
+        const bool ok = SW_DIAG_FACTOR(G, ld, rdiag, Lv, T.lane);
         if (T.lane == 0) *flag = ok ? 0 : 1;
     }
     __syncthreads();
@@ -133,7 +193,7 @@ __device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld,
             C[rr * ld + 2 * q] = acc[0];
             C[rr * ld + 2 * q + 1] = acc[1];
             __syncwarp();
-            const bool ok = diag_factor_inv(C, ld, rdiag + (kb + 1) * 8, Lv + (kb + 1) * 64, T.lane);
+            const bool ok = SW_DIAG_FACTOR(C, ld, rdiag + (kb + 1) * 8, Lv + (kb + 1) * 64, T.lane);
             if (T.lane == 0) *flag = ok ? 0 : 1;
         } else {
             // the rest of the trailing SYRK: G_ij -= P_i P_j^T, kb < j <= i, (i, j) != (kb+1, kb+1),
