@@ -1570,7 +1570,9 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
     double* G = base;
     double* B = base + (size_t)mp * ld;
     double* Qm = G;  // Lanczos basis reuses L's space while L is parked in P.lsave
-    double* vec = B + (size_t)mp * ld;
+    // the vector area (+ inverse diagonal blocks) in shared memory on both variants; the global
+    // variant keeps only G, B (the Lanczos basis, M) in its scratch slice
+    double* vec = SMEM ? B + (size_t)mp * ld : smem_dyn;
     double* Lsave = P.lsave + (size_t)blockIdx.x * P.lsave_stride;
     const int vl = mp + 8;
     double* uu = vec + 0 * vl;

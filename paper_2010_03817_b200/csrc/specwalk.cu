@@ -99,6 +99,7 @@ struct spec_ctx {
     int f_grid = 0, l_grid = 0, t_grid = 0;
     size_t f_smem = 0, l_smem = 0, t_smem = 0;
     size_t smem_bytes = 0;
+    size_t g_smem = 0;  // global-scratch K2 variant: vector area in shared memory
     int chord_threads = 256;
     int chord_grid_max = 0;
     int num_sms = 0;
@@ -285,7 +286,11 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     } else {
         ctx->smem_path = false;
         ctx->k2_variant = 2;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false, 16>, 512, 0));
+        // vectors + inverse diagonal blocks in shared memory, matrices in the scratch slice
+        ctx->g_smem = sizeof(double) * (vecs + 8 * (size_t)mp);
+        CK(cudaFuncSetAttribute(chord_kernel2<512, false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ctx->g_smem));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false, 16>, 512, ctx->g_smem));
         if (occ < 1) occ = 1;
         if (occ > 2) occ = 2;
         ctx->chord_grid_max = occ * ctx->num_sms;
@@ -465,7 +470,7 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
     else if (ctx->k2_variant == 3)
         chord_kernel2<512, true, 16><<<grid, 512, ctx->smem_bytes, ctx->stream>>>(P);
     else
-        chord_kernel2<512, false, 16><<<grid, 512, 0, ctx->stream>>>(P);
+        chord_kernel2<512, false, 16><<<grid, 512, ctx->g_smem, ctx->stream>>>(P);
     ctx->launches++;
 }
 
