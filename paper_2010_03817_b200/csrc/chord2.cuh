@@ -22,6 +22,18 @@ constexpr int NVEC2 = 20;
 #ifndef SW_GLOBAL_LL
 #define SW_GLOBAL_LL 1  // global-scratch variant (m > 112): left-looking congruence
 #endif
+#ifndef SW_PRO
+// partial reorthogonalisation: correct (82% of the iterations plain at m = 100, parity green) but
+// measured 0.7% slower: a plain iteration's two barrier stages cost about what the three of the
+// full Gram-Schmidt iteration do (the loop is bound by per-stage latency, not by the O(j) work)
+#define SW_PRO 0
+#endif
+#ifndef SW_PRO_RUN
+#define SW_PRO_RUN 1
+#endif
+#ifndef SW_PRO_TAU
+#define SW_PRO_TAU 1e-10  // reorthogonalise once an omega estimate exceeds this (sqrt(eps) ~ 1.5e-8)
+#endif
 #ifndef SW_LANCZOS_TOL
 // Lanczos convergence: residual of the top Ritz pair <= SW_LANCZOS_TOL |T_J|.  The Ritz value
 // error is ~res^2 / gap; the Ritz vector (the kernel vector y, the normal) error ~res / gap.
@@ -502,7 +514,8 @@ __device__ __noinline__ double tri_twisted_vec(const Team& T, const double* al, 
 __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, int mdp, int ld, bool need_top,
                            bool need_bot, double* wv, double* hb, double* al, double* be, double* sv, double* sv2,
                            double* dp, double* dm, double* red, int* sh_r, double* shd,
-                           unsigned long long* prof, double* theta_top, double* theta_bot) {
+                           unsigned long long* prof, double* theta_top, double* theta_bot,
+                           double* om = nullptr, double* part = nullptr) {
     const int lrow = T.tid >> 2, lg = T.tid & 3;
     const int NT = T.nthr;
     double* red2 = red + 16;  // per-warp partial norms (NT <= 512)
@@ -528,11 +541,50 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
     double tnorm = 0.0;
     double th_prev = -SW_INF, res_prev = SW_INF;
     int J = 0;
+    // partial reorthogonalisation (as lanczos_reg's SW_PRO, here where Q and M live in global
+    // scratch and the Gram-Schmidt dots / updates read O(j m) from L2 every iteration): the
+    // three-term step w = y' - alpha q_j always, one Gram-Schmidt pass on w only when Simon's
+    // omega estimates (3 rows in `om`) cross tau, for two consecutive vectors.
+    const bool pro = SW_PRO_RUN && (om != nullptr);
+    const int ovl = mdp + 8;
+    const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
+    double bjm1 = 0.0, invb_prev = 0.0;
+    int reorth_left = 0;
+    bool was_full = true;
+    if (pro && T.tid == 0) {
+        om[0] = 1.0;
+        part[40] = 0.0;
+        part[41] = 0.0;
+    }
+    __syncthreads();
     for (int j = 0; j < md; ++j) {
         double* qj = Q + (size_t)j * ld;
         long long tl0 = clock64();
         // ---- (A) q_j = w / beta stored; w' = M q_j: 4 threads per row, double2 columns
         for (int e = T.tid; e < mdp; e += T.nthr) qj[e] = win[e] * invb;
+        double apl = 0.0;  // PRO: this thread's part of alpha = q_j . y'
+        if (pro) {
+            // omega_{j,k} estimates for k = tid <= j (rows j-1, j-2 of the ring); flag > tau
+            if (T.tid == 0) part[40 + ((j + 1) & 1)] = 0.0;
+            const int k = T.tid;
+            if (j >= 1 && k <= j) {
+                double v;
+                if (k == j) v = 1.0;
+                else if (k == j - 1) v = eps1 * tnorm * invb;
+                else if (was_full) v = eps1;
+                else {
+                    const double* P1 = om + ((j - 1) % 3) * ovl;
+                    const double* P2 = om + ((j - 2) % 3) * ovl;
+                    const double bk = be[k], bkm = (k > 0) ? be[k - 1] : 0.0;
+                    double num = bk * P1[k + 1] + (al[k] - al[j - 1]) * P1[k] + ((k > 0) ? bkm * P1[k - 1] : 0.0) -
+                                 be[j - 2] * P2[k];
+                    num += copysign(eps1 * (bk + bjm1), num);
+                    v = num * invb;
+                    if (fabs(v) > SW_PRO_TAU) part[40 + (j & 1)] = 1.0;
+                }
+                om[(j % 3) * ovl + k] = v;
+            }
+        }
         if (mdp <= 128) {
             // fast path: 16 double2 loads per thread issued up front, 4 accumulators
             for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
@@ -556,7 +608,14 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                 double a0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
                 a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
                 a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-                if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
+                if (lg == 0 && rw < mdp) {
+                    double yv = a0 * invb;
+                    if (pro) {  // y' = M q_j - beta_{j-1} q_{j-1}; alpha partial q_j . y'
+                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
+                        apl += (win[rw] * invb) * yv;
+                    }
+                    wout[rw] = yv;
+                }
             }
         } else {
             for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
@@ -574,15 +633,54 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
                 a0 += a1;
                 a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
                 a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-                if (lg == 0 && rw < mdp) wout[rw] = a0 * invb;
+                if (lg == 0 && rw < mdp) {
+                    double yv = a0 * invb;
+                    if (pro) {
+                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
+                        apl += (win[rw] * invb) * yv;
+                    }
+                    wout[rw] = yv;
+                }
             }
+        }
+        if (pro) {  // alpha partials: the owner lanes (lg == 0)
+            apl += __shfl_xor_sync(0xffffffffu, apl, 16);
+            apl += __shfl_xor_sync(0xffffffffu, apl, 8);
+            apl += __shfl_xor_sync(0xffffffffu, apl, 4);
+            if (T.lane == 0) part[T.warp] = apl;
         }
         __syncthreads();
         long long tl1 = clock64();
         long long tl2 = tl1, tl3 = tl1;
         // ---- (B..E) classical Gram-Schmidt against q_0..q_j
         double alpha = 0.0, nn = 0.0, nn_before = 0.0;
-        for (int pass = 0; pass < 2; ++pass) {
+        int pass0 = 0;
+        bool full = true;
+        if (pro) {
+            bool reorth;
+            if (reorth_left > 0) { reorth = true; --reorth_left; }
+            else if (part[40 + (j & 1)] != 0.0) { reorth = true; reorth_left = 1; }
+            else reorth = false;
+            for (int w = 0; w < T.nwarps; ++w) alpha += part[w];
+            double nloc = 0.0;
+            for (int e = T.tid; e < mdp; e += T.nthr) {
+                const double wn = (e < md) ? wout[e] - alpha * (win[e] * invb) : 0.0;  // q_j from shared memory
+                wout[e] = wn;
+                nloc += wn * wn;
+            }
+            nloc = warp_sum(nloc);
+            if (T.lane == 0) red2[T.warp] = nloc;
+            __syncthreads();
+            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
+            nn_before = alpha * alpha + nn;  // |y'|^2
+            if (!reorth && nn >= 1e-12 * nn_before) {
+                pass0 = 2;
+                full = false;
+            } else {
+                pass0 = 1;  // one Gram-Schmidt pass on w
+            }
+        }
+        for (int pass = pass0; pass < 2; ++pass) {
             const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w'.w'
             if (mdp <= 128) {
                 double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
@@ -678,6 +776,11 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
         if (T.tid == 0) {
             al[j] = alpha;
             be[j] = beta;
+        }
+        if (pro) {
+            bjm1 = beta;
+            was_full = full;
+            invb_prev = invb;  // 1 / beta_{j-1}, the scale of u_j held in win (q_j = u_j * invb)
         }
         tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
         J = j + 1;
@@ -1101,17 +1204,8 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
 
-#ifndef SW_PRO
-// partial reorthogonalisation: correct (82% of the iterations plain at m = 100, parity green) but
-// measured 0.7% slower: a plain iteration's two barrier stages cost about what the three of the
-// full Gram-Schmidt iteration do (the loop is bound by per-stage latency, not by the O(j) work)
-#define SW_PRO 0
-#endif
 #ifndef SW_RSQRT_BETA
 #define SW_RSQRT_BETA 1
-#endif
-#ifndef SW_PRO_TAU
-#define SW_PRO_TAU 1e-10  // reorthogonalise once an omega estimate exceeds this (sqrt(eps) ~ 1.5e-8)
 #endif
 #ifndef SW_ASYNC_CHECK
 // measured 3% slower at m = 100: a check takes ~33k cycles next to the iterating warps, so
@@ -1722,7 +1816,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                 }
                 else
                     J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
-                                    &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min);
+                                    &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min, vec + 17 * vl, vec);
                 lanczos_J = J;
                 if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);
                 PROF_MARK(4);
