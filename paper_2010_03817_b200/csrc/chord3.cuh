@@ -417,7 +417,9 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
             const int mdp = (md + 7) & ~7;
             cp_async_wait_all();
             __syncthreads();
+            PROF_MARK(5);
             back_solve_lt(T, G, ld, mdp, zz, yy, rdiag);  // y = L^{-T} z
+            PROF_MARK(6);
             if (T.warp == 0) {
                 if (defl) {  // y = H [ -b^T yh / a ; yh ]
                     double s = 0.0;
