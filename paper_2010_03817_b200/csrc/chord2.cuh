@@ -248,107 +248,6 @@ __device__ void trsm_blocked(const Team& T, const double* G, double* B, int n, i
     }
 }
 
-// extreme eigenvalue of the tridiagonal (al, be) of size J by CTA multisection
-// inside [lo, hi]; top = largest, else smallest.
-__device__ double tri_multisect(const Team& T, const double* al, const double* be, int J, bool top, double lo,
-                                double hi, double* red) {
-    const double eps = 2.220446049250313e-16;
-    for (int it = 0; it < 24; ++it) {
-        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
-        double sig = lo + (hi - lo) * ((double)(T.tid + 1) / (double)(T.nthr + 1));
-        int c = sturm_below(al, be, J, sig);
-        double ch, cl;
-        if (top) {
-            ch = (c == J) ? sig : SW_INF;
-            cl = (c < J) ? sig : -SW_INF;
-        } else {
-            ch = (c >= 1) ? sig : SW_INF;
-            cl = (c == 0) ? sig : -SW_INF;
-        }
-        double nh = block_min(T, ch, red);
-        double nl = block_max(T, cl, red);
-        hi = fmin(hi, nh);
-        lo = fmax(lo, nl);
-    }
-    return 0.5 * (lo + hi);
-}
-
-// four interleaved Sturm counts (independent dependency chains for ILP)
-__device__ __forceinline__ void sturm_below4(const double* d, const double* e, int md, const double (&sg)[4],
-                                             int (&cnt)[4]) {
-    double pp[4], p[4];
-    bool neg[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        pp[u] = 1.0;
-        p[u] = d[0] - sg[u];
-        cnt[u] = (p[u] <= 0.0) ? 1 : 0;
-        neg[u] = (p[u] <= 0.0);
-        if (p[u] == 0.0) p[u] = -1e-300;
-    }
-    for (int i = 1; i < md; ++i) {
-        const double e2 = e[i - 1] * e[i - 1], di = d[i];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            double pn = (di - sg[u]) * p[u] - e2 * pp[u];
-            bool nneg;
-            if (pn == 0.0) {
-                nneg = !neg[u];
-                pn = neg[u] ? 1e-300 : -1e-300;
-            } else {
-                nneg = pn < 0.0;
-            }
-            cnt[u] += (nneg != neg[u]) ? 1 : 0;
-            neg[u] = nneg;
-            pp[u] = p[u];
-            p[u] = pn;
-            double ap = fabs(pn);
-            if (ap > 0x1p+500) {
-                p[u] *= 0x1p-500;
-                pp[u] *= 0x1p-500;
-            } else if (ap < 0x1p-500 && fabs(pp[u]) < 0x1p-500) {
-                p[u] *= 0x1p+500;
-                pp[u] *= 0x1p+500;
-            }
-        }
-    }
-}
-
-// CTA multisection with 4 Sturm counts per thread (4*NT points per round)
-__device__ double tri_multisect4(const Team& T, const double* al, const double* be, int J, bool top, double lo,
-                                 double hi, double* red) {
-    const double eps = 2.220446049250313e-16;
-    const double inv = 1.0 / (double)(4 * T.nthr + 1);
-    for (int it = 0; it < 16; ++it) {
-        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
-        double sg[4];
-        int c[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) sg[u] = lo + (hi - lo) * ((double)(4 * T.tid + u + 1) * inv);
-        sturm_below4(al, be, J, sg, c);
-        double ch = SW_INF, cl = -SW_INF;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            bool above = top ? (c[u] == J) : (c[u] >= 1);
-            if (above) ch = fmin(ch, sg[u]);
-            else cl = fmax(cl, sg[u]);
-        }
-        ch = warp_min(ch);
-        cl = warp_max(cl);
-        if (T.lane == 0) {
-            red[T.warp] = ch;
-            red[32 + T.warp] = cl;
-        }
-        __syncthreads();
-        for (int w = 0; w < T.nwarps; ++w) {
-            hi = fmin(hi, red[w]);
-            lo = fmax(lo, red[32 + w]);
-        }
-        __syncthreads();
-    }
-    return 0.5 * (lo + hi);
-}
-
 // Extreme eigenvalue of the symmetric tridiagonal (al, be) of size J by
 // Laguerre's method on p(x) = det(x I - T) (all roots real): started above the
 // spectrum (top) it decreases monotonically to lambda_max, started below it
@@ -388,28 +287,6 @@ __device__ double tri_laguerre(const double* al, const double* be, int J, double
         if (fabs(step) <= 2.0 * eps * fabs(x)) break;
     }
     return x;
-}
-
-// warp-level multisection (32 Sturm counts per round, no block barriers)
-__device__ double tri_multisect_warp(int lane, const double* al, const double* be, int J, bool top, double lo,
-                                     double hi) {
-    const double eps = 2.220446049250313e-16;
-    for (int it = 0; it < 64; ++it) {
-        if (!(hi - lo > 2.0 * eps * fmax(fabs(lo), fabs(hi))) || !(hi > lo)) break;
-        double sig = lo + (hi - lo) * ((double)(lane + 1) * (1.0 / 33.0));
-        int c = sturm_below(al, be, J, sig);
-        double ch, cl;
-        if (top) {
-            ch = (c == J) ? sig : SW_INF;
-            cl = (c < J) ? sig : -SW_INF;
-        } else {
-            ch = (c >= 1) ? sig : SW_INF;
-            cl = (c == 0) ? sig : -SW_INF;
-        }
-        hi = fmin(hi, warp_min(ch));
-        lo = fmax(lo, warp_max(cl));
-    }
-    return 0.5 * (lo + hi);
 }
 
 // Eigenvector s of the tridiagonal T_J (al, be) for the eigenvalue theta by a
@@ -856,85 +733,6 @@ __device__ double tri_back_lastcomp(const double* al, const double* be, const do
         }
     }
     return sJ / sqrt(nn);
-}
-
-// Lanczos with full (classical Gram-Schmidt) reorthogonalisation on the
-// symmetric md x md matrix M, M REGISTER-resident: thread (r = tid/4, g = tid%4)
-// holds row r at the column pairs 2g + 8k, k < NT/32 (so md <= NT/4).
-// Iteration j (three barriers):
-//   (1) w' = M q_j: 4 lanes per row, q_j read from the unnormalised copy u_j
-//       (ping-pong buffer wu) times 1/beta_{j-1}; the row owner stores the
-//       normalised q_j into the basis Q and w' into wp;
-//   (2) h_i = q_i . w' for i <= j, four dots per warp in flight; alpha_j = h_j;
-//   (3) w = w' - Q h (4 lanes per row split i), beta_j = |w|, u_{j+1} = w.
-// Plain Lanczos (no reorthogonalisation) was measured to lose 1e-6..1e-3 of
-// theta_max near the boundary (huge |theta_min| converging first); one CGS pass
-// keeps theta_max within ~20 eps |M| of LAPACK on BASELINE instances.
-// Convergence: residual be[J-1] |s_J| of the requested extreme Ritz pair(s)
-// <= 1e-14 |T_J|; Ritz values by Laguerre from the Gershgorin bound, |s_J| by
-// the backward recurrence; the first check at J = 0.4 md, the next ones
-// predicted from the observed linear rate (at most 8 iterations apart).
-// On return sv holds the top Ritz vector of T_J (z = Q sv).  wv: 3 (mdp + 8).
-// Extreme eigenvalue of the tridiagonal T_J (diagonal sm[oA..], squared
-// off-diagonal sm[oB2..]) by Laguerre's method on p(x) = det(x I - T) (all roots
-// real, cubic convergence, monotone from outside the spectrum).  Started at x
-// (a warm bound); if the Sturm signs of the first sweep show that x is not
-// outside the spectrum, restarted at xsafe (Gershgorin).  Stops at 2 eps |x| or
-// when the step changes direction (rounding-noise level).  One thread; the
-// recurrence is rescaled by powers of two every 4 steps.
-__device__ double tri_laguerre_sm(const int oA, const int oB2, const int J, double x, const double xsafe,
-                                  const bool top) {
-    extern __shared__ __align__(16) double sm[];
-    const double eps = 2.220446049250313e-16;
-    if (J == 1) return sm[oA];
-    const double n = (double)J;
-    bool first = true, has_step = false;
-    double last_step = 0.0;
-    for (int it = 0; it < 40; ++it) {
-        double p0 = 1.0, d0 = 0.0, s0 = 0.0;
-        double p1 = x - sm[oA], d1 = 1.0, s1 = 0.0;
-        // outside the spectrum: all p_k > 0 (above) / sign (-1)^k (below)
-        bool outside = top ? (p1 > 0.0) : (p1 < 0.0);
-        int i = 1;
-        for (; i < J; ++i) {
-            const double t = x - sm[oA + i], b2 = sm[oB2 + i - 1];
-            const double p2 = t * p1 - b2 * p0;
-            const double d2 = p1 + t * d1 - b2 * d0;
-            const double s2 = 2.0 * d1 + t * s1 - b2 * s0;
-            p0 = p1; d0 = d1; s0 = s1;
-            p1 = p2; d1 = d2; s1 = s2;
-            if (first) outside = outside && (top ? (p1 > 0.0) : ((i & 1) ? (p1 > 0.0) : (p1 < 0.0)));
-            if ((i & 3) == 0) {
-                const double ap = fmax(fabs(p1), fmax(fabs(d1), fabs(s1)));
-                if (ap > 0x1p+400) {
-                    p0 *= 0x1p-400; d0 *= 0x1p-400; s0 *= 0x1p-400;
-                    p1 *= 0x1p-400; d1 *= 0x1p-400; s1 *= 0x1p-400;
-                } else if (ap < 0x1p-400) {
-                    p0 *= 0x1p+400; d0 *= 0x1p+400; s0 *= 0x1p+400;
-                    p1 *= 0x1p+400; d1 *= 0x1p+400; s1 *= 0x1p+400;
-                }
-            }
-        }
-        if (first && !outside && x != xsafe) {
-            x = xsafe;
-            first = false;
-            continue;
-        }
-        first = false;
-        if (p1 == 0.0) return x;
-        const double G = d1 / p1;
-        const double H = G * G - s1 / p1;
-        const double disc = fmax((n - 1.0) * (n * H - G * G), 0.0);
-        const double den = G + copysign(sqrt(disc), G);
-        if (den == 0.0) return x;
-        const double step = n / den;
-        if (has_step && (step > 0.0) != (last_step > 0.0)) break;  // direction flip: noise level
-        x -= step;
-        last_step = step;
-        has_step = true;
-        if (fabs(step) <= 2.0 * eps * fabs(x)) break;
-    }
-    return x;
 }
 
 // |s_J| / |s| of the eigenvector of T_J at the eigenvalue th (backward
