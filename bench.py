@@ -513,7 +513,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--chains", type=int, default=CHAINS, help="chains per GPU")
-    ap.add_argument("--e2e-chains", type=int, default=2048)
+    ap.add_argument("--e2e-chains", type=int, default=16384)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--volume-seeds", type=int, default=3)
     ap.add_argument("--hmc-rounds", type=int, default=4)
