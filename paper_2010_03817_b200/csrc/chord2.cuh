@@ -1171,7 +1171,21 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     (void)jhint;
     // first check by size: small problems need nearly the full dimension (m = 40: J ~ 0.85 md;
     // m <= 24: J = md), larger ones about half (m = 100: J ~ 0.5 md)
-    int next_check = (md <= 24) ? md : (md <= 64) ? (md * 4) / 5 : max(12, (md * 2) / 5);
+#ifndef SW_FIRST_CHECK_PCT
+#define SW_FIRST_CHECK_PCT 25  // m > 64 (measured: 25% of md +6.7% over 40% at m = 100)
+#endif
+#ifndef SW_FIRST_CHECK_PCT_SMALL
+#define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
+#endif
+#ifndef SW_FIRST_CHECK_SMALL_MD
+#define SW_FIRST_CHECK_SMALL_MD 48
+#endif
+#ifndef SW_FIRST_CHECK_PCT_MID
+#define SW_FIRST_CHECK_PCT_MID 50  // SW_FIRST_CHECK_SMALL_MD < m <= 64
+#endif
+    int next_check = (md <= 24) ? md
+                   : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
+                   : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
     int J = 0;
     double tnorm = 0.0;
     if (ASYNC && warp == NW - 1) {
