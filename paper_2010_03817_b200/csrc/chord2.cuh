@@ -34,6 +34,12 @@ constexpr int NVEC2 = 20;
 #ifndef SW_PRO_TAU
 #define SW_PRO_TAU 1e-10  // reorthogonalise once an omega estimate exceeds this (sqrt(eps) ~ 1.5e-8)
 #endif
+#ifndef SW_CHECK_STEP0
+#define SW_CHECK_STEP0 4    // iterations from the first check to the second (no rate known yet; measured)
+#endif
+#ifndef SW_CHECK_STEPMAX
+#define SW_CHECK_STEPMAX 8  // cap on the rate-predicted distance to the next check
+#endif
 #ifndef SW_LANCZOS_TOL
 // Lanczos convergence: residual of the top Ritz pair <= SW_LANCZOS_TOL |T_J|.  The Ritz value
 // error is ~res^2 / gap; the Ritz vector (the kernel vector y, the normal) error ~res / gap.
@@ -987,11 +993,11 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     const double lres = log(fmax(res, resb));
     const int jprev = (int)sm[oShd + CK_JPREV];
     const double lres_prev = sm[oShd + CK_LRES];
-    int step = (sm[oShd + CK_HINTED] != 0.0) ? 2 : 8;  // a hinted first check is close to convergence
+    int step = (sm[oShd + CK_HINTED] != 0.0) ? 2 : SW_CHECK_STEP0;  // a hinted first check is close to convergence
     if (jprev > 0 && lres < lres_prev) {
         const double rate = (lres_prev - lres) / (double)(J - jprev);
         step = (int)ceil((lres - log(tol)) / rate);
-        step = max(1, min(8, step));
+        step = max(1, min(SW_CHECK_STEPMAX, step));
     }
     sm[oShd + CK_JPREV] = (double)J;
     sm[oShd + CK_LRES] = lres;
