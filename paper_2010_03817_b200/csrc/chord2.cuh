@@ -40,6 +40,18 @@ constexpr int NVEC2 = 20;
 #ifndef SW_CHECK_STEPMAX
 #define SW_CHECK_STEPMAX 8  // cap on the rate-predicted distance to the next check
 #endif
+#ifndef SW_FIRST_CHECK_PCT
+#define SW_FIRST_CHECK_PCT 25  // m > 64 (measured: 25% of md +6.7% over 40% at m = 100)
+#endif
+#ifndef SW_FIRST_CHECK_PCT_SMALL
+#define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
+#endif
+#ifndef SW_FIRST_CHECK_SMALL_MD
+#define SW_FIRST_CHECK_SMALL_MD 48
+#endif
+#ifndef SW_FIRST_CHECK_PCT_MID
+#define SW_FIRST_CHECK_PCT_MID 50  // SW_FIRST_CHECK_SMALL_MD < m <= 64
+#endif
 #ifndef SW_LANCZOS_TOL
 // Lanczos convergence: residual of the top Ritz pair <= SW_LANCZOS_TOL |T_J|.  The Ritz value
 // error is ~res^2 / gap; the Ritz vector (the kernel vector y, the normal) error ~res / gap.
@@ -384,341 +396,6 @@ __device__ __noinline__ double tri_twisted_vec(const Team& T, const double* al, 
     return fabs(beta_last) * fabs(s[J - 1]);
 }
 
-// Lanczos (CGS with a DGKS second pass) on the symmetric md x md matrix M
-// (shared or global memory, leading dimension ld, zero padded to mdp).  Q holds
-// the orthonormal basis (rows of length ld).  Per iteration: (A) w' = M (w / beta)
-// (ping-pong buffers, q_j stored on the fly), (B) dots with q_0..q_j and |w'|^2,
-// (C) w' -= Q h with per-warp partial norms; a second pass (D, E) only when the
-// first cancelled more than half of |w'|^2.  3 barriers per iteration (5 with
-// the second pass).  Convergence: residual beta_J |s_J| <= 1e-14 |T| for the
-// requested extreme Ritz pair(s) (top: sv, bottom: sv2), checked from J =
-// 0.45 md on, every 8 steps; Ritz values by Laguerre, vectors by a twisted
-// factorisation.  wv must hold 2 (mdp + 8) doubles.  Returns J.
-__device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, int mdp, int ld, bool need_top,
-                           bool need_bot, double* wv, double* hb, double* al, double* be, double* sv, double* sv2,
-                           double* dp, double* dm, double* red, int* sh_r, double* shd,
-                           unsigned long long* prof, double* theta_top, double* theta_bot,
-                           double* om = nullptr, double* part = nullptr) {
-    const int lrow = T.tid >> 2, lg = T.tid & 3;
-    const int NT = T.nthr;
-    double* red2 = red + 16;  // per-warp partial norms (NT <= 512)
-    *theta_top = -SW_INF;
-    *theta_bot = SW_INF;
-    double* win = wv;
-    double* wout = wv + (mdp + 8);
-    // start vector: fixed pseudo-random, zero padding (w_{-1} = q_0, beta_{-1} = 1)
-    double s0 = 0.0;
-    for (int e = T.tid; e < mdp; e += T.nthr) {
-        double val = 0.0;
-        if (e < md) {
-            double f = (double)e * 0.6180339887498949;
-            val = 0.5 + (f - floor(f));
-        }
-        win[e] = val;
-        s0 += val * val;
-    }
-    s0 = block_sum(T, s0, red);
-    double invb = 1.0 / sqrt(s0);
-    const int jfirst = max(min(md, 12), (md * 9) / 20);
-    int next_check = jfirst;
-    double tnorm = 0.0;
-    double th_prev = -SW_INF, res_prev = SW_INF;
-    int J = 0;
-    // partial reorthogonalisation (as lanczos_reg's SW_PRO, here where Q and M live in global
-    // scratch and the Gram-Schmidt dots / updates read O(j m) from L2 every iteration): the
-    // three-term step w = y' - alpha q_j always, one Gram-Schmidt pass on w only when Simon's
-    // omega estimates (3 rows in `om`) cross tau, for two consecutive vectors.
-    const bool pro = SW_PRO_RUN && (om != nullptr);
-    const int ovl = mdp + 8;
-    const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
-    double bjm1 = 0.0, invb_prev = 0.0;
-    int reorth_left = 0;
-    bool was_full = true;
-    if (pro && T.tid == 0) {
-        om[0] = 1.0;
-        part[40] = 0.0;
-        part[41] = 0.0;
-    }
-    __syncthreads();
-    for (int j = 0; j < md; ++j) {
-        double* qj = Q + (size_t)j * ld;
-        long long tl0 = clock64();
-        // ---- (A) q_j = w / beta stored; w' = M q_j: 4 threads per row, double2 columns
-        for (int e = T.tid; e < mdp; e += T.nthr) qj[e] = win[e] * invb;
-        double apl = 0.0;  // PRO: this thread's part of alpha = q_j . y'
-        if (pro) {
-            // omega_{j,k} estimates for k = tid <= j (rows j-1, j-2 of the ring); flag > tau
-            if (T.tid == 0) part[40 + ((j + 1) & 1)] = 0.0;
-            const int k = T.tid;
-            if (j >= 1 && k <= j) {
-                double v;
-                if (k == j) v = 1.0;
-                else if (k == j - 1) v = eps1 * tnorm * invb;
-                else if (was_full) v = eps1;
-                else {
-                    const double* P1 = om + ((j - 1) % 3) * ovl;
-                    const double* P2 = om + ((j - 2) % 3) * ovl;
-                    const double bk = be[k], bkm = (k > 0) ? be[k - 1] : 0.0;
-                    double num = bk * P1[k + 1] + (al[k] - al[j - 1]) * P1[k] + ((k > 0) ? bkm * P1[k - 1] : 0.0) -
-                                 be[j - 2] * P2[k];
-                    num += copysign(eps1 * (bk + bjm1), num);
-                    v = num * invb;
-                    if (fabs(v) > SW_PRO_TAU) part[40 + (j & 1)] = 1.0;
-                }
-                om[(j % 3) * ovl + k] = v;
-            }
-        }
-        if (mdp <= 128) {
-            // fast path: 16 double2 loads per thread issued up front, 4 accumulators
-            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
-                const int rw = r0 + lrow;
-                double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                if (rw < mdp) {
-                    const double* Mr = M + (size_t)rw * ld;
-                    double2 mv[16], wq[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const int c = 2 * lg + 8 * k;
-                        mv[k] = (c < mdp) ? *reinterpret_cast<const double2*>(Mr + c) : make_double2(0.0, 0.0);
-                        wq[k] = (c < mdp) ? *reinterpret_cast<const double2*>(win + c) : make_double2(0.0, 0.0);
-                    }
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        acc[k & 3] += mv[k].x * wq[k].x;
-                        acc[k & 3] += mv[k].y * wq[k].y;
-                    }
-                }
-                double a0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
-                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-                if (lg == 0 && rw < mdp) {
-                    double yv = a0 * invb;
-                    if (pro) {  // y' = M q_j - beta_{j-1} q_{j-1}; alpha partial q_j . y'
-                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
-                        apl += (win[rw] * invb) * yv;
-                    }
-                    wout[rw] = yv;
-                }
-            }
-        } else {
-            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
-                const int rw = r0 + lrow;
-                double a0 = 0.0, a1 = 0.0;
-                if (rw < mdp) {
-                    const double* Mr = M + (size_t)rw * ld;
-                    for (int c = 2 * lg; c < mdp; c += 8) {
-                        double2 mv = *reinterpret_cast<const double2*>(Mr + c);
-                        double2 wq = *reinterpret_cast<const double2*>(win + c);
-                        a0 += mv.x * wq.x;
-                        a1 += mv.y * wq.y;
-                    }
-                }
-                a0 += a1;
-                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
-                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
-                if (lg == 0 && rw < mdp) {
-                    double yv = a0 * invb;
-                    if (pro) {
-                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
-                        apl += (win[rw] * invb) * yv;
-                    }
-                    wout[rw] = yv;
-                }
-            }
-        }
-        if (pro) {  // alpha partials: the owner lanes (lg == 0)
-            apl += __shfl_xor_sync(0xffffffffu, apl, 16);
-            apl += __shfl_xor_sync(0xffffffffu, apl, 8);
-            apl += __shfl_xor_sync(0xffffffffu, apl, 4);
-            if (T.lane == 0) part[T.warp] = apl;
-        }
-        __syncthreads();
-        long long tl1 = clock64();
-        long long tl2 = tl1, tl3 = tl1;
-        // ---- (B..E) classical Gram-Schmidt against q_0..q_j
-        double alpha = 0.0, nn = 0.0, nn_before = 0.0;
-        int pass0 = 0;
-        bool full = true;
-        if (pro) {
-            bool reorth;
-            if (reorth_left > 0) { reorth = true; --reorth_left; }
-            else if (part[40 + (j & 1)] != 0.0) { reorth = true; reorth_left = 1; }
-            else reorth = false;
-            for (int w = 0; w < T.nwarps; ++w) alpha += part[w];
-            double nloc = 0.0;
-            for (int e = T.tid; e < mdp; e += T.nthr) {
-                const double wn = (e < md) ? wout[e] - alpha * (win[e] * invb) : 0.0;  // q_j from shared memory
-                wout[e] = wn;
-                nloc += wn * wn;
-            }
-            nloc = warp_sum(nloc);
-            if (T.lane == 0) red2[T.warp] = nloc;
-            __syncthreads();
-            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
-            nn_before = alpha * alpha + nn;  // |y'|^2
-            if (!reorth && nn >= 1e-12 * nn_before) {
-                pass0 = 2;
-                full = false;
-            } else {
-                pass0 = 1;  // one Gram-Schmidt pass on w
-            }
-        }
-        for (int pass = pass0; pass < 2; ++pass) {
-            const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w'.w'
-            if (mdp <= 128) {
-                double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
-                const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
-                if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wout + i0);
-                if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wout + i1);
-                const int NW = T.nwarps;
-                for (int ib = T.warp; ib < nrows; ib += 4 * NW) {
-                    double sacc[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const int i = ib + u * NW;
-                        const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
-                        double sa = 0.0;
-                        if (i < nrows) {
-                            if (i0 < mdp) {
-                                double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
-                                sa += q0.x * w0.x + q0.y * w0.y;
-                            }
-                            if (i1 < mdp) {
-                                double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
-                                sa += q1.x * w1.x + q1.y * w1.y;
-                            }
-                        }
-                        sacc[u] = sa;
-                    }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], o);
-                    if (T.lane == 0) {
-#pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (ib + u * NW < nrows) hb[ib + u * NW] = sacc[u];
-                    }
-                }
-            } else {
-                for (int i = T.warp; i < nrows; i += T.nwarps) {
-                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
-                    double sacc = 0.0;
-                    for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wout[c];
-                    sacc = warp_sum(sacc);
-                    if (T.lane == 0) hb[i] = sacc;
-                }
-            }
-            __syncthreads();
-            if (pass == 0) tl2 = clock64();
-            alpha += hb[j];
-            if (pass == 0) nn_before = hb[j + 1];
-            {
-                const int g = T.tid & 3, egrp = T.nthr >> 2;
-                double nloc = 0.0;
-                for (int e0 = 0; e0 < mdp; e0 += egrp) {
-                    const int e = e0 + (T.tid >> 2);
-                    double sa = 0.0, sb = 0.0;
-                    if (e < mdp) {
-                        for (int ibase = 0; ibase <= j; ibase += 64) {
-                            double acc4[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                            for (int k = 0; k < 16; ++k) {
-                                const int i = ibase + g + 4 * k;
-                                if (i <= j) acc4[k & 3] += hb[i] * Q[(size_t)i * ld + e];
-                            }
-                            sa += (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
-                        }
-                    }
-                    sa += sb;
-                    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
-                    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
-                    if (e < mdp) {
-                        double wn = wout[e] - sa;
-                        __syncwarp();
-                        if (g == 0) wout[e] = wn;
-                        nloc += (g == 0) ? wn * wn : 0.0;
-                    }
-                }
-                // partial norms live in the g == 0 lanes: reduce over lanes 4, 8, 16 apart
-                nloc += __shfl_xor_sync(0xffffffffu, nloc, 4);
-                nloc += __shfl_xor_sync(0xffffffffu, nloc, 8);
-                nloc += __shfl_xor_sync(0xffffffffu, nloc, 16);
-                if (T.lane == 0) red2[T.warp] = nloc;
-            }
-            __syncthreads();
-            nn = 0.0;
-            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
-            if (pass == 0) tl3 = clock64();
-            if (prof && T.tid == 0 && pass == 1) atomicAdd(&prof[15], 1ull);
-            // second (DGKS) pass only on severe cancellation, as in lanczos_reg (one CGS pass
-            // keeps theta_max within ~20 eps |M|; the 0.5 criterion fired on 2/3 of the iterations)
-            if (!(nn < 1e-12 * nn_before)) break;
-        }
-        const double beta = sqrt(nn);
-        if (T.tid == 0) {
-            al[j] = alpha;
-            be[j] = beta;
-        }
-        if (pro) {
-            bjm1 = beta;
-            was_full = full;
-            invb_prev = invb;  // 1 / beta_{j-1}, the scale of u_j held in win (q_j = u_j * invb)
-        }
-        tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
-        J = j + 1;
-        const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
-        if (prof && T.tid == 0) {
-            long long tl4 = clock64();
-            atomicAdd(&prof[12], (unsigned long long)(tl1 - tl0));
-            atomicAdd(&prof[13], (unsigned long long)(tl2 - tl1));
-            atomicAdd(&prof[14], (unsigned long long)(tl3 - tl2));
-            atomicAdd(&prof[16], (unsigned long long)(tl4 - tl3));
-        }
-        // next iteration uses q_{j+1} = w' / beta
-        double* tmp = win;
-        win = wout;
-        wout = tmp;
-        invb = 1.0 / beta;
-        if (exhausted || J >= next_check) {
-            __syncthreads();  // al/be of this step visible
-            long long tc0 = clock64();
-            double glo = SW_INF, ghi = -SW_INF;
-            for (int i = T.tid; i < J; i += T.nthr) {
-                double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
-                glo = fmin(glo, al[i] - rsum);
-                ghi = fmax(ghi, al[i] + rsum);
-            }
-            ghi = block_max(T, ghi, red);
-            if (need_bot) glo = block_min(T, glo, red);
-            if (T.tid == 0) shd[0] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
-            if (need_bot && T.tid == 32) shd[1] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
-            __syncthreads();
-            const double th = shd[0];
-            double res = tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, sh_r);
-            double thmin = SW_INF, resmin = 0.0;
-            if (need_bot) {
-                thmin = shd[1];
-                resmin = tri_twisted_vec(T, al, be, J, thmin, be[J - 1], dp, dm, sv2, red, sh_r);
-            }
-            th_prev = th;
-            res_prev = res;
-            *theta_top = th;
-            *theta_bot = thmin;
-            if (prof && T.tid == 0) {
-                atomicAdd(&prof[9], (unsigned long long)(clock64() - tc0));
-                atomicAdd(&prof[11], 1ull);
-            }
-            const double tol = 1e-14 * tnorm;
-            if (exhausted || ((!need_top || res <= tol) && (!need_bot || resmin <= tol))) break;
-            next_check = min(md, J + 8);
-        }
-    }
-    (void)th_prev;
-    (void)res_prev;
-    __syncthreads();
-    return J;
-}
 
 // |s_J| / |s| for the eigenvector s of the tridiagonal T_J (al, be) at the
 // eigenvalue th, by the backward recurrence from s_J = 1 (the top Ritz vector
@@ -1004,6 +681,382 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     sm[oShd + CK_NEXT] = (double)min(md, J + step);
 }
 
+// Lanczos (CGS with a DGKS second pass) on the symmetric md x md matrix M
+// (shared or global memory, leading dimension ld, zero padded to mdp).  Q holds
+// the orthonormal basis (rows of length ld).  Per iteration: (A) w' = M (w / beta)
+// (ping-pong buffers, q_j stored on the fly), (B) dots with q_0..q_j and |w'|^2,
+// (C) w' -= Q h with per-warp partial norms; a second pass (D, E) only when the
+// first cancelled more than half of |w'|^2.  3 barriers per iteration (5 with
+// the second pass).  Convergence: residual beta_J |s_J| <= 1e-14 |T| for the
+// requested extreme Ritz pair(s) (top: sv, bottom: sv2), checked from J =
+// 0.45 md on, every 8 steps; Ritz values by Laguerre, vectors by a twisted
+// factorisation.  wv must hold 2 (mdp + 8) doubles.  Returns J.
+__device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, int mdp, int ld, bool need_top,
+                           bool need_bot, double* wv, double* hb, double* al, double* be, double* sv, double* sv2,
+                           double* dp, double* dm, double* red, int* sh_r, double* shd,
+                           unsigned long long* prof, double* theta_top, double* theta_bot,
+                           double* om = nullptr, double* part = nullptr, double* b2 = nullptr,
+                           double* rbe = nullptr, int oShd = -1) {
+    const int lrow = T.tid >> 2, lg = T.tid & 3;
+    const int NT = T.nthr;
+    double* red2 = red + 16;  // per-warp partial norms (NT <= 512)
+    *theta_top = -SW_INF;
+    *theta_bot = SW_INF;
+    double* win = wv;
+    double* wout = wv + (mdp + 8);
+    // start vector: fixed pseudo-random, zero padding (w_{-1} = q_0, beta_{-1} = 1)
+    double s0 = 0.0;
+    for (int e = T.tid; e < mdp; e += T.nthr) {
+        double val = 0.0;
+        if (e < md) {
+            double f = (double)e * 0.6180339887498949;
+            val = 0.5 + (f - floor(f));
+        }
+        win[e] = val;
+        s0 += val * val;
+    }
+    s0 = block_sum(T, s0, red);
+    double invb = 1.0 / sqrt(s0);
+    // oShd >= 0 (al, be, b2, rbe and the check state in dynamic shared memory): lanczos_reg's
+    // warp-parallel checks (Laguerre warm-started from the previous Ritz value, residual by the
+    // backward recurrence, the next check from the observed rate) and its first-check rule
+    const bool fastck = (oShd >= 0);
+    extern __shared__ __align__(16) double sm[];
+    const int jfirst = fastck ? ((md <= 24) ? md
+                                 : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
+                                 : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100
+                                              : max(12, (md * SW_FIRST_CHECK_PCT) / 100))
+                              : max(min(md, 12), (md * 9) / 20);
+    int next_check = jfirst;
+    if (fastck && T.tid == 0) {
+        sm[oShd + CK_INTOP] = -SW_INF;
+        sm[oShd + CK_INBOT] = SW_INF;
+        sm[oShd + CK_JPREV] = 0.0;
+        sm[oShd + CK_LRES] = 0.0;
+        sm[oShd + CK_TTOP] = -SW_INF;
+        sm[oShd + CK_TBOT] = SW_INF;
+        sm[oShd + CK_HINTED] = 0.0;
+    }
+    double tnorm = 0.0;
+    double th_prev = -SW_INF, res_prev = SW_INF;
+    int J = 0;
+    // partial reorthogonalisation (as lanczos_reg's SW_PRO, here where Q and M live in global
+    // scratch and the Gram-Schmidt dots / updates read O(j m) from L2 every iteration): the
+    // three-term step w = y' - alpha q_j always, one Gram-Schmidt pass on w only when Simon's
+    // omega estimates (3 rows in `om`) cross tau, for two consecutive vectors.
+    const bool pro = SW_PRO_RUN && (om != nullptr);
+    const int ovl = mdp + 8;
+    const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
+    double bjm1 = 0.0, invb_prev = 0.0;
+    int reorth_left = 0;
+    bool was_full = true;
+    if (pro && T.tid == 0) {
+        om[0] = 1.0;
+        part[40] = 0.0;
+        part[41] = 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < md; ++j) {
+        double* qj = Q + (size_t)j * ld;
+        long long tl0 = clock64();
+        // ---- (A) q_j = w / beta stored; w' = M q_j: 4 threads per row, double2 columns
+        for (int e = T.tid; e < mdp; e += T.nthr) qj[e] = win[e] * invb;
+        double apl = 0.0;  // PRO: this thread's part of alpha = q_j . y'
+        if (pro) {
+            // omega_{j,k} estimates for k = tid <= j (rows j-1, j-2 of the ring); flag > tau
+            if (T.tid == 0) part[40 + ((j + 1) & 1)] = 0.0;
+            const int k = T.tid;
+            if (j >= 1 && k <= j) {
+                double v;
+                if (k == j) v = 1.0;
+                else if (k == j - 1) v = eps1 * tnorm * invb;
+                else if (was_full) v = eps1;
+                else {
+                    const double* P1 = om + ((j - 1) % 3) * ovl;
+                    const double* P2 = om + ((j - 2) % 3) * ovl;
+                    const double bk = be[k], bkm = (k > 0) ? be[k - 1] : 0.0;
+                    double num = bk * P1[k + 1] + (al[k] - al[j - 1]) * P1[k] + ((k > 0) ? bkm * P1[k - 1] : 0.0) -
+                                 be[j - 2] * P2[k];
+                    num += copysign(eps1 * (bk + bjm1), num);
+                    v = num * invb;
+                    if (fabs(v) > SW_PRO_TAU) part[40 + (j & 1)] = 1.0;
+                }
+                om[(j % 3) * ovl + k] = v;
+            }
+        }
+        if (mdp <= 128) {
+            // fast path: 16 double2 loads per thread issued up front, 4 accumulators
+            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+                const int rw = r0 + lrow;
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                if (rw < mdp) {
+                    const double* Mr = M + (size_t)rw * ld;
+                    double2 mv[16], wq[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const int c = 2 * lg + 8 * k;
+                        mv[k] = (c < mdp) ? *reinterpret_cast<const double2*>(Mr + c) : make_double2(0.0, 0.0);
+                        wq[k] = (c < mdp) ? *reinterpret_cast<const double2*>(win + c) : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        acc[k & 3] += mv[k].x * wq[k].x;
+                        acc[k & 3] += mv[k].y * wq[k].y;
+                    }
+                }
+                double a0 = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+                if (lg == 0 && rw < mdp) {
+                    double yv = a0 * invb;
+                    if (pro) {  // y' = M q_j - beta_{j-1} q_{j-1}; alpha partial q_j . y'
+                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
+                        apl += (win[rw] * invb) * yv;
+                    }
+                    wout[rw] = yv;
+                }
+            }
+        } else {
+            for (int r0 = 0; r0 < mdp; r0 += (NT >> 2)) {
+                const int rw = r0 + lrow;
+                double a0 = 0.0, a1 = 0.0;
+                if (rw < mdp) {
+                    const double* Mr = M + (size_t)rw * ld;
+                    for (int c = 2 * lg; c < mdp; c += 8) {
+                        double2 mv = *reinterpret_cast<const double2*>(Mr + c);
+                        double2 wq = *reinterpret_cast<const double2*>(win + c);
+                        a0 += mv.x * wq.x;
+                        a1 += mv.y * wq.y;
+                    }
+                }
+                a0 += a1;
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 1);
+                a0 += __shfl_xor_sync(0xffffffffu, a0, 2);
+                if (lg == 0 && rw < mdp) {
+                    double yv = a0 * invb;
+                    if (pro) {
+                        if (j > 0) yv -= bjm1 * (wout[rw] * invb_prev);  // q_{j-1} (u_{j-1} still in wout)
+                        apl += (win[rw] * invb) * yv;
+                    }
+                    wout[rw] = yv;
+                }
+            }
+        }
+        if (pro) {  // alpha partials: the owner lanes (lg == 0)
+            apl += __shfl_xor_sync(0xffffffffu, apl, 16);
+            apl += __shfl_xor_sync(0xffffffffu, apl, 8);
+            apl += __shfl_xor_sync(0xffffffffu, apl, 4);
+            if (T.lane == 0) part[T.warp] = apl;
+        }
+        __syncthreads();
+        long long tl1 = clock64();
+        long long tl2 = tl1, tl3 = tl1;
+        // ---- (B..E) classical Gram-Schmidt against q_0..q_j
+        double alpha = 0.0, nn = 0.0, nn_before = 0.0;
+        int pass0 = 0;
+        bool full = true;
+        if (pro) {
+            bool reorth;
+            if (reorth_left > 0) { reorth = true; --reorth_left; }
+            else if (part[40 + (j & 1)] != 0.0) { reorth = true; reorth_left = 1; }
+            else reorth = false;
+            for (int w = 0; w < T.nwarps; ++w) alpha += part[w];
+            double nloc = 0.0;
+            for (int e = T.tid; e < mdp; e += T.nthr) {
+                const double wn = (e < md) ? wout[e] - alpha * (win[e] * invb) : 0.0;  // q_j from shared memory
+                wout[e] = wn;
+                nloc += wn * wn;
+            }
+            nloc = warp_sum(nloc);
+            if (T.lane == 0) red2[T.warp] = nloc;
+            __syncthreads();
+            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
+            nn_before = alpha * alpha + nn;  // |y'|^2
+            if (!reorth && nn >= 1e-12 * nn_before) {
+                pass0 = 2;
+                full = false;
+            } else {
+                pass0 = 1;  // one Gram-Schmidt pass on w
+            }
+        }
+        for (int pass = pass0; pass < 2; ++pass) {
+            const int nrows = (pass == 0) ? j + 2 : j + 1;  // row j+1 = w'.w'
+            if (mdp <= 128) {
+                double2 w0 = make_double2(0.0, 0.0), w1 = make_double2(0.0, 0.0);
+                const int i0 = 2 * T.lane, i1 = 64 + 2 * T.lane;
+                if (i0 < mdp) w0 = *reinterpret_cast<const double2*>(wout + i0);
+                if (i1 < mdp) w1 = *reinterpret_cast<const double2*>(wout + i1);
+                const int NW = T.nwarps;
+                for (int ib = T.warp; ib < nrows; ib += 4 * NW) {
+                    double sacc[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int i = ib + u * NW;
+                        const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
+                        double sa = 0.0;
+                        if (i < nrows) {
+                            if (i0 < mdp) {
+                                double2 q0 = *reinterpret_cast<const double2*>(qi + i0);
+                                sa += q0.x * w0.x + q0.y * w0.y;
+                            }
+                            if (i1 < mdp) {
+                                double2 q1 = *reinterpret_cast<const double2*>(qi + i1);
+                                sa += q1.x * w1.x + q1.y * w1.y;
+                            }
+                        }
+                        sacc[u] = sa;
+                    }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) sacc[u] += __shfl_xor_sync(0xffffffffu, sacc[u], o);
+                    if (T.lane == 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (ib + u * NW < nrows) hb[ib + u * NW] = sacc[u];
+                    }
+                }
+            } else {
+                for (int i = T.warp; i < nrows; i += T.nwarps) {
+                    const double* qi = (i <= j) ? Q + (size_t)i * ld : wout;
+                    double sacc = 0.0;
+                    for (int c = T.lane; c < mdp; c += 32) sacc += qi[c] * wout[c];
+                    sacc = warp_sum(sacc);
+                    if (T.lane == 0) hb[i] = sacc;
+                }
+            }
+            __syncthreads();
+            if (pass == 0) tl2 = clock64();
+            alpha += hb[j];
+            if (pass == 0) nn_before = hb[j + 1];
+            {
+                const int g = T.tid & 3, egrp = T.nthr >> 2;
+                double nloc = 0.0;
+                for (int e0 = 0; e0 < mdp; e0 += egrp) {
+                    const int e = e0 + (T.tid >> 2);
+                    double sa = 0.0, sb = 0.0;
+                    if (e < mdp) {
+                        for (int ibase = 0; ibase <= j; ibase += 64) {
+                            double acc4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int i = ibase + g + 4 * k;
+                                if (i <= j) acc4[k & 3] += hb[i] * Q[(size_t)i * ld + e];
+                            }
+                            sa += (acc4[0] + acc4[1]) + (acc4[2] + acc4[3]);
+                        }
+                    }
+                    sa += sb;
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 1);
+                    sa += __shfl_xor_sync(0xffffffffu, sa, 2);
+                    if (e < mdp) {
+                        double wn = wout[e] - sa;
+                        __syncwarp();
+                        if (g == 0) wout[e] = wn;
+                        nloc += (g == 0) ? wn * wn : 0.0;
+                    }
+                }
+                // partial norms live in the g == 0 lanes: reduce over lanes 4, 8, 16 apart
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 4);
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 8);
+                nloc += __shfl_xor_sync(0xffffffffu, nloc, 16);
+                if (T.lane == 0) red2[T.warp] = nloc;
+            }
+            __syncthreads();
+            nn = 0.0;
+            for (int w = 0; w < T.nwarps; ++w) nn += red2[w];
+            if (pass == 0) tl3 = clock64();
+            if (prof && T.tid == 0 && pass == 1) atomicAdd(&prof[15], 1ull);
+            // second (DGKS) pass only on severe cancellation, as in lanczos_reg (one CGS pass
+            // keeps theta_max within ~20 eps |M|; the 0.5 criterion fired on 2/3 of the iterations)
+            if (!(nn < 1e-12 * nn_before)) break;
+        }
+        const double beta = sqrt(nn);
+        if (T.tid == 0) {
+            al[j] = alpha;
+            be[j] = beta;
+            if (fastck) {
+                b2[j] = nn;
+                rbe[j] = 1.0 / beta;
+            }
+        }
+        if (pro) {
+            bjm1 = beta;
+            was_full = full;
+            invb_prev = invb;  // 1 / beta_{j-1}, the scale of u_j held in win (q_j = u_j * invb)
+        }
+        tnorm = fmax(tnorm, fabs(alpha) + beta + (j > 0 ? be[j - 1] : 0.0));
+        J = j + 1;
+        const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
+        if (prof && T.tid == 0) {
+            long long tl4 = clock64();
+            atomicAdd(&prof[12], (unsigned long long)(tl1 - tl0));
+            atomicAdd(&prof[13], (unsigned long long)(tl2 - tl1));
+            atomicAdd(&prof[14], (unsigned long long)(tl3 - tl2));
+            atomicAdd(&prof[16], (unsigned long long)(tl4 - tl3));
+        }
+        // next iteration uses q_{j+1} = w' / beta
+        double* tmp = win;
+        win = wout;
+        wout = tmp;
+        invb = 1.0 / beta;
+        if (fastck && (exhausted || J >= next_check)) {
+            __syncthreads();  // al / be / b2 / rbe of this step visible
+            lanczos_check(T.tid, (int)(al - sm), (int)(be - sm), (int)(b2 - sm), (int)(rbe - sm), J, beta, tnorm,
+                          need_bot, exhausted, md, oShd, prof);
+            __syncthreads();
+            if (sm[oShd + CK_DONE] != 0.0) break;
+            next_check = (int)sm[oShd + CK_NEXT];
+        } else if (exhausted || J >= next_check) {
+            __syncthreads();  // al/be of this step visible
+            long long tc0 = clock64();
+            double glo = SW_INF, ghi = -SW_INF;
+            for (int i = T.tid; i < J; i += T.nthr) {
+                double rsum = (i > 0 ? fabs(be[i - 1]) : 0.0) + (i + 1 < J ? fabs(be[i]) : 0.0);
+                glo = fmin(glo, al[i] - rsum);
+                ghi = fmax(ghi, al[i] + rsum);
+            }
+            ghi = block_max(T, ghi, red);
+            if (need_bot) glo = block_min(T, glo, red);
+            if (T.tid == 0) shd[0] = tri_laguerre(al, be, J, ghi + 1e-13 * tnorm);
+            if (need_bot && T.tid == 32) shd[1] = tri_laguerre(al, be, J, glo - 1e-13 * tnorm);
+            __syncthreads();
+            const double th = shd[0];
+            double res = tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, sh_r);
+            double thmin = SW_INF, resmin = 0.0;
+            if (need_bot) {
+                thmin = shd[1];
+                resmin = tri_twisted_vec(T, al, be, J, thmin, be[J - 1], dp, dm, sv2, red, sh_r);
+            }
+            th_prev = th;
+            res_prev = res;
+            *theta_top = th;
+            *theta_bot = thmin;
+            if (prof && T.tid == 0) {
+                atomicAdd(&prof[9], (unsigned long long)(clock64() - tc0));
+                atomicAdd(&prof[11], 1ull);
+            }
+            const double tol = 1e-14 * tnorm;
+            if (exhausted || ((!need_top || res <= tol) && (!need_bot || resmin <= tol))) break;
+            next_check = min(md, J + 8);
+        }
+    }
+    (void)th_prev;
+    (void)res_prev;
+    __syncthreads();
+    if (fastck) {  // the converged Ritz values and their vectors of T_J
+        const double th = sm[oShd + CK_TTOP];
+        *theta_top = th;
+        tri_twisted_vec(T, al, be, J, th, be[J - 1], dp, dm, sv, red, sh_r);
+        if (need_bot) {
+            const double thb = sm[oShd + CK_TBOT];
+            *theta_bot = thb;
+            tri_twisted_vec(T, al, be, J, thb, be[J - 1], dp, dm, sv2, red, sh_r);
+        }
+    }
+    return J;
+}
+
 // K2 vector slots (length vl = mp + 8 each) in the shared vector area
 enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_AL = 6, V_BE = 7, V_SV = 8, V_ZZ = 9,
              V_YY = 10, V_DP = 11, V_BV = 12, V_SV2 = 13, V_B2 = 13, V_DM = 14, V_WV = 15, V_LZ = 17 };
@@ -1177,18 +1230,6 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     (void)jhint;
     // first check by size: small problems need nearly the full dimension (m = 40: J ~ 0.85 md;
     // m <= 24: J = md), larger ones about half (m = 100: J ~ 0.5 md)
-#ifndef SW_FIRST_CHECK_PCT
-#define SW_FIRST_CHECK_PCT 25  // m > 64 (measured: 25% of md +6.7% over 40% at m = 100)
-#endif
-#ifndef SW_FIRST_CHECK_PCT_SMALL
-#define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
-#endif
-#ifndef SW_FIRST_CHECK_SMALL_MD
-#define SW_FIRST_CHECK_SMALL_MD 48
-#endif
-#ifndef SW_FIRST_CHECK_PCT_MID
-#define SW_FIRST_CHECK_PCT_MID 50  // SW_FIRST_CHECK_SMALL_MD < m <= 64
-#endif
     int next_check = (md <= 24) ? md
                    : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                    : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
@@ -1634,7 +1675,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                 }
                 else
                     J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
-                                    &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min, vec + 17 * vl, vec);
+                                    &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min, vec + 17 * vl, vec,
+                                    vec + 4 * vl, vec + 9 * vl, (int)(vec - smem_dyn) + 48);
                 lanczos_J = J;
                 if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);
                 PROF_MARK(4);
