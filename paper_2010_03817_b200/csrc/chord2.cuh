@@ -82,8 +82,10 @@ __device__ __forceinline__ void tile_msub(double (&acc)[2], const double* A, int
 }
 
 // X <- H X H and Y <- H Y H together (H = I - beta h h^T, X, Y symmetric m x m)
+// apply = false: only the rank-2 vectors p (X <- X - h p^T - p h^T is left to the caller, who may
+// fuse it into its next pass over the matrices)
 __device__ void householder_congruence2(const Team& T, double* X, double* Y, int m, int ld, const double* h,
-                                        double beta, double* px, double* py, double* red) {
+                                        double beta, double* px, double* py, double* red, bool apply = true) {
     for (int i = T.warp; i < m; i += T.nwarps) {
         double sx = 0.0, sy = 0.0;
         for (int j = T.lane; j < m; j += 32) {
@@ -124,6 +126,7 @@ __device__ void householder_congruence2(const Team& T, double* X, double* Y, int
         py[i] -= Ky * h[i];
     }
     __syncthreads();
+    if (!apply) return;
     for (int i = T.warp; i < m; i += T.nwarps) {
         const double hi = h[i], pxi = px[i], pyi = py[i];
         for (int j = T.lane; j < m; j += 32) {

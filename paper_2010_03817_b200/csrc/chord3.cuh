@@ -62,9 +62,11 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
     const int m = P.m, ld = P.ld;
     const int mp = (m + 7) & ~7;
     const int vl = mp + 8;
+    // one spare row each: a deflated boundary start works in place on the trailing block
+    // (G + ld + 1, B + ld + 1), whose padded rows reach row mp
     double* G = smem_dyn;
-    double* B = G + (size_t)mp * ld;
-    double* vec = B + (size_t)mp * ld;
+    double* B = G + (size_t)(mp + 1) * ld;
+    double* vec = B + (size_t)(mp + 1) * ld;
     double* uu = vec + V_UU * vl;
     double* hh = vec + V_HH * vl;
     double* pw = vec + V_PW * vl;
@@ -98,6 +100,8 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         int md = m;
         double a_schur = 0.0, beta_h = 0.0;
         bool outward = false;
+        double* Gd = G;  // the matrices of the (possibly deflated) pencil
+        double* Bd = B;
         if (defl) {
             double nu = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) nu += uu[i] * uu[i];
@@ -109,63 +113,53 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
             double h2 = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
             beta_h = 2.0 / block_sum(T, h2, red);
-            householder_congruence2(T, G, B, m, ld, hh, beta_h, pw, yy, red);
-            a_schur = B[0];
+            // H G H and H B H (H u = -+|u| e_0) as rank-2 updates X - h p^T - p h^T, applied below
+            // only where needed: the trailing block, in place, fused with the Schur complement of
+            // B's (0, 0) pivot a and border b (R6)
+            householder_congruence2(T, G, B, m, ld, hh, beta_h, pw, yy, red, false);
+            a_schur = B[0] - (hh[0] * yy[0] + yy[0] * hh[0]);
             outward = !(a_schur > 0.0);
-            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld];
+            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld] - (hh[i + 1] * yy[0] + yy[i + 1] * hh[0]);
             __syncthreads();
-            // Schur complement + shift the (1..m-1) block to (0..m-2)
             md = m - 1;
-            for (int i0 = 0; i0 < md; i0 += T.nwarps) {
-                constexpr int CMAX = 8;
-                double gv[CMAX], bvv[CMAX];
-                const int i = i0 + T.warp;
-#pragma unroll
-                for (int c = 0; c < CMAX; ++c) {
-                    int jx = T.lane + 32 * c;
-                    if (i < md && jx < md) {
-                        gv[c] = G[(i + 1) * ld + jx + 1];
-                        bvv[c] = outward ? 0.0 : B[(i + 1) * ld + jx + 1] - bv[i] * bv[jx] / a_schur;
-                    }
+            for (int i = 1 + T.warp; i < m; i += T.nwarps) {
+                const double hi = hh[i], pxi = pw[i], pyi = yy[i], bi = bv[i - 1];
+                for (int jx = 1 + T.lane; jx < m; jx += 32) {
+                    const double hj = hh[jx];
+                    G[i * ld + jx] -= hi * pw[jx] + pxi * hj;
+                    const double bij = B[i * ld + jx] - (hi * yy[jx] + pyi * hj);
+                    B[i * ld + jx] = outward ? 0.0 : bij - bi * bv[jx - 1] / a_schur;
                 }
-                __syncthreads();
-#pragma unroll
-                for (int c = 0; c < CMAX; ++c) {
-                    int jx = T.lane + 32 * c;
-                    if (i < md && jx < md) {
-                        G[i * ld + jx] = gv[c];
-                        B[i * ld + jx] = bvv[c];
-                    }
-                }
-                __syncthreads();
             }
+            Gd = G + ld + 1;
+            Bd = B + ld + 1;
         }
         const int mdp = (md + 7) & ~7;
         for (int i = md + T.warp; i < mdp; i += T.nwarps)
             for (int j = T.lane; j < mdp; j += 32) {
-                G[i * ld + j] = (i == j) ? 1.0 : 0.0;
-                G[j * ld + i] = (i == j) ? 1.0 : 0.0;
-                B[i * ld + j] = 0.0;
-                B[j * ld + i] = 0.0;
+                Gd[i * ld + j] = (i == j) ? 1.0 : 0.0;
+                Gd[j * ld + i] = (i == j) ? 1.0 : 0.0;
+                Bd[i * ld + j] = 0.0;
+                Bd[j * ld + i] = 0.0;
             }
         __syncthreads();
         int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
         PROF_MARK(1);
         if (!outward && md >= 1) {
-            const bool okc = cholesky_inv_blocked_la(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
+            const bool okc = cholesky_inv_blocked_la(T, Gd, mdp, ld, rdiag, Lv, &sh_i[2]);
             PROF_MARK(2);
             if (!okc) {
                 status |= ST_FAILED;
             } else {
-                congruence_inv(T, G, Lv, B, mdp, ld);
+                congruence_inv(T, Gd, Lv, Bd, mdp, ld);
                 PROF_MARK(3);
                 // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
                 double* Mw = P.wM + (size_t)slot * P.w_mstride;
                 double* Lw = P.wL + (size_t)slot * P.w_mstride;
                 for (int i = T.warp; i < mdp; i += T.nwarps)
                     for (int jx = T.lane; jx < mdp; jx += 32) {
-                        Mw[i * ld + jx] = -0.5 * (B[i * ld + jx] + B[jx * ld + i]);
-                        if (jx <= i) Lw[i * ld + jx] = G[i * ld + jx];
+                        Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
+                        if (jx <= i) Lw[i * ld + jx] = Gd[i * ld + jx];
                     }
             }
         }
