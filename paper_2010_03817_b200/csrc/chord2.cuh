@@ -1524,11 +1524,11 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
     const int mp = (m + 7) & ~7;
     double* base = SMEM ? smem_dyn : (P.scratch + (size_t)blockIdx.x * P.scratch_stride);
     double* G = base;
-    double* B = base + (size_t)mp * ld;
+    double* B = base + (size_t)(mp + 1) * ld;  // one spare row each: in-place deflation (below)
     double* Qm = G;  // Lanczos basis reuses L's space while L is parked in P.lsave
     // the vector area (+ inverse diagonal blocks) in shared memory on both variants; the global
     // variant keeps only G, B (the Lanczos basis, M) in its scratch slice
-    double* vec = SMEM ? B + (size_t)mp * ld : smem_dyn;
+    double* vec = SMEM ? B + (size_t)(mp + 1) * ld + 2 : smem_dyn;
     double* Lsave = P.lsave + (size_t)blockIdx.x * P.lsave_stride;
     const int vl = mp + 8;
     double* uu = vec + 0 * vl;
@@ -1561,10 +1561,13 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
         __syncthreads();
         long long t_prof = clock64();
 
-        // ---- 1. unpack A(x) -> G, A(v) -> B (full symmetric), zero padding
-        unpack_sym(T, ax, G, m, ld);
-        unpack_sym(T, av, B, m, ld);
+        // ---- 1. unpack A(x) -> G, A(v) -> B0 (full symmetric), zero padding.  A boundary start
+        // puts B one double further (B0 = B + 1) so that its deflated trailing block
+        // B0 + ld + 1 -- M for the Lanczos double2 loads -- is 16-byte aligned
         const bool defl = (bnd == 0);
+        double* B0 = B + (defl ? 1 : 0);
+        unpack_sym(T, ax, G, m, ld);
+        unpack_sym(T, av, B0, m, ld);
         if (defl)
             for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
         __syncthreads();
@@ -1572,6 +1575,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
         int md = m;
         double a_schur = 0.0, beta_h = 0.0;
         bool outward = false;
+        double* Gd = G;  // the matrices of the (possibly deflated) pencil
+        double* Bd = B0;
         if (defl) {
             double nu = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) nu += uu[i] * uu[i];
@@ -1583,46 +1588,34 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
             double h2 = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
             beta_h = 2.0 / block_sum(T, h2, red);
-            householder_congruence2(T, G, B, m, ld, hh, beta_h, pw, yy, red);
-            a_schur = B[0];
+            // the rank-2 congruence fused with the Schur complement on the trailing block, in
+            // place (as factor_kernel): the deflated pencil is (G + ld + 1, B + ld + 1)
+            householder_congruence2(T, G, B0, m, ld, hh, beta_h, pw, yy, red, false);
+            a_schur = B0[0] - (hh[0] * yy[0] + yy[0] * hh[0]);
             outward = !(a_schur > 0.0);
-            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B[(i + 1) * ld];
+            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = B0[(i + 1) * ld] - (hh[i + 1] * yy[0] + yy[i + 1] * hh[0]);
             __syncthreads();
-            // Schur complement + shift the (1..m-1) block to (0..m-2): chunks of nwarps
-            // rows, each warp stages one source row in registers (m <= 256).
             md = m - 1;
-            for (int i0 = 0; i0 < md; i0 += T.nwarps) {
-                constexpr int CMAX = 8;
-                double gv[CMAX], bvv[CMAX];
-                const int i = i0 + T.warp;
-#pragma unroll
-                for (int c = 0; c < CMAX; ++c) {
-                    int jx = T.lane + 32 * c;
-                    if (i < md && jx < md) {
-                        gv[c] = G[(i + 1) * ld + jx + 1];
-                        bvv[c] = outward ? 0.0 : B[(i + 1) * ld + jx + 1] - bv[i] * bv[jx] / a_schur;
-                    }
+            for (int i = 1 + T.warp; i < m; i += T.nwarps) {
+                const double hi = hh[i], pxi = pw[i], pyi = yy[i], bi = bv[i - 1];
+                for (int jx = 1 + T.lane; jx < m; jx += 32) {
+                    const double hj = hh[jx];
+                    G[i * ld + jx] -= hi * pw[jx] + pxi * hj;
+                    const double bij = B0[i * ld + jx] - (hi * yy[jx] + pyi * hj);
+                    B0[i * ld + jx] = outward ? 0.0 : bij - bi * bv[jx - 1] / a_schur;
                 }
-                __syncthreads();
-#pragma unroll
-                for (int c = 0; c < CMAX; ++c) {
-                    int jx = T.lane + 32 * c;
-                    if (i < md && jx < md) {
-                        G[i * ld + jx] = gv[c];
-                        B[i * ld + jx] = bvv[c];
-                    }
-                }
-                __syncthreads();
             }
+            Gd = G + ld + 1;
+            Bd = B0 + ld + 1;
         }
         const int mdp = (md + 7) & ~7;
         // padding rows/cols [md, mdp): G = I, B = 0
         for (int i = md + T.warp; i < mdp; i += T.nwarps)
             for (int j = T.lane; j < mdp; j += 32) {
-                G[i * ld + j] = (i == j) ? 1.0 : 0.0;
-                G[j * ld + i] = (i == j) ? 1.0 : 0.0;
-                B[i * ld + j] = 0.0;
-                B[j * ld + i] = 0.0;
+                Gd[i * ld + j] = (i == j) ? 1.0 : 0.0;
+                Gd[j * ld + i] = (i == j) ? 1.0 : 0.0;
+                Bd[i * ld + j] = 0.0;
+                Bd[j * ld + i] = 0.0;
             }
         __syncthreads();
         PROF_MARK(1);
@@ -1637,30 +1630,30 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
             // (the shared-memory variants with cholesky_inv_blocked_la + the left-looking
             // congruence were measured 3-7% slower at m = 10..60)
             double* Lv = vec + NVEC2 * vl + 64;
-            bool okc = SMEM ? cholesky_blocked(T, G, mdp, ld, rdiag, &sh_i[2])
-                            : cholesky_inv_blocked(T, G, mdp, ld, rdiag, Lv, &sh_i[2]);
+            bool okc = SMEM ? cholesky_blocked(T, Gd, mdp, ld, rdiag, &sh_i[2])
+                            : cholesky_inv_blocked(T, Gd, mdp, ld, rdiag, Lv, &sh_i[2]);
             PROF_MARK(2);
             if (!okc) {
                 failed = true;
             } else {
                 if (!SMEM && SW_GLOBAL_LL) {  // m > 112: +11% at m = 200
-                    congruence_inv(T, G, Lv, B, mdp, ld);
+                    congruence_inv(T, Gd, Lv, Bd, mdp, ld);
                 } else if (SMEM) {
-                    trsm_blocked<false>(T, G, B, mdp, ld, rdiag);
-                    trsm_blocked<true>(T, G, B, mdp, ld, rdiag);
+                    trsm_blocked<false>(T, Gd, Bd, mdp, ld, rdiag);
+                    trsm_blocked<true>(T, Gd, Bd, mdp, ld, rdiag);
                 } else {
-                    trsm_inv_blocked<false>(T, G, Lv, B, mdp, ld);
-                    trsm_inv_blocked<true>(T, G, Lv, B, mdp, ld);
+                    trsm_inv_blocked<false>(T, Gd, Lv, Bd, mdp, ld);
+                    trsm_inv_blocked<true>(T, Gd, Lv, Bd, mdp, ld);
                 }
                 PROF_MARK(3);
                 // ---- M = -(B + B^T)/2 in place; park L (lower, with rdiag) in global
                 // scratch so that the Lanczos basis can use its shared memory.
                 for (int i = T.warp; i < mdp; i += T.nwarps) {
                     for (int jx = T.lane; jx <= i; jx += 32) {
-                        double sv_ = -0.5 * (B[i * ld + jx] + B[jx * ld + i]);
-                        B[i * ld + jx] = sv_;
-                        B[jx * ld + i] = sv_;
-                        Lsave[i * ld + jx] = G[i * ld + jx];
+                        double sv_ = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
+                        Bd[i * ld + jx] = sv_;
+                        Bd[jx * ld + i] = sv_;
+                        Lsave[i * ld + jx] = Gd[i * ld + jx];
                     }
                 }
                 __syncthreads();
@@ -1670,14 +1663,14 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                     // vector area + 64 slack doubles: [0,32) partial sums, [32,40) check results
                     const int oVec = (int)(vec - smem_dyn), oRed = oVec + NVEC2 * vl;
                     const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
-                    J = lanczos_reg<NT, KC>((int)(B - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
+                    J = lanczos_reg<NT, KC>((int)(Bd - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
                                             vl, oRed, jhint, P.prof);
                     if (P.jlast && T.tid == 0) P.jlast[slot] = J;
                     theta_max = smem_dyn[oRed + 32 + 4];
                     theta_min = smem_dyn[oRed + 32 + 5];
                 }
                 else
-                    J = lanczos_run(T, B, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
+                    J = lanczos_run(T, Bd, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
                                     &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min, vec + 17 * vl, vec,
                                     vec + 4 * vl, vec + 9 * vl, (int)(vec - smem_dyn) + 48);
                 lanczos_J = J;
@@ -1700,7 +1693,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                     }
                     __syncthreads();
                     for (int i = T.warp; i < md; i += T.nwarps)
-                        for (int jx = T.lane; jx < i; jx += 32) G[i * ld + jx] = Lsave[i * ld + jx];
+                        for (int jx = T.lane; jx < i; jx += 32) Gd[i * ld + jx] = Lsave[i * ld + jx];
                     __syncthreads();
                     PROF_MARK(6);
                     // y = L^{-T} z, blocked backwards over 8-row blocks: warp 0 solves the
@@ -1715,7 +1708,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                                 // y_c = z_c / L_cc; then z_r -= L_cr y_c for r < c
                                 const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
                                 if (r == c) zr = yc;
-                                else if (r < c) zr -= G[(k0 + c) * ld + k0 + r] * yc;
+                                else if (r < c) zr -= Gd[(k0 + c) * ld + k0 + r] * yc;
                             }
                             if (r < 8) yy[k0 + r] = zr;
                         }
@@ -1723,7 +1716,7 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                         for (int i = T.tid; i < k0; i += T.nthr) {
                             double acc = zz[i];
 #pragma unroll
-                            for (int c = 0; c < 8; ++c) acc -= G[(k0 + c) * ld + i] * yy[k0 + c];
+                            for (int c = 0; c < 8; ++c) acc -= Gd[(k0 + c) * ld + i] * yy[k0 + c];
                             zz[i] = acc;
                         }
                         __syncthreads();

@@ -260,7 +260,8 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         ctx->chord_threads = 512;
     }
     size_t vecs = (size_t)NVEC2 * (mp + 8) + 64;
-    size_t per_cta = (size_t)2 * mp * ctx->ld + vecs;
+    // G, B with one spare row each (in-place deflation) and B's alignment shift
+    size_t per_cta = (size_t)2 * (mp + 1) * ctx->ld + 2 + vecs;
     ctx->smem_bytes = per_cta * sizeof(double);
     int occ = 0;
     if (ctx->k2_variant != 2 && ctx->smem_bytes <= 227 * 1024) {
@@ -303,8 +304,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     // fused kernel was measured faster: 1.9M vs 1.4M calls/s at m = 40; it does not spill there)
     // (and only where the factor kernel's G, B and inverse diagonal blocks fit: mp <= 104;
     // 104 < mp <= 112 keeps the fused variant 3)
-    // + inverse diagonal blocks, + one spare row per matrix (in-place deflation)
-    const size_t f_smem = per_cta * sizeof(double) + sizeof(double) * 8 * (size_t)mp + sizeof(double) * 2 * ctx->ld;
+    const size_t f_smem = per_cta * sizeof(double) + sizeof(double) * 8 * (size_t)mp;  // + inverse diagonal blocks
     if ((ctx->k2_variant == 1 || ctx->k2_variant == 3) && f_smem <= 227 * 1024 && !getenv("SPECWALK_K2_FUSED")) {
         ctx->k2_split = 1;
         ctx->f_smem = f_smem;
