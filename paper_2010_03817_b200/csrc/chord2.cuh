@@ -41,7 +41,7 @@ constexpr int NVEC2 = 20;
 #define SW_CHECK_STEPMAX 8  // cap on the rate-predicted distance to the next check
 #endif
 #ifndef SW_FIRST_CHECK_PCT
-#define SW_FIRST_CHECK_PCT 25  // m > 64 (measured: 25% of md +6.7% over 40% at m = 100)
+#define SW_FIRST_CHECK_PCT 30  // m > 64 (measured: 25-30% of md ~+7% over 40% at m = 100)
 #endif
 #ifndef SW_FIRST_CHECK_PCT_SMALL
 #define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
