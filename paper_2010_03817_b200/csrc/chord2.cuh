@@ -43,6 +43,9 @@ constexpr int NVEC2 = 20;
 #ifndef SW_FIRST_CHECK_PCT
 #define SW_FIRST_CHECK_PCT 30  // m > 64 (measured: 25-30% of md ~+7% over 40% at m = 100)
 #endif
+#ifndef SW_FIRST_CHECK_PCT_GLOBAL
+#define SW_FIRST_CHECK_PCT_GLOBAL 15  // global-scratch variant (m > 112): costlier iterations, cheap checks (measured)
+#endif
 #ifndef SW_FIRST_CHECK_PCT_SMALL
 #define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
 #endif
@@ -728,7 +731,7 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
     const int jfirst = fastck ? ((md <= 24) ? md
                                  : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                                  : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100
-                                              : max(12, (md * SW_FIRST_CHECK_PCT) / 100))
+                                              : max(12, (md * SW_FIRST_CHECK_PCT_GLOBAL) / 100))
                               : max(min(md, 12), (md * 9) / 20);
     int next_check = jfirst;
     if (fastck && T.tid == 0) {
