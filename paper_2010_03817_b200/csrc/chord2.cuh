@@ -43,11 +43,14 @@ constexpr int NVEC2 = 20;
 #ifndef SW_FIRST_CHECK_PCT
 #define SW_FIRST_CHECK_PCT 30  // m > 64 (measured: 25-30% of md ~+7% over 40% at m = 100)
 #endif
+#ifndef SW_FIRST_CHECK_FULL_MD
+#define SW_FIRST_CHECK_FULL_MD 36  // up to here the first check is at J = md (the whole space: ~+50% at m = 30)
+#endif
 #ifndef SW_FIRST_CHECK_PCT_GLOBAL
 #define SW_FIRST_CHECK_PCT_GLOBAL 15  // global-scratch variant (m > 112): costlier iterations, cheap checks (measured)
 #endif
 #ifndef SW_FIRST_CHECK_PCT_SMALL
-#define SW_FIRST_CHECK_PCT_SMALL 80  // 24 < m <= SW_FIRST_CHECK_SMALL_MD
+#define SW_FIRST_CHECK_PCT_SMALL 88  // SW_FIRST_CHECK_FULL_MD < m <= SW_FIRST_CHECK_SMALL_MD (measured)
 #endif
 #ifndef SW_FIRST_CHECK_SMALL_MD
 #define SW_FIRST_CHECK_SMALL_MD 48
@@ -728,7 +731,7 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
     // backward recurrence, the next check from the observed rate) and its first-check rule
     const bool fastck = (oShd >= 0);
     extern __shared__ __align__(16) double sm[];
-    const int jfirst = fastck ? ((md <= 24) ? md
+    const int jfirst = fastck ? ((md <= SW_FIRST_CHECK_FULL_MD) ? md
                                  : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                                  : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100
                                               : max(12, (md * SW_FIRST_CHECK_PCT_GLOBAL) / 100))
@@ -1236,7 +1239,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     (void)jhint;
     // first check by size: small problems need nearly the full dimension (m = 40: J ~ 0.85 md;
     // m <= 24: J = md), larger ones about half (m = 100: J ~ 0.5 md)
-    int next_check = (md <= 24) ? md
+    int next_check = (md <= SW_FIRST_CHECK_FULL_MD) ? md
                    : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                    : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
     int J = 0;
