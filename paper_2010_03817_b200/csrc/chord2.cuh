@@ -46,6 +46,9 @@ constexpr int NVEC2 = 20;
 #ifndef SW_FIRST_CHECK_FULL_MD
 #define SW_FIRST_CHECK_FULL_MD 36  // up to here the first check is at J = md (the whole space: ~+50% at m = 30)
 #endif
+#ifndef SW_FIRST_CHECK_PCT_HMC
+#define SW_FIRST_CHECK_PCT_HMC 10  // lambda_min(N_1) solves of HMC-r (lanczos_kernel with zall), m > 64 (measured)
+#endif
 #ifndef SW_FIRST_CHECK_PCT_GLOBAL
 #define SW_FIRST_CHECK_PCT_GLOBAL 15  // global-scratch variant (m > 112): costlier iterations, cheap checks (measured)
 #endif
@@ -1143,7 +1146,7 @@ __device__ __noinline__ void lanczos_checker(const int lane, const int oAl, cons
 template <int NT, int KC, bool GM = false, bool USEQT = true>
 __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
                                            const bool need_bot, const int oVec, const int vl, const int oRed,
-                                           const int jhint, unsigned long long* prof, const double* __restrict__ Mg = nullptr,
+                                           const int first_pct, unsigned long long* prof, const double* __restrict__ Mg = nullptr,
                                            int oQTin = -1) {
     // everything addressed as offsets into the dynamic shared memory (32-bit LDS/STS)
     extern __shared__ __align__(16) double sm[];
@@ -1236,12 +1239,13 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     // of a chain need similar J), else at 40% of md; later checks from the observed rate
     // (a per-chain hint from the previous call was measured to RAISE J: consecutive calls of a
     // chain differ too much; the first check stays at 40% of md)
-    (void)jhint;
+
     // first check by size: small problems need nearly the full dimension (m = 40: J ~ 0.85 md;
     // m <= 24: J = md), larger ones about half (m = 100: J ~ 0.5 md)
     int next_check = (md <= SW_FIRST_CHECK_FULL_MD) ? md
                    : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                    : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
+    if (first_pct > 0 && md > 64) next_check = max(12, (md * first_pct) / 100);  // caller's rule (HMC-r)
     int J = 0;
     double tnorm = 0.0;
     if (ASYNC && warp == NW - 1) {
@@ -1668,9 +1672,8 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                 {
                     // vector area + 64 slack doubles: [0,32) partial sums, [32,40) check results
                     const int oVec = (int)(vec - smem_dyn), oRed = oVec + NVEC2 * vl;
-                    const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
                     J = lanczos_reg<NT, KC>((int)(Bd - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
-                                            vl, oRed, jhint, P.prof);
+                                            vl, oRed, 0, P.prof);
                     if (P.jlast && T.tid == 0) P.jlast[slot] = J;
                     theta_max = smem_dyn[oRed + 32 + 4];
                     theta_min = smem_dyn[oRed + 32 + 5];

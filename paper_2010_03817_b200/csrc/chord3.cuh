@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         }
         const int mdp = (md + 7) & ~7;
         const double* Mw = P.wM + (size_t)slot * P.w_mstride;
-        const int jhint = (P.jlast && P.mode == 0) ? P.jlast[slot] : 0;
-        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1 && !P.zall, oVec, vl, oRed, jhint,
+        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1 && !P.zall, oVec, vl, oRed,
+                                                       P.zall ? SW_FIRST_CHECK_PCT_HMC : 0,
                                                        P.prof, Mw, 0);
         if (P.jlast && tid == 0) P.jlast[slot] = J;
         const double theta_max = smem_dyn[oRed + 32 + 4];
