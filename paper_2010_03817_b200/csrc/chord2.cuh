@@ -49,6 +49,9 @@ constexpr int NVEC2 = 20;
 #ifndef SW_FIRST_CHECK_PCT_HMC
 #define SW_FIRST_CHECK_PCT_HMC 10  // lambda_min(N_1) solves of HMC-r (lanczos_kernel with zall), m > 64 (measured)
 #endif
+#ifndef SW_FIRST_PCT_MIN_MD
+#define SW_FIRST_PCT_MIN_MD 12  // the caller's first-check rule applies above this md (HMC-r: measured +5..35% at m = 16..60)
+#endif
 #ifndef SW_FIRST_CHECK_PCT_GLOBAL
 #define SW_FIRST_CHECK_PCT_GLOBAL 15  // global-scratch variant (m > 112): costlier iterations, cheap checks (measured)
 #endif
@@ -1245,7 +1248,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     int next_check = (md <= SW_FIRST_CHECK_FULL_MD) ? md
                    : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
                    : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
-    if (first_pct > 0 && md > 64) next_check = max(12, (md * first_pct) / 100);  // caller's rule (HMC-r)
+    if (first_pct > 0 && md > SW_FIRST_PCT_MIN_MD) next_check = max(12, (md * first_pct) / 100);  // caller's rule (HMC-r)
     int J = 0;
     double tnorm = 0.0;
     if (ASYNC && warp == NW - 1) {
