@@ -18,6 +18,9 @@
 // chain-call at m = 100 (~3% of a round).
 #pragma once
 #include "chord2.cuh"
+#ifndef SW_TAIL_CTAS
+#define SW_TAIL_CTAS 3  // K2c CTAs per SM (L packed: ~49 KB of shared memory each at m = 100)
+#endif
 #include "chol_inv.cuh"
 
 namespace sw {
@@ -159,7 +162,7 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
                 for (int i = T.warp; i < mdp; i += T.nwarps)
                     for (int jx = T.lane; jx < mdp; jx += 32) {
                         Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
-                        if (jx <= i) Lw[i * ld + jx] = Gd[i * ld + jx];
+                        if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];  // packed lower rows (tail_kernel)
                     }
             }
         }
@@ -342,9 +345,36 @@ __device__ __forceinline__ void back_solve_lt(const Team& T, const double* G, in
     }
 }
 
+// back_solve_lt with L packed by rows (L[i][j] at pk(i, j), j <= i)
+__device__ __forceinline__ void back_solve_lt_packed(const Team& T, const double* Lp, int mdp, double* zz, double* yy,
+                                                     const double* rdiag) {
+    for (int kb = (mdp >> 3) - 1; kb >= 0; --kb) {
+        const int k0 = kb * 8;
+        if (T.warp == 0) {
+            const int r = T.lane;
+            double zr = (r < 8) ? zz[k0 + r] : 0.0;
+#pragma unroll
+            for (int c = 7; c >= 0; --c) {
+                const double yc = __shfl_sync(0xffffffffu, zr, c) * rdiag[k0 + c];
+                if (r == c) zr = yc;
+                else if (r < c) zr -= Lp[pk(k0 + c, k0 + r)] * yc;
+            }
+            if (r < 8) yy[k0 + r] = zr;
+        }
+        __syncthreads();
+        for (int i = T.tid; i < k0; i += T.nthr) {
+            double acc = zz[i];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc -= Lp[pk(k0 + c, i)] * yy[k0 + c];
+            zz[i] = acc;
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- K2c
 template <int NT>
-__global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
+__global__ void __launch_bounds__(NT, SW_TAIL_CTAS) tail_kernel(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
     T.tid = threadIdx.x;
@@ -355,11 +385,11 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
     __shared__ double red[64];
     __shared__ int sh_i[8];
     __shared__ double sh_d[16];
-    const int m = P.m, n = P.n, ld = P.ld;
+    const int m = P.m, n = P.n;
     const int mp = (m + 7) & ~7;
     const int vl = mp + 8;
-    double* G = smem_dyn;  // L (lower)
-    double* vec = G + (size_t)mp * ld;
+    double* G = smem_dyn;  // L (packed lower rows)
+    double* vec = G + (((size_t)mp * (mp + 1) / 2 + 1) & ~(size_t)1);
     double* zz = vec + 0 * vl;
     double* yy = vec + 1 * vl;
     double* hh = vec + 2 * vl;
@@ -392,8 +422,8 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
             // L (lower rows, 16-byte segments [0, i+1]) into shared memory asynchronously
             const int mdp = (md + 7) & ~7;
             const double* Lw = P.wL + (size_t)slot * P.w_mstride;
-            for (int i = T.warp; i < mdp; i += T.nwarps)
-                for (int c2 = T.lane; 2 * c2 <= i; c2 += 32) cp_async16(G + i * ld + 2 * c2, Lw + i * ld + 2 * c2);
+            const int lp = mdp * (mdp + 1) / 2;
+            for (int c2 = T.tid; 2 * c2 < lp; c2 += T.nthr) cp_async16(G + 2 * c2, Lw + 2 * c2);
             for (int i = T.tid; i < mdp; i += T.nthr) {
                 zz[i] = S[S_VEC + 3 * vl + i];
                 rdiag[i] = S[S_VEC + 2 * vl + i];
@@ -412,7 +442,7 @@ __global__ void __launch_bounds__(NT, 2) tail_kernel(ChordParams P) {
             cp_async_wait_all();
             __syncthreads();
             PROF_MARK(5);
-            back_solve_lt(T, G, ld, mdp, zz, yy, rdiag);  // y = L^{-T} z
+            back_solve_lt_packed(T, G, mdp, zz, yy, rdiag);  // y = L^{-T} z
             PROF_MARK(6);
             if (T.warp == 0) {
                 if (defl) {  // y = H [ -b^T yh / a ; yh ]

@@ -309,7 +309,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         ctx->k2_split = 1;
         ctx->f_smem = f_smem;
         ctx->l_smem = sizeof(double) * ((size_t)mp * ctx->ld + (size_t)NVEC2 * (mp + 8) + 64);  // Q + vectors
-        ctx->t_smem = sizeof(double) * ((size_t)mp * ctx->ld + 5 * (size_t)(mp + 8) + 64);
+        ctx->t_smem = sizeof(double) * ((((size_t)mp * (mp + 1) / 2 + 1) & ~(size_t)1) + 5 * (size_t)(mp + 8) + 64);
         int of = 0, ol = 0, ot = 0;
 #define SW_SPLIT_SETUP(NT_, KC_)                                                                                     \
     CK(cudaFuncSetAttribute(factor_kernel<NT_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->f_smem));     \
