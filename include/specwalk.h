@@ -15,6 +15,13 @@
  * - The library never falls back to the CPU: without a usable CUDA device
  *   spec_create fails with SPEC_ECUDA.
  * - Calls on one context are not re-entrant; distinct contexts are independent.
+ * - Between walk_begin and walk_end the resumable walk owns the context's chain
+ *   buffers: every other call that uses them (boundary_oracle*, hmc_oracle,
+ *   walk_sample*, walk_trace, volume, expectation, spec_set_objective,
+ *   spec_set_ball, walk_begin) returns SPEC_EINVAL until walk_end.
+ * - Multi-rank (spec_set_comm): a failure on one rank inside volume,
+ *   expectation or walk_sample's moment reduction is exchanged through the
+ *   allgather, so every rank returns the failing rank's code together.
  * - Layouts are row-major.  n = ambient dimension, m = matrix size of the LMI.
  * - A "boundary-oracle call" (the unit of BASELINE.json's metric) is one chord
  *   solve (Alg. 2) plus, if the segment ends on a dense-block hit,
@@ -106,7 +113,10 @@ int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const dou
  * quadratic pencil (interior start) or on the sqrt(t)-deflated symmetric
  * quartic (u != NULL: x on the dense boundary with unit kernel u).
  * Outputs as boundary_oracle (no t_minus); normal is the outward normal at
- * the hit.  EINVAL without an objective or T <= 0. */
+ * the hit.  A line whose Weyl stepping reaches the iteration cap (60) without
+ * converging gets t_plus = NaN, normal NaN, binding SPEC_BIND_NONE (the call
+ * still returns SPEC_OK; spec_last_error() names the count).
+ * EINVAL without an objective or T <= 0. */
 int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, double T,
                double* t_plus, double* normal, double* kernel, int32_t* binding);
 
@@ -134,6 +144,9 @@ typedef struct spec_walk_stats {
     int64_t steps;
     int64_t rounds;      /* scheduler rounds (one oracle call per active chain) */
     double device_ms;    /* CUDA-event time of the walk on the context stream */
+    int64_t capped;      /* HMC-r steps rejected because the Weyl stepping of a chord reached
+                            its iteration cap (60) before converging: the crossing time is then
+                            only bounded below, so the step is rejected (never silent) */
 } spec_walk_stats;
 
 /* walk_sample -- run p->chains independent chains for p->steps steps each

@@ -294,7 +294,10 @@ def walk(lmi: Lmi, kind: int, seed: int, chain_begin: int, chain_end: int, steps
 
 
 def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_refl: int,
-          x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK) -> dict:
+          x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, stop: bool = False) -> dict:
+    """First max_refl reflections of one chain.  stop=True ends the walk right after the last
+    record (orc_trace; calls = None), else the step of the last record is completed
+    (orc_trace_stats; calls = every oracle call made)."""
     n = lmi.n
     x0 = _arr(np.zeros(n) if x0 is None else x0)
     p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
@@ -305,13 +308,18 @@ def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho:
     bind = np.zeros(max_refl, dtype=np.int32)
     nrec = C.c_int64()
     st = _Stats()
-    rc = lib().orc_trace_stats(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
-                               bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec), C.byref(st))
+    if stop:
+        rc = lib().orc_trace(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
+                             bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec))
+    else:
+        rc = lib().orc_trace_stats(lmi._h, C.byref(p), chain, _p(x0), max_refl, _p(hit), _p(t), _p(w), _p(va),
+                                   bind.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nrec), C.byref(st))
     if rc:
         raise ValueError(f"orc_trace rc={rc}")
     k = nrec.value
     # calls: every boundary-oracle call of the walk (it finishes the step of the last record)
-    return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k], calls=int(st.calls))
+    return dict(hit_x=hit[:k], t=t[:k], w=w[:k], v_after=va[:k], binding=bind[:k],
+                calls=None if stop else int(st.calls))
 
 
 def replay(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_calls: int,

@@ -988,6 +988,7 @@ typedef struct {
     int64_t max_refl, nrec;
     double *hit_x, *t, *w, *v_after;
     int32_t* binding;
+    int stop; /* end the walk right after the max_refl-th record (no arithmetic change) */
 } trace_rec;
 
 /* One step of the Billiard walk (Alg. 5; readings R4, R5) or
@@ -1083,6 +1084,7 @@ static int walk_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain,
             memcpy(tr->v_after + k * n, W->v, sizeof(double) * n);
             tr->binding[k] = r->binding;
             tr->nrec += 1;
+            if (tr->stop && tr->nrec >= tr->max_refl) return 6; /* trace complete */
         }
     }
 reject:
@@ -1179,10 +1181,15 @@ int orc_replay(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const 
     return rc;
 }
 
+/* orc_trace stops right after the max_refl-th reflection is recorded (the records are
+   those of orc_trace_stats; only the unrecorded remainder of that step is skipped) */
+static int trace_impl(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
+                      int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
+                      int32_t* binding, int64_t* nrec, orc_stats* st_out, int stop);
 int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
               int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
               int32_t* binding, int64_t* nrec) {
-    return orc_trace_stats(L, p, chain, x0, max_refl, hit_x, t, w, v_after, binding, nrec, NULL);
+    return trace_impl(L, p, chain, x0, max_refl, hit_x, t, w, v_after, binding, nrec, NULL, 1);
 }
 
 /* as orc_trace; st_out (may be NULL) receives the walk statistics: the walk always
@@ -1191,16 +1198,26 @@ int orc_trace(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const d
 int orc_trace_stats(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
                     int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
                     int32_t* binding, int64_t* nrec, orc_stats* st_out) {
+    return trace_impl(L, p, chain, x0, max_refl, hit_x, t, w, v_after, binding, nrec, st_out, 0);
+}
+
+static int trace_impl(const orc_lmi* L, const orc_walk_params* p, int64_t chain, const double* x0,
+                      int64_t max_refl, double* hit_x, double* t, double* w, double* v_after,
+                      int32_t* binding, int64_t* nrec, orc_stats* st_out, int stop) {
     int n = L->n;
     walk_ws W;
     ws_init(&W, L);
     orc_stats st = {0, 0, 0, 0, 0, 0};
-    trace_rec tr = {max_refl, 0, hit_x, t, w, v_after, binding};
+    trace_rec tr = {max_refl, 0, hit_x, t, w, v_after, binding, stop};
     memcpy(W.x, x0, sizeof(double) * n);
     orc_eval_block(L, 0, W.x, W.F);
     int rc = 0;
     for (int64_t s = 0; s < p->steps && tr.nrec < max_refl; ++s) {
         rc = walk_step(L, p, (uint32_t)chain, (uint32_t)s, &W, &st, &tr);
+        if (rc == 6) {
+            rc = 0;
+            break;
+        }
         if (rc) break;
     }
     *nrec = tr.nrec;

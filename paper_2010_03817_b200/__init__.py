@@ -79,6 +79,7 @@ class WalkStats(C.Structure):
     _fields_ = [
         ("calls", C.c_int64), ("reflections", C.c_int64), ("rejects", C.c_int64), ("degenerates", C.c_int64),
         ("failures", C.c_int64), ("steps", C.c_int64), ("rounds", C.c_int64), ("device_ms", C.c_double),
+        ("capped", C.c_int64),
     ]
 
     def as_dict(self) -> dict:

@@ -31,6 +31,7 @@ struct ChordParams {
     long long* nrefl;
     int* nrej;
     int* ndeg;
+    int* ncap;  // HMC-r steps rejected because Weyl stepping hit its iteration cap
     const double* lo;
     const double* hi;
     const double* ball_c;

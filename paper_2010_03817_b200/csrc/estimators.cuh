@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256) ball_sample_kernel(int count, long long b
 template <int NT>
 __global__ void __launch_bounds__(NT) membership_kernel(int count, int n, int np, int m, int mt, int mtp, int ld,
                                                         const double* X, const double* AX, const double* lo,
-                                                        const double* hi, int* inside) {
+                                                        const double* hi, int* inside, double* gscr,
+                                                        long long gstride) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
     T.tid = threadIdx.x;
@@ -63,8 +64,9 @@ __global__ void __launch_bounds__(NT) membership_kernel(int count, int n, int np
     __shared__ double red[64];
     __shared__ int flag;
     const int mp = (m + 7) & ~7;
-    double* G = smem_dyn;
-    double* rdiag = G + (size_t)mp * ld;
+    // A(x_j) in shared memory, or (large m, gscr != NULL) in this CTA's global scratch slice
+    double* G = gscr ? gscr + (size_t)blockIdx.x * gstride : smem_dyn;
+    double* rdiag = gscr ? smem_dyn : G + (size_t)mp * ld;
     for (int s = blockIdx.x; s < count; s += gridDim.x) {
         const double* x = X + (size_t)s * np;
         bool ok = true;

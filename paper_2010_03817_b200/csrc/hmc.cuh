@@ -20,6 +20,10 @@
 
 namespace sw {
 
+// Weyl-stepping iteration cap of one HMC-r chord (V6: ~4 iterations; reaching it is counted
+// in spec_walk_stats.capped and the step is rejected)
+constexpr int HMC_MAX_IT = 60;
+
 // smallest positive root of alpha + beta t + gamma t^2 (alpha >= 0); on_face:
 // alpha is exactly 0 (the face just left), the root t = 0 is excluded.
 __device__ __forceinline__ double first_pos_root2(double alpha, double beta, double gamma, bool on_face) {
@@ -78,8 +82,8 @@ __device__ double weyl_step(double a, const double* c, int d) {
 // kernel vector yy (shared memory) -- shared by hmc_kernel and the split tail.
 __device__ __forceinline__ void hmc_finish(const Team& T, const ChordParams& P, int slot, long long gidv, double* x,
                                            double* v, const double* av, double* ax, int bnd, const double* yy,
-                                           double t_dense, bool failed, bool outward, double* red, double* sh_d,
-                                           int* sh_i) {
+                                           double t_dense, bool failed, bool outward, bool capped, double* red,
+                                           double* sh_d, int* sh_i) {
     const int m = P.m, n = P.n;
     const double Tinv = 1.0 / P.Temp;
     {
@@ -115,12 +119,15 @@ __device__ __forceinline__ void hmc_finish(const Team& T, const ChordParams& P, 
         const double tplus = sh_d[0];
         const int bind = sh_i[1];
         if (P.mode == 1) {
+            // a dense hit found with the Weyl iteration cap reached is only a lower bound on
+            // the crossing time: reported as status 3, t+ = NaN, binding none (never silent)
+            const bool cap_hit = capped && bind == 0;
             if (T.tid == 0) {
-                P.o_tplus[slot] = tplus;
+                P.o_tplus[slot] = cap_hit ? __longlong_as_double(0x7ff8000000000000LL) : tplus;
                 P.o_tminus[slot] = 0.0;
-                P.o_binding[slot] = bind;
-                P.o_status[slot] = failed ? 2 : 0;
-                P.flags[slot] = (bind == 0 && !failed) ? CF_NEED_NORMAL : 0;
+                P.o_binding[slot] = cap_hit ? SW_BIND_NONE_DEV : bind;
+                P.o_status[slot] = failed ? 2 : (cap_hit ? 3 : 0);
+                P.flags[slot] = (bind == 0 && !failed && !cap_hit) ? CF_NEED_NORMAL : 0;
             }
             if (P.o_kernel)
                 for (int i = T.tid; i < m; i += T.nthr) P.o_kernel[(size_t)slot * m + i] = (bind == 0) ? yy[i] : 0.0;
@@ -167,6 +174,11 @@ __device__ __forceinline__ void hmc_finish(const Team& T, const ChordParams& P, 
                 if (outward) {
                     reject = end_step = true;
                     if (T.tid == 0) P.ndeg[slot] += 1;
+                } else if (capped) {
+                    // Weyl stepping hit HMC_MAX_IT: s is a lower bound on the root only,
+                    // so the segment cannot be advanced to a boundary point: reject the step
+                    reject = end_step = true;
+                    if (T.tid == 0) P.ncap[slot] += 1;
                 } else {
                     double* yh = P.Yh + (size_t)slot * P.mtp;
                     for (int i = T.warp; i < m; i += T.nwarps)
@@ -347,10 +359,11 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
 
         // ---- monotone Weyl stepping on G~(s)
         double s = 0.0;
-        bool failed = false, hit = false;
+        bool failed = false, hit = false, capped = false;
         int iters = 0;
         if (!outward) {
-            for (int it = 0; it < 60; ++it) {
+            bool ended = false;  // converged, Cholesky breakdown, or no root
+            for (int it = 0; it < HMC_MAX_IT; ++it) {
                 ++iters;
                 // Kf = G~(s) (Horner), Cholesky
                 for (int i = T.warp; i < mp; i += T.nwarps)
@@ -363,6 +376,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
                 bool ok = cholesky_blocked(T, Kf, mp, ld, rdiag, &sh_i[2]);
                 if (!ok) {
                     if (it == 0) failed = true;  // start not interior
+                    ended = true;
                     break;                       // rounding past the root: keep s (the last safe point)
                 }
                 // N1 = K^{-1} G~'(s) K^{-T}
@@ -425,15 +439,18 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
                 __syncthreads();
                 if (!(h < SW_INF)) {
                     s = SW_INF;
+                    ended = true;
                     break;
                 }
                 s += h;
                 if (h <= 1e-15 * s) {
                     hit = true;
+                    ended = true;
                     break;
                 }
             }
             if (s < SW_INF) hit = true;
+            capped = !ended;
         }
         if (P.prof && T.tid == 0) atomicAdd(&P.prof[17], (unsigned long long)iters);
         PROF_MARK(4);
@@ -455,7 +472,7 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
         }
         __syncthreads();
         double t_dense = outward ? 0.0 : (hit ? (d == 4 ? s * s : s) : SW_INF);
-        hmc_finish(T, P, slot, gidv, x, v, av, ax, bnd, yy, t_dense, failed, outward, red, sh_d, sh_i);
+        hmc_finish(T, P, slot, gidv, x, v, av, ax, bnd, yy, t_dense, failed, outward, capped, red, sh_d, sh_i);
         PROF_MARK(8);
     }
 }

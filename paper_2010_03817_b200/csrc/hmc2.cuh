@@ -31,8 +31,7 @@ namespace sw {
 
 // per-slot Weyl state (P.wH, H_NS doubles per slot)
 enum : int { H_S = 0, H_D = 1, H_IT = 2, H_ST = 3, H_C2 = 4, H_C3 = 5, H_C4 = 6, H_BH = 7, H_NS = 8 };
-enum : int { HS_ITER = 0, HS_HIT = 1, HS_FAILED = 2, HS_INF = 3, HS_OUTWARD = 4 };
-constexpr int HMC_MAX_IT = 60;  // as hmc_kernel
+enum : int { HS_ITER = 0, HS_HIT = 1, HS_FAILED = 2, HS_INF = 3, HS_OUTWARD = 4, HS_CAPPED = 5 };
 
 // X_w <- L^{-1} X_w for nv vectors (stride vl) with L lower in G and the inverse 8 x 8
 // diagonal blocks Lv (cholesky_inv_blocked_la): one warp per vector, left-looking over
@@ -364,8 +363,12 @@ __global__ void hmc_weyl_kernel(ChordParams P) {
         }
         const double s = H[H_S] + h;
         H[H_S] = s;
-        if (h <= 1e-15 * s || it >= HMC_MAX_IT) {
+        if (h <= 1e-15 * s) {
             H[H_ST] = (double)HS_HIT;
+            continue;
+        }
+        if (it >= HMC_MAX_IT) {  // not converged: s is a lower bound only (rejected, counted)
+            H[H_ST] = (double)HS_CAPPED;
             continue;
         }
         const int q = atomicAdd(P.nxt_count, 1);
@@ -448,7 +451,7 @@ __global__ void __launch_bounds__(NT, 2) hmc_tail_kernel(ChordParams P) {
         }
         __syncthreads();
         const double t_dense = outward ? 0.0 : (hit ? (d == 4 ? s * s : s) : SW_INF);
-        hmc_finish(T, P, slot, gidv, x, v, av, ax, bnd, yy, t_dense, failed, outward, red, sh_d, sh_i);
+        hmc_finish(T, P, slot, gidv, x, v, av, ax, bnd, yy, t_dense, failed, outward, st == HS_CAPPED, red, sh_d, sh_i);
     }
 }
 

@@ -44,11 +44,20 @@ static int fail(int code, const std::string& msg) {
 
 static int roundup(int a, int b) { return (a + b - 1) / b * b; }
 
+struct spec_ctx;
+static bool walk_is_active(spec_ctx* ctx);
+#define SW_NOT_DURING_WALK(ctx)                                                                  \
+    do {                                                                                        \
+        if (walk_is_active(ctx))                                                                \
+            return fail(SPEC_EINVAL, "a resumable walk is in progress (call walk_end first)"); \
+    } while (0)
+
 struct ChainBuf {
     long long cap = 0;
     double *X = nullptr, *Xs = nullptr, *V = nullptr, *AX = nullptr, *AXs = nullptr, *AV = nullptr, *Yh = nullptr,
            *U = nullptr, *Gn = nullptr, *ell = nullptr, *tlast = nullptr;
-    int *steps_done = nullptr, *refl = nullptr, *bound = nullptr, *flags = nullptr, *nrej = nullptr, *ndeg = nullptr;
+    int *steps_done = nullptr, *refl = nullptr, *bound = nullptr, *flags = nullptr, *nrej = nullptr, *ndeg = nullptr,
+        *ncap = nullptr;
     int* jlast = nullptr;
     double *wM = nullptr, *wL = nullptr, *wS = nullptr;  // K2 split work buffers
     long long *calls = nullptr, *nrefl = nullptr;
@@ -57,6 +66,19 @@ struct ChainBuf {
     long long* gid = nullptr;
 };
 
+struct OracleBuf {
+    long long cap = 0;
+    int m_cap = 0;
+    double *x = nullptr, *v = nullptr, *u = nullptr;            // host-input staging (batch x n, batch x m)
+    double *tm = nullptr, *tp = nullptr, *nrm = nullptr, *ker = nullptr;
+    int *bind = nullptr, *stat = nullptr;
+};
+static void free_obuf(OracleBuf& o) {
+    void* ps[] = {o.x, o.v, o.u, o.tm, o.tp, o.nrm, o.ker, o.bind, o.stat};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    o = OracleBuf();
+}
 // K5 split work buffers (hmc2.cuh), grown with the chain capacity on first HMC use
 struct HmcBuf {
     long long cap = 0;
@@ -86,6 +108,7 @@ struct spec_ctx {
     size_t hf_smem = 0, hl_smem = 0, ht_smem = 0;
     HmcBuf hb;
     double* ball_c = nullptr;
+    double* c0 = nullptr;  // centre of the exact ball samples of volume() (n doubles)
     double ball_r = 0.0;
     int has_ball = 0;
     double amax = 0.0;
@@ -112,11 +135,12 @@ struct spec_ctx {
     void* walk = nullptr;  // WalkRun*
     spec_comm comm{nullptr, 0, 1, nullptr};
     int has_comm = 0;
+    void* obuf = nullptr;  // OracleBuf*
 };
 
 static void free_chains(ChainBuf& b) {
     void* ps[] = {b.X, b.Xs, b.V, b.AX, b.AXs, b.AV, b.Yh, b.U, b.Gn, b.ell, b.tlast, b.steps_done, b.refl, b.bound,
-                  b.flags, b.nrej, b.ndeg, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid, b.jlast, b.wM, b.wL, b.wS};
+                  b.flags, b.nrej, b.ndeg, b.ncap, b.calls, b.nrefl, b.list, b.list2, b.nlist, b.counters, b.gid, b.jlast, b.wM, b.wL, b.wS};
     for (void* p : ps)
         if (p) cudaFree(p);
     b = ChainBuf();
@@ -144,7 +168,7 @@ static int ensure_chains(spec_ctx* ctx, long long C) {
     if (e == cudaSuccess) e = zalloc(&b.ptr, (size_t)(cnt));
     ZA(X, cap * np) ZA(Xs, cap * np) ZA(V, cap * np) ZA(Gn, cap * np) ZA(AX, cap * mtp) ZA(AXs, cap * mtp)
     ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(tlast, cap) ZA(steps_done, cap) ZA(refl, cap)
-    ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
+    ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(ncap, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
     ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap) ZA(jlast, cap)
     if (ctx->k2_split) {
         const size_t mp = (size_t)roundup(ctx->m, 8);
@@ -160,6 +184,8 @@ static int ensure_chains(spec_ctx* ctx, long long C) {
     return SPEC_OK;
 }
 
+static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const double* cube_lo, const double* cube_hi,
+                       int device);
 extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo, const double* cube_hi,
                            int device, spec_ctx** out) {
     if (!out) return fail(SPEC_EINVAL, "out is NULL");
@@ -185,6 +211,21 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
         return fail(SPEC_ECUDA, "no CUDA device (the library has no CPU fallback)");
     }
     spec_ctx* ctx = new spec_ctx();
+    ctx->obuf = new OracleBuf();
+    int rc = create_impl(ctx, n, m, A, cube_lo, cube_hi, device);
+    if (rc) {
+        std::string msg = g_err;
+        spec_destroy(ctx);  // frees whatever was allocated before the failure
+        g_err = msg;
+        return rc;
+    }
+    *out = ctx;
+    return SPEC_OK;
+}
+
+static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const double* cube_lo, const double* cube_hi,
+                       int device) {
+    const size_t mm = (size_t)m * m;
     if (device < 0) cudaGetDevice(&device);
     ctx->dev = device;
     CK(cudaSetDevice(device));
@@ -231,6 +272,7 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     CK(zalloc(&ctx->c, ctx->np));
     CK(zalloc(&ctx->Ac, ctx->mtp));
     CK(zalloc(&ctx->ball_c, ctx->np));
+    CK(zalloc(&ctx->c0, ctx->np));
     CK(zalloc(&ctx->dstats, 8));
     if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 32));
     // K2 variant: M register-resident (m <= 128) with matrices in shared memory,
@@ -333,7 +375,6 @@ extern "C" int spec_create(int n, int m, const double* A, const double* cube_lo,
     }
     ctx->lsave_stride = (long long)mp * ctx->ld;
     CK(zalloc(&ctx->lsave, (size_t)ctx->lsave_stride * ctx->chord_grid_max));
-    *out = ctx;
     return SPEC_OK;
 }
 
@@ -345,7 +386,11 @@ extern "C" int spec_destroy(spec_ctx* ctx) {
     cudaSetDevice(ctx->dev);
     free_chains(ctx->cb);
     free_hmc_bufs(ctx->hb);
-    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
+    if (ctx->obuf) {
+        free_obuf(*(OracleBuf*)ctx->obuf);
+        delete (OracleBuf*)ctx->obuf;
+    }
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->c0, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -366,6 +411,7 @@ static void launch_gemm_av(spec_ctx* ctx, const double* Arows, const int* list, 
                            int count_host, double* out, const double* bias);
 extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
     if (!ctx || !c) return fail(SPEC_EINVAL, "null argument");
+    if (walk_is_active(ctx)) return fail(SPEC_EINVAL, "a resumable walk is in progress (call walk_end first)");
     double s = 0.0;
     for (int i = 0; i < ctx->n; ++i) s += c[i] * c[i];
     if (!(s > 0.0) || !std::isfinite(s)) return fail(SPEC_EINVAL, "|c| must be finite and > 0");
@@ -380,6 +426,7 @@ extern "C" int spec_set_objective(spec_ctx* ctx, const double* c) {
 
 extern "C" int spec_set_ball(spec_ctx* ctx, const double* center, double radius) {
     if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    if (walk_is_active(ctx)) return fail(SPEC_EINVAL, "a resumable walk is in progress (call walk_end first)");
     CK(cudaSetDevice(ctx->dev));
     if (!(radius > 0.0)) {
         ctx->has_ball = 0;
@@ -416,7 +463,7 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.mode = mode;
     P.AV = b.AV; P.AX = b.AX; P.AXs = b.AXs; P.Yh = b.Yh; P.X = b.X; P.Xs = b.Xs; P.V = b.V; P.U = b.U;
     P.ell = b.ell; P.steps_done = b.steps_done; P.refl = b.refl; P.bound = b.bound; P.flags = b.flags;
-    P.calls = b.calls; P.nrefl = b.nrefl; P.nrej = b.nrej; P.ndeg = b.ndeg;
+    P.calls = b.calls; P.nrefl = b.nrefl; P.nrej = b.nrej; P.ndeg = b.ndeg; P.ncap = b.ncap;
     P.lo = ctx->has_cube ? ctx->lo : nullptr;
     P.hi = ctx->has_cube ? ctx->hi : nullptr;
     P.ball_c = ctx->ball_c; P.ball_r = ctx->ball_r; P.has_ball = ctx->has_ball;
@@ -633,10 +680,32 @@ static NormalParams normal_params(spec_ctx* ctx, int mode) {
 }
 
 // ---------------------------------------------------------------- boundary_oracle
+// Device staging of one boundary_oracle / hmc_oracle batch: grown with the batch and kept in the
+// context (no cudaMalloc / cudaFree per call); freed by spec_destroy.
+static int ensure_obuf(spec_ctx* ctx, long long B) {
+    OracleBuf& o = *(OracleBuf*)ctx->obuf;
+    if (B <= o.cap) return SPEC_OK;
+    free_obuf(o);
+    const size_t n = ctx->n, m = ctx->m;
+    cudaError_t e = cudaSuccess;
+#define ZA(ptr, cnt) \
+    if (e == cudaSuccess) e = zalloc(&o.ptr, (size_t)(cnt));
+    ZA(x, B * n) ZA(v, B * n) ZA(u, B * m) ZA(tm, B) ZA(tp, B) ZA(nrm, B * n) ZA(ker, B * m) ZA(bind, B) ZA(stat, B)
+#undef ZA
+    if (e != cudaSuccess) {
+        free_obuf(o);
+        cudaGetLastError();
+        return fail(SPEC_ENOMEM, std::string("oracle buffers: ") + cudaGetErrorString(e));
+    }
+    o.cap = B;
+    return SPEC_OK;
+}
+
 static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const double* dv, const double* du,
                        double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
-                       bool host_out, int* status_out, double hmcT = 0.0) {
+                       bool host_out, int* status_out, int* capped_out, double hmcT = 0.0) {
     ChainBuf& b = ctx->cb;
+    OracleBuf& o = *(OracleBuf*)ctx->obuf;
     const int B = (int)batch;
     const int n = ctx->n, np = ctx->np, m = ctx->m;
     // pad x, v into the chain layout
@@ -651,17 +720,10 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     launch_gemm_av(ctx, b.X, nullptr, nullptr, B, b.AX, ctx->a0);
     launch_gemm_av(ctx, b.V, nullptr, nullptr, B, b.AV, nullptr);
     // K2 in oracle mode
-    double *o_tm, *o_tp, *o_nrm, *o_ker = nullptr;
-    int *o_bind, *o_stat;
-    CK(cudaMalloc(&o_tm, sizeof(double) * B));
-    CK(cudaMalloc(&o_tp, sizeof(double) * B));
-    CK(cudaMalloc(&o_nrm, sizeof(double) * (size_t)B * n));
-    if (kernel) CK(cudaMalloc(&o_ker, sizeof(double) * (size_t)B * m));
-    CK(cudaMalloc(&o_bind, sizeof(int) * B));
-    CK(cudaMalloc(&o_stat, sizeof(int) * B));
     ChordParams P = chord_params(ctx, 1);
     P.count_host = B;
-    P.o_tminus = o_tm; P.o_tplus = o_tp; P.o_kernel = o_ker; P.o_binding = o_bind; P.o_status = o_stat;
+    P.o_tminus = o.tm; P.o_tplus = o.tp; P.o_kernel = kernel ? o.ker : nullptr; P.o_binding = o.bind;
+    P.o_status = o.stat;
     if (hmcT > 0.0) {
         P.Temp = hmcT;
         int rc = launch_hmc(ctx, P, B);
@@ -673,24 +735,27 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     launch_gemm_normal(ctx, nullptr, nullptr, B);
     NormalParams Q = normal_params(ctx, 1);
     Q.count_host = B;
-    Q.o_binding = o_bind; Q.o_tplus = o_tp; Q.Vin = b.V; Q.o_normal = o_nrm;
+    Q.o_binding = o.bind; Q.o_tplus = o.tp; Q.Vin = b.V; Q.o_normal = o.nrm;
     normal_reflect_kernel<<<(B + 7) / 8, 256, 0, ctx->stream>>>(Q);
     ctx->launches++;
     CK(cudaGetLastError());
     cudaMemcpyKind kind = host_out ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    CK(cudaMemcpyAsync(t_minus, o_tm, sizeof(double) * B, kind, ctx->stream));
-    CK(cudaMemcpyAsync(t_plus, o_tp, sizeof(double) * B, kind, ctx->stream));
-    CK(cudaMemcpyAsync(normal, o_nrm, sizeof(double) * (size_t)B * n, kind, ctx->stream));
-    if (kernel) CK(cudaMemcpyAsync(kernel, o_ker, sizeof(double) * (size_t)B * m, kind, ctx->stream));
-    CK(cudaMemcpyAsync(binding, o_bind, sizeof(int) * B, kind, ctx->stream));
+    CK(cudaMemcpyAsync(t_minus, o.tm, sizeof(double) * B, kind, ctx->stream));
+    CK(cudaMemcpyAsync(t_plus, o.tp, sizeof(double) * B, kind, ctx->stream));
+    CK(cudaMemcpyAsync(normal, o.nrm, sizeof(double) * (size_t)B * n, kind, ctx->stream));
+    if (kernel) CK(cudaMemcpyAsync(kernel, o.ker, sizeof(double) * (size_t)B * m, kind, ctx->stream));
+    CK(cudaMemcpyAsync(binding, o.bind, sizeof(int) * B, kind, ctx->stream));
     std::vector<int> st(B);
-    CK(cudaMemcpyAsync(st.data(), o_stat, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(st.data(), o.stat, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(o_tm); cudaFree(o_tp); cudaFree(o_nrm); cudaFree(o_bind); cudaFree(o_stat);
-    if (o_ker) cudaFree(o_ker);
     int worst = 0;
-    for (int i = 0; i < B; ++i) worst = std::max(worst, st[i] == 2 ? 2 : 0);
+    int ncapped = 0;
+    for (int i = 0; i < B; ++i) {
+        worst = std::max(worst, st[i] == 2 ? 2 : 0);
+        ncapped += st[i] == 3;
+    }
     if (status_out) *status_out = worst;
+    if (capped_out) *capped_out = ncapped;
     return SPEC_OK;
 }
 
@@ -698,38 +763,34 @@ static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const dou
                         double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
                         bool host, double hmcT = 0.0) {
     if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    if (walk_is_active(ctx)) return fail(SPEC_EINVAL, "a resumable walk is in progress (call walk_end first)");
     if (batch < 0 || batch > (1LL << 30)) return fail(SPEC_EINVAL, "bad batch");
     if (batch == 0) return SPEC_OK;
     if (!x || !v || !t_minus || !t_plus || !normal || !binding) return fail(SPEC_EINVAL, "null buffer");
+    if (hmcT > 0.0 && !ctx->has_obj) return fail(SPEC_EINVAL, "hmc_oracle needs spec_set_objective");
     CK(cudaSetDevice(ctx->dev));
     int rc = ensure_chains(ctx, batch);
     if (rc) return rc;
-    const int n = ctx->n, m = ctx->m;
-    const double *dx = x, *dv = v, *du = u;
-    double *bx = nullptr, *bv = nullptr, *bu = nullptr;
-    if (host) {
-        CK(cudaMalloc(&bx, sizeof(double) * batch * n));
-        CK(cudaMalloc(&bv, sizeof(double) * batch * n));
-        CK(cudaMemcpyAsync(bx, x, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(bv, v, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
-        if (u) {
-            CK(cudaMalloc(&bu, sizeof(double) * batch * m));
-            CK(cudaMemcpyAsync(bu, u, sizeof(double) * batch * m, cudaMemcpyHostToDevice, ctx->stream));
-        }
-        dx = bx; dv = bv; du = bu;
-    }
-    int status = 0;
+    rc = ensure_obuf(ctx, batch);
+    if (rc) return rc;
     if (hmcT > 0.0) {
-        if (!ctx->has_obj) return fail(SPEC_EINVAL, "hmc_oracle needs spec_set_objective");
         rc = ensure_hmc(ctx);
         if (rc) return rc;
     }
-    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status, hmcT);
-    if (bx) cudaFree(bx);
-    if (bv) cudaFree(bv);
-    if (bu) cudaFree(bu);
+    OracleBuf& o = *(OracleBuf*)ctx->obuf;
+    const int n = ctx->n, m = ctx->m;
+    const double *dx = x, *dv = v, *du = u;
+    if (host) {
+        CK(cudaMemcpyAsync(o.x, x, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(o.v, v, sizeof(double) * batch * n, cudaMemcpyHostToDevice, ctx->stream));
+        if (u) CK(cudaMemcpyAsync(o.u, u, sizeof(double) * batch * m, cudaMemcpyHostToDevice, ctx->stream));
+        dx = o.x; dv = o.v; du = u ? o.u : nullptr;
+    }
+    int status = 0, capped = 0;
+    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status, &capped, hmcT);
     if (rc) return rc;
     if (status == 2) return fail(SPEC_EPRECOND, "some x is not interior (Cholesky of F(x) failed)");
+    if (capped) g_err = std::to_string(capped) + " line(s): Weyl iteration cap reached (t_plus = NaN)";
     return SPEC_OK;
 }
 
@@ -787,6 +848,7 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     CK(cudaMemsetAsync(b.flags, 0, sizeof(int) * C, ctx->stream));
     CK(cudaMemsetAsync(b.nrej, 0, sizeof(int) * C, ctx->stream));
     CK(cudaMemsetAsync(b.ndeg, 0, sizeof(int) * C, ctx->stream));
+    CK(cudaMemsetAsync(b.ncap, 0, sizeof(int) * C, ctx->stream));
     CK(cudaMemsetAsync(b.calls, 0, sizeof(long long) * C, ctx->stream));
     CK(cudaMemsetAsync(b.nrefl, 0, sizeof(long long) * C, ctx->stream));
     CK(cudaMemsetAsync(b.jlast, 0, sizeof(int) * C, ctx->stream));
@@ -943,7 +1005,7 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
     const int C = (int)W.p.chains;
     CK(cudaMemsetAsync(ctx->dstats, 0, sizeof(long long) * 8, ctx->stream));
     stats_kernel<<<std::min((C + 255) / 256, 1024), 256, 0, ctx->stream>>>(C, b.calls, b.nrefl, b.nrej, b.ndeg,
-                                                                           b.flags, b.steps_done, ctx->dstats);
+                                                                           b.ncap, b.flags, b.steps_done, ctx->dstats);
     ctx->launches++;
     long long hs[8];
     CK(cudaMemcpyAsync(hs, ctx->dstats, sizeof(long long) * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -955,6 +1017,7 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
         st->degenerates = hs[3];
         st->failures = hs[4];
         st->steps = hs[5];
+        st->capped = hs[6];
         st->rounds = W.rounds;
         st->device_ms = W.ms;
     }
@@ -1001,15 +1064,13 @@ static int walk_collect_stats(spec_ctx* ctx, spec_walk_stats* st) {
 static int run_walk(spec_ctx* ctx, const spec_walk_params* p, const double* dx0, int x0_per_chain,
                     const long long* dgid, TraceBufs* tr, spec_walk_stats* st) {
     int rc = walk_setup(ctx, p, dx0, x0_per_chain, dgid, tr);
-    if (rc) return rc;
-    rc = walk_do_rounds(ctx, 0);
-    if (rc) return rc;
-    rc = walk_collect_stats(ctx, st);
-    walk_run(ctx).active = false;
+    if (!rc) rc = walk_do_rounds(ctx, 0);
+    if (!rc) rc = walk_collect_stats(ctx, st);
+    walk_run(ctx).active = false;  // also on failure: the context stays usable
     return rc;
 }
 
-static int gather_f64(spec_ctx* ctx, const std::vector<double>& local, std::vector<double>& global);
+static int gather_f64(spec_ctx* ctx, int rc_local, const std::vector<double>& local, std::vector<double>& global);
 static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
     if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC) return fail(SPEC_EINVAL, "unknown walk kind");
@@ -1027,48 +1088,87 @@ static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     return SPEC_OK;
 }
 
-static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain,
-                      double* sum_x, double* sum_xx, double* final_x, spec_walk_stats* st, bool host) {
+// Scoped device allocation (freed on every return path).
+struct DevBuf {
+    void* p = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 1); }
+    template <typename T>
+    T* as() const {
+        return (T*)p;
+    }
+};
+
+// The walk itself (no collective): parameters, x0 upload, rounds to completion.
+static int walk_local(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain, bool host,
+                      spec_walk_stats* local) {
     int rc = check_walk_params(ctx, p);
     if (rc) return rc;
     CK(cudaSetDevice(ctx->dev));
     rc = ensure_chains(ctx, p->chains);
     if (rc) return rc;
-    const int C = (int)p->chains, n = ctx->n, np = ctx->np;
-    double* dx0 = nullptr;
+    const int C = (int)p->chains, n = ctx->n;
+    DevBuf dx0;
     const double* x0d = x0;
     if (x0 && host) {
         size_t cnt = (size_t)(x0_per_chain ? C : 1) * n;
-        CK(cudaMalloc(&dx0, sizeof(double) * cnt));
-        CK(cudaMemcpyAsync(dx0, x0, sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
-        x0d = dx0;
+        CK(dx0.alloc(sizeof(double) * cnt));
+        CK(cudaMemcpyAsync(dx0.p, x0, sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+        x0d = dx0.as<double>();
     }
+    rc = run_walk(ctx, p, x0d, x0_per_chain, nullptr, nullptr, local);
+    CK(cudaStreamSynchronize(ctx->stream));  // x0 staging is read by the walk's first kernels
+    return rc;
+}
+
+// end-point moments of this rank's chains as chunk partials (1024 consecutive global chain ids
+// per chunk, chain order), into part (host)
+static int local_moment_chunks(spec_ctx* ctx, int C, std::vector<double>& part) {
+    const int n = ctx->n, np = ctx->np, nxx = n * (n + 1) / 2;
+    const int CH = 1024;
+    const int nchunk = (C + CH - 1) / CH;
+    const int stride = n + nxx;
+    DevBuf dpart;
+    CK(dpart.alloc(sizeof(double) * (size_t)nchunk * stride));
+    moments_chunk_kernel<<<std::min((nchunk * stride + 255) / 256, 8192), 256, 0, ctx->stream>>>(
+        ctx->cb.X, np, n, C, CH, dpart.as<double>());
+    ctx->launches++;
+    part.assign((size_t)nchunk * stride, 0.0);
+    CK(cudaMemcpyAsync(part.data(), dpart.p, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return SPEC_OK;
+}
+
+static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0, int x0_per_chain,
+                      double* sum_x, double* sum_xx, double* final_x, spec_walk_stats* st, bool host) {
+    SW_NOT_DURING_WALK(ctx);
+    if (!p) return fail(SPEC_EINVAL, "null argument");
+    const bool moments = sum_x || sum_xx;
+    const int n = ctx->n, np = ctx->np, nxx = n * (n + 1) / 2;
+    const int C = (int)p->chains;
     spec_walk_stats local;
-    rc = run_walk(ctx, p, x0d, x0_per_chain, nullptr, nullptr, &local);
-    if (dx0) cudaFree(dx0);
-    if (rc) return rc;
+    memset(&local, 0, sizeof(local));
+    int rc = SPEC_OK;
+    if (moments && ctx->has_comm && (C % 1024 || p->chain_begin % 1024))
+        rc = fail(SPEC_EINVAL, "multi-rank moments need shards of multiples of 1024 chains");
+    if (!rc) rc = walk_local(ctx, p, x0, x0_per_chain, host, &local);
+    if (!rc && local.failures > 0)
+        rc = fail(SPEC_EPRECOND, std::to_string(local.failures) + " chain(s) started outside int S");
     if (st) *st = local;
-    // outputs: end-point moments as chunk partials (1024 consecutive global chain ids
-    // per chunk, chain order), gathered over ranks and summed in global chunk order
-    ChainBuf& b = ctx->cb;
-    const int nxx = n * (n + 1) / 2;
-    if ((sum_x || sum_xx) && ctx->has_comm && (C % 1024 || p->chain_begin % 1024))
-        return fail(SPEC_EINVAL, "multi-rank moments need shards of multiples of 1024 chains");
-    if (sum_x || sum_xx) {
-        const int CH = 1024;
-        const int nchunk = (C + CH - 1) / CH;
-        const int stride = n + nxx;
-        double* dpart;
-        CK(cudaMalloc(&dpart, sizeof(double) * (size_t)nchunk * stride));
-        moments_chunk_kernel<<<std::min((nchunk * stride + 255) / 256, 8192), 256, 0, ctx->stream>>>(
-            b.X, np, n, C, CH, dpart);
-        ctx->launches++;
-        std::vector<double> part((size_t)nchunk * stride), allp;
-        CK(cudaMemcpyAsync(part.data(), dpart, sizeof(double) * part.size(), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(dpart);
-        rc = gather_f64(ctx, part, allp);
+    if (moments) {
+        // gathered over ranks (every rank reaches the collective, with its status) and summed
+        // in global chunk order: identical for any world size
+        std::vector<double> part, allp;
+        if (!rc) rc = local_moment_chunks(ctx, C, part);
+        else part.assign((size_t)((C + 1023) / 1024) * (n + nxx), 0.0);
+        rc = gather_f64(ctx, rc, part, allp);
         if (rc) return rc;
+        const int stride = n + nxx;
         std::vector<double> acc(allp.begin(), allp.begin() + stride);
         for (size_t k = 1; k < allp.size() / stride; ++k)
             for (int q = 0; q < stride; ++q) acc[q] += allp[k * stride + q];
@@ -1077,22 +1177,21 @@ static int walk_entry(spec_ctx* ctx, const spec_walk_params* p, const double* x0
         if (sum_xx) CK(cudaMemcpyAsync(sum_xx, acc.data() + n, sizeof(double) * nxx, kk, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
+    if (rc) return rc;
     if (final_x) {
+        ChainBuf& b = ctx->cb;
         if (host) {
-            double* tmp;
-            CK(cudaMalloc(&tmp, sizeof(double) * (size_t)C * n));
-            unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(b.X, np, C, n, tmp);
-            CK(cudaMemcpyAsync(final_x, tmp, sizeof(double) * (size_t)C * n, cudaMemcpyDeviceToHost, ctx->stream));
+            DevBuf tmp;
+            CK(tmp.alloc(sizeof(double) * (size_t)C * n));
+            unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(b.X, np, C, n, tmp.as<double>());
+            CK(cudaMemcpyAsync(final_x, tmp.p, sizeof(double) * (size_t)C * n, cudaMemcpyDeviceToHost, ctx->stream));
             CK(cudaStreamSynchronize(ctx->stream));
-            cudaFree(tmp);
         } else {
             unpad_rows_kernel<<<4096, 256, 0, ctx->stream>>>(b.X, np, C, n, final_x);
         }
         ctx->launches++;
     }
     CK(cudaStreamSynchronize(ctx->stream));
-    if (local.failures > 0)
-        return fail(SPEC_EPRECOND, std::to_string(local.failures) + " chain(s) started outside int S");
     return SPEC_OK;
 }
 
@@ -1109,6 +1208,7 @@ extern "C" int walk_trace(spec_ctx* ctx, const spec_walk_params* p, const int64_
                           int64_t max_refl, double* hit_x, double* t, double* w, double* v_after, int32_t* binding,
                           int64_t* nrec) {
     if (!chain_ids || nchains < 1 || max_refl < 1) return fail(SPEC_EINVAL, "bad trace arguments");
+    SW_NOT_DURING_WALK(ctx);
     spec_walk_params q = *p;
     q.chains = nchains;
     int rc = check_walk_params(ctx, &q);
@@ -1147,6 +1247,9 @@ static WalkRun& walk_run(spec_ctx* ctx) {
     if (!ctx->walk) ctx->walk = new WalkRun();
     return *(WalkRun*)ctx->walk;
 }
+// The resumable walk owns the chain buffers between walk_begin and walk_end: every other
+// entry point that uses them (oracle, walks, estimators, objective) returns EINVAL meanwhile.
+static bool walk_is_active(spec_ctx* ctx) { return ctx && ctx->walk && ((WalkRun*)ctx->walk)->active; }
 static void free_walk(spec_ctx* ctx) {
     delete (WalkRun*)ctx->walk;
     ctx->walk = nullptr;
@@ -1154,6 +1257,7 @@ static void free_walk(spec_ctx* ctx) {
 
 // ---------------------------------------------------------------- resumable walk API
 extern "C" int walk_begin(spec_ctx* ctx, const spec_walk_params* p, const double* x0_dev, int x0_per_chain) {
+    SW_NOT_DURING_WALK(ctx);
     int rc = check_walk_params(ctx, p);
     if (rc) return rc;
     CK(cudaSetDevice(ctx->dev));
@@ -1247,16 +1351,33 @@ extern "C" int spec_set_comm(spec_ctx* ctx, const spec_comm* comm) {
     return SPEC_OK;
 }
 
-// allgather of equal host shards in rank order (identity on one rank)
-static int gather_f64(spec_ctx* ctx, const std::vector<double>& local, std::vector<double>& global) {
+// allgather of equal host shards in rank order (identity on one rank).  rc_local is this
+// rank's status so far: it travels with the shard, every rank reaches the collective even
+// after a local failure, and all ranks return the first failing rank's code together
+// (no rank is left blocked in a collective the others skipped).
+static int gather_f64(spec_ctx* ctx, int rc_local, const std::vector<double>& local, std::vector<double>& global) {
     const int W = ctx->has_comm ? ctx->comm.world : 1;
-    global.assign(local.size() * (size_t)W, 0.0);
     if (W == 1) {
-        std::copy(local.begin(), local.end(), global.begin());
+        if (rc_local) return rc_local;
+        global = local;
         return SPEC_OK;
     }
-    int rc = ctx->comm.allgather_f64(ctx->comm.user, local.data(), (int64_t)local.size(), global.data());
+    const size_t nl = local.size();
+    std::vector<double> buf(nl + 1, 0.0), all((nl + 1) * (size_t)W, 0.0);
+    std::copy(local.begin(), local.end(), buf.begin());
+    buf[nl] = (double)rc_local;
+    const std::string msg = g_err;
+    int rc = ctx->comm.allgather_f64(ctx->comm.user, buf.data(), (int64_t)(nl + 1), all.data());
     if (rc) return fail(SPEC_ECUDA, "allgather callback failed");
+    for (int r = 0; r < W; ++r) {
+        const int rr = (int)all[(size_t)r * (nl + 1) + nl];
+        if (rr) return fail(rr, r == ctx->comm.rank ? msg : "rank " + std::to_string(r) + " failed (code " +
+                                                                 std::to_string(rr) + ")");
+    }
+    global.resize(nl * (size_t)W);
+    for (int r = 0; r < W; ++r)
+        std::copy(all.begin() + (size_t)r * (nl + 1), all.begin() + (size_t)r * (nl + 1) + nl,
+                  global.begin() + (size_t)r * nl);
     return SPEC_OK;
 }
 
@@ -1267,32 +1388,37 @@ static int ball_inside_count(spec_ctx* ctx, uint64_t seed, uint32_t tag, long lo
     int rc = ensure_chains(ctx, count);
     if (rc) return rc;
     const int n = ctx->n, np = ctx->np, m = ctx->m;
-    double* dc0;
-    CK(cudaMalloc(&dc0, sizeof(double) * n));
+    double* dc0 = ctx->c0;
     CK(cudaMemcpyAsync(dc0, c0_host, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     ball_sample_kernel<<<(count + 7) / 8, 256, 0, ctx->stream>>>(count, begin, n, np, seed, tag, dc0, r, b.X);
     ctx->launches++;
     launch_gemm_av(ctx, b.X, nullptr, nullptr, count, b.AX, ctx->a0);  // A(x_j)
     const int mp = roundup(m, 8);
-    const size_t smem = sizeof(double) * ((size_t)mp * ctx->ld + mp + 8);
+    size_t smem = sizeof(double) * ((size_t)mp * ctx->ld + mp + 8);
     const int NT = mp <= 64 ? 128 : 256;
     if (NT == 128) {
         CK(cudaFuncSetAttribute(membership_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         membership_kernel<128><<<std::min(count, ctx->num_sms * 8), 128, smem, ctx->stream>>>(
             count, n, np, m, ctx->mt, ctx->mtp, ctx->ld, b.X, b.AX, ctx->has_cube ? ctx->lo : nullptr, ctx->hi,
-            b.steps_done);
-    } else {
+            b.steps_done, nullptr, 0);
+    } else if (smem <= 227 * 1024 || !ctx->scratch) {
         CK(cudaFuncSetAttribute(membership_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         membership_kernel<256><<<std::min(count, ctx->num_sms * 2), 256, smem, ctx->stream>>>(
             count, n, np, m, ctx->mt, ctx->mtp, ctx->ld, b.X, b.AX, ctx->has_cube ? ctx->lo : nullptr, ctx->hi,
-            b.steps_done);
+            b.steps_done, nullptr, 0);
+    } else {
+        // m > ~160: A(x_j) does not fit in shared memory; factor it in the global-scratch slices
+        // of the K2 variant (one per CTA, >= mp x ld doubles each)
+        smem = sizeof(double) * (mp + 8);
+        membership_kernel<256><<<std::min(count, ctx->scratch_ctas), 256, smem, ctx->stream>>>(
+            count, n, np, m, ctx->mt, ctx->mtp, ctx->ld, b.X, b.AX, ctx->has_cube ? ctx->lo : nullptr, ctx->hi,
+            b.steps_done, ctx->scratch, ctx->scratch_stride);
     }
     ctx->launches++;
     std::vector<int> flags(count);
     CK(cudaMemcpyAsync(flags.data(), b.steps_done, sizeof(int) * count, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaGetLastError());
-    cudaFree(dc0);
     long long cnt = 0;
     for (int v : flags) cnt += v;
     *inside_out = cnt;
@@ -1312,6 +1438,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
                       const spec_volume_opts* o, spec_volume_report* out) {
     if (!ctx || !out) return fail(SPEC_EINVAL, "null argument");
     if (!(eps > 0.0 && eps < 1.0)) return fail(SPEC_EINVAL, "eps must be in (0,1)");
+    SW_NOT_DURING_WALK(ctx);
     const int n = ctx->n;
     spec_volume_opts opt;
     opt.walk_len = 10; opt.burn = 20; opt.L = 2.0 * std::sqrt((double)n); opt.rho = 10 * n;  // burn: R25
@@ -1332,14 +1459,26 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
     CK(cudaSetDevice(ctx->dev));
     std::vector<double> c0(n, 0.0);
     long long calls = 0;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
+    // the phase balls are installed on the context: removed on every return path
+    struct BallGuard {
+        spec_ctx* c;
+        ~BallGuard() { c->has_ball = 0; }
+    } ball_guard{ctx};
+    struct EventGuard {
+        cudaEvent_t e = nullptr;
+        ~EventGuard() {
+            if (e) cudaEventDestroy(e);
+        }
+    } g0, g1;
+    CK(cudaEventCreate(&g0.e));
+    CK(cudaEventCreate(&g1.e));
+    cudaEvent_t e0 = g0.e, e1 = g1.e;
     CK(cudaEventRecord(e0, ctx->stream));
 
     auto walk_phase = [&](double r, const std::vector<double>& X0, long long Nt, long long steps, uint32_t tag,
                           std::vector<double>& X) -> int {
         const long long Cl = Nt / W, begin = (long long)R * Cl;
+        X.assign((size_t)Cl * n, 0.0);
         int rc2 = spec_set_ball(ctx, r > 0 ? c0.data() : nullptr, r > 0 ? r : 0.0);
         if (rc2) return rc2;
         spec_walk_params p;
@@ -1358,9 +1497,8 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         const long long Cl = Nt / W, begin = (long long)R * Cl;
         long long cnt = 0;
         int rc2 = ball_inside_count(ctx, seed, tag, begin, (int)Cl, c0.data(), r, &cnt);
-        if (rc2) return rc2;
         std::vector<double> loc(1, (double)cnt), glob;
-        rc2 = gather_f64(ctx, loc, glob);
+        rc2 = gather_f64(ctx, rc2, loc, glob);
         if (rc2) return rc2;
         double tot = 0.0;
         for (double v : glob) tot += v;
@@ -1400,8 +1538,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
     std::vector<double> X, Xg, X0((size_t)(N / W) * n, 0.0), burned_g;
     // ---- pilot
     rc = walk_phase(-1.0, X0, N, opt.burn, vol_tag(3, 0, false, 0), X);
-    if (rc) return rc;
-    rc = gather_f64(ctx, X, burned_g);
+    rc = gather_f64(ctx, rc, X, burned_g);
     if (rc) return rc;
     Xg = burned_g;
     for (int i = 0; i < opt.max_phases; ++i) {
@@ -1419,8 +1556,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         rc = resample(Xg, r_next, N, X0);
         if (rc) return rc;
         rc = walk_phase(r_next, X0, N, opt.walk_len, vol_tag(3, i + 1, false, 0), X);
-        if (rc) return rc;
-        rc = gather_f64(ctx, X, Xg);
+        rc = gather_f64(ctx, rc, X, Xg);
         if (rc) return rc;
     }
     const int k = (int)radii.size();
@@ -1439,8 +1575,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         ratios.clear();
         for (int i = 0; i < k; ++i) {
             rc = walk_phase(i == 0 ? -1.0 : radii[i - 1], X0, Ne, opt.walk_len, vol_tag(1, i, false, attempt), X);
-            if (rc) return rc;
-            rc = gather_f64(ctx, X, Xg);
+            rc = gather_f64(ctx, rc, X, Xg);
             if (rc) return rc;
             long long in = 0;
             for (long long j = 0; j < Ne; ++j) in += (norm(&Xg[(size_t)j * n]) <= radii[i]) ? 1 : 0;
@@ -1459,18 +1594,17 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
         ++attempt;
         Ne *= 2;
     }
-    spec_set_ball(ctx, nullptr, 0.0);
+    ctx->has_ball = 0;
     CK(cudaEventRecord(e1, ctx->stream));
     CK(cudaEventSynchronize(e1));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     double logv = log_ball_volume(n, radii[k - 1]) + std::log(q);
     for (double rt : ratios) logv -= std::log(rt);
     // calls summed over ranks
     std::vector<double> cl(1, (double)calls), clg;
-    gather_f64(ctx, cl, clg);
+    rc = gather_f64(ctx, SPEC_OK, cl, clg);
+    if (rc) return rc;
     double calls_tot = 0.0;
     for (double v : clg) calls_tot += v;
     memset(out, 0, sizeof(*out));
@@ -1493,6 +1627,7 @@ extern "C" int volume(spec_ctx* ctx, double eps, uint64_t seed, int64_t chains_p
 extern "C" int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, const spec_expect_params* ep,
                            double* est, double* stderr_out) {
     if (!ctx || !ep || !est) return fail(SPEC_EINVAL, "null argument");
+    SW_NOT_DURING_WALK(ctx);
     if (f_id < 0 || f_id > 2) return fail(SPEC_EINVAL, "unknown f_id");
     if ((f_id == SPEC_F_LINEAR_C || f_id == SPEC_F_HALFSPACE_UNION) && !ctx->has_obj)
         return fail(SPEC_EINVAL, "f needs the objective c (spec_set_objective)");
@@ -1512,18 +1647,21 @@ extern "C" int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, con
     p.tag = 0;
     p.T = hmc ? T : 1.0;
     spec_walk_stats st;
+    std::vector<double> fl((size_t)Cl, 0.0), fg;
     int rc = walk_entry(ctx, &p, nullptr, 0, nullptr, nullptr, nullptr, &st, true);
-    if (rc) return rc;
-    double* df;
-    CK(cudaMalloc(&df, sizeof(double) * Cl));
-    fvalue_kernel<<<(int)std::min<long long>((Cl + 7) / 8, 65535), 256, 0, ctx->stream>>>(
-        (int)Cl, ctx->n, ctx->np, ctx->cb.X, ctx->c, f_id, ep->b1, ep->b2, df);
-    ctx->launches++;
-    std::vector<double> fl((size_t)Cl), fg;
-    CK(cudaMemcpyAsync(fl.data(), df, sizeof(double) * Cl, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    cudaFree(df);
-    rc = gather_f64(ctx, fl, fg);
+    if (!rc) {
+        rc = [&]() -> int {
+            DevBuf df;
+            CK(df.alloc(sizeof(double) * Cl));
+            fvalue_kernel<<<(int)std::min<long long>((Cl + 7) / 8, 65535), 256, 0, ctx->stream>>>(
+                (int)Cl, ctx->n, ctx->np, ctx->cb.X, ctx->c, f_id, ep->b1, ep->b2, df.as<double>());
+            ctx->launches++;
+            CK(cudaMemcpyAsync(fl.data(), df.p, sizeof(double) * Cl, cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+            return SPEC_OK;
+        }();
+    }
+    rc = gather_f64(ctx, rc, fl, fg);
     if (rc) return rc;
     double s = 0.0;
     for (double v : fg) s += v;  // global chain order: identical for any GPU count

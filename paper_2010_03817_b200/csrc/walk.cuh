@@ -219,11 +219,12 @@ __global__ void moments_kernel(const double* X, int np, int n, int chains, doubl
 }
 
 __global__ void stats_kernel(int chains, const long long* calls, const long long* nrefl, const int* nrej,
-                             const int* ndeg, const int* flags, const int* steps_done, long long* out) {
-    __shared__ long long acc[6];
-    if (threadIdx.x < 6) acc[threadIdx.x] = 0;
+                             const int* ndeg, const int* ncap, const int* flags, const int* steps_done,
+                             long long* out) {
+    __shared__ long long acc[7];
+    if (threadIdx.x < 7) acc[threadIdx.x] = 0;
     __syncthreads();
-    long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
+    long long a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0;
     for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < chains; c += gridDim.x * blockDim.x) {
         a0 += calls[c];
         a1 += nrefl[c];
@@ -231,6 +232,7 @@ __global__ void stats_kernel(int chains, const long long* calls, const long long
         a3 += ndeg[c];
         a4 += (flags[c] & CF_FAILED) ? 1 : 0;
         a5 += steps_done[c];
+        a6 += ncap[c];
     }
     atomicAdd((unsigned long long*)&acc[0], (unsigned long long)a0);
     atomicAdd((unsigned long long*)&acc[1], (unsigned long long)a1);
@@ -238,8 +240,9 @@ __global__ void stats_kernel(int chains, const long long* calls, const long long
     atomicAdd((unsigned long long*)&acc[3], (unsigned long long)a3);
     atomicAdd((unsigned long long*)&acc[4], (unsigned long long)a4);
     atomicAdd((unsigned long long*)&acc[5], (unsigned long long)a5);
+    atomicAdd((unsigned long long*)&acc[6], (unsigned long long)a6);
     __syncthreads();
-    if (threadIdx.x < 6) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)acc[threadIdx.x]);
+    if (threadIdx.x < 7) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)acc[threadIdx.x]);
 }
 
 __global__ void iota_kernel(int* list, int count) {

@@ -162,3 +162,46 @@ def test_hmc_boltzmann_cube_moments():
         _check_moment(X[:, i], e1)
         _check_moment(X[:, i] ** 2, e2)
     assert st["failures"] == 0
+
+
+# ---------------------------------------------------------------- orc_replay / orc_trace budget semantics
+def test_replay_one_call_cube_closed_form():
+    """Replay budget = 1 call on the cube [-1,1]^n (P1): from x0 = 0 the billiard's first
+    segment (Alg. 5) ends at min(l, t+) v, with l = -L ln eta and
+    t+ = min_i (sgn v_i - 0)/v_i = 1/max|v_i| (closed form), v = g/|g| from the step draws."""
+    n = 6
+    lmi = oracle.Lmi(specgen.cube_only(n))
+    for chain in range(20):
+        for L in (0.3, 3.0):
+            g, eta = oracle.step_draws(5, 0, chain, 0, n)
+            v = g / np.linalg.norm(g)
+            ell = -L * np.log(eta)
+            tp = 1.0 / np.max(np.abs(v))
+            x, calls = oracle.replay(lmi, oracle.BILLIARD, 5, chain, 10, L, 100, 1)
+            assert calls == 1
+            expect = min(ell, tp) * v
+            assert np.allclose(x, expect, rtol=0, atol=1e-14), (chain, L, x, expect)
+
+
+def test_replay_matches_walk_and_trace():
+    """Replay with the budget of s whole steps ends exactly where an s-step walk ends; a budget
+    inside a step ends at the last recorded hit point of the trace (bit for bit: same chains)."""
+    inst = specgen.rand_cube(8, 8, 3)
+    lmi = oracle.Lmi(inst)
+    L, rho = 2 * np.sqrt(8), 80
+    for chain in (0, 5, 11):
+        for s in (1, 3):
+            X, st = oracle.walk(lmi, oracle.BILLIARD, 7, chain, chain + 1, s, L, rho, nthreads=1)
+            x, calls = oracle.replay(lmi, oracle.BILLIARD, 7, chain, 50, L, rho, st["calls"])
+            assert calls == st["calls"]
+            assert np.array_equal(x, X[0]), (chain, s)
+        tr = oracle.trace(lmi, oracle.BILLIARD, 7, chain, 50, L, rho, 6, stop=True)
+        full = oracle.trace(lmi, oracle.BILLIARD, 7, chain, 50, L, rho, 6)
+        for k in ("hit_x", "t", "w", "v_after", "binding"):
+            assert np.array_equal(tr[k], full[k])
+        # the first step of these chains reflects at least 6 times before it ends
+        g, eta = oracle.step_draws(7, 0, chain, 0, 8)
+        assert len(tr["t"]) == 6 and -L * np.log(eta) > tr["t"].sum()
+        x, calls = oracle.replay(lmi, oracle.BILLIARD, 7, chain, 50, L, rho, 6)
+        assert calls == 6
+        assert np.array_equal(x, tr["hit_x"][5])
