@@ -38,7 +38,7 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liborc.so")
 
 INF = float("inf")
-BILLIARD, HMC = 0, 1
+BILLIARD, HMC, HNR, CHNR = 0, 1, 2, 3  # HnR: Alg. 4; CHnR: P:985-996
 TAG_WALK = 0 << 28
 TAG_VOLUME = 1 << 28
 TAG_PILOT = 3 << 28
@@ -98,6 +98,7 @@ def lib():
         l.orc_u01.restype = C.c_double
         l.orc_u01.argtypes = [C.c_uint32, C.c_uint32]
         l.orc_step_draws.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _dp, _dp]
+        l.orc_step_uniforms.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, _dp, _dp]
         l.orc_chord.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_int, _dp, C.POINTER(_ChordRes)]
         l.orc_normal.argtypes = [C.c_void_p, C.c_int, _dp, C.c_int, _dp]
         l.orc_reflect.argtypes = [C.c_int, _dp, _dp, _dp]
@@ -207,6 +208,13 @@ def step_draws(seed: int, tag: int, chain: int, step: int, n: int):
     eta = C.c_double()
     lib().orc_step_draws(seed, tag, chain, step, n, _p(g), C.byref(eta))
     return g, eta.value
+
+
+def step_uniforms(seed: int, tag: int, chain: int, step: int, n: int):
+    """(eta, u2): the two doubles of Philox block ceil(n/2) of a step (W-CHnR: j = floor(u2 n))."""
+    eta, u2 = C.c_double(), C.c_double()
+    lib().orc_step_uniforms(seed, tag, chain, step, n, C.byref(eta), C.byref(u2))
+    return eta.value, u2.value
 
 
 def chord(lmi: Lmi, x, v, F0=None, bound: int = -1, u=None) -> dict:

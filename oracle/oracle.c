@@ -299,6 +299,18 @@ void orc_step_draws(uint64_t seed, uint32_t tag, uint32_t chain, uint32_t step, 
     }
 }
 
+/* the two doubles of block ceil(n/2): eta (as orc_step_draws) and the second one, which
+   picks the coordinate of a W-CHnR step (R29) */
+void orc_step_uniforms(uint64_t seed, uint32_t tag, uint32_t chain, uint32_t step, int n, double* eta,
+                       double* u2) {
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t ctr[4] = {(uint32_t)((n + 1) / 2), step, chain, tag};
+    uint32_t w[4];
+    orc_philox4x32_10(ctr, key, w);
+    *eta = orc_u01(w[0], w[1]);
+    *u2 = orc_u01(w[2], w[3]);
+}
+
 /* ------------------------------------------------------------------------ */
 /* INTERSECTION on one block (Alg. 2; Lemma 3)            */
 /* ------------------------------------------------------------------------ */
@@ -994,11 +1006,48 @@ typedef struct {
 /* One step of the Billiard walk (Alg. 5; readings R4, R5) or
  * of HMC-r (Alg. 6; eq:boltz_ode).  Returns 0, or 2 if the start
  * point is not interior. */
+/* One step of Hit-and-Run (Alg. 4 alg:hitandrun P:939-965) or of coordinate-directions
+ * Hit-and-Run (W-CHnR) for the uniform law: v ~ U(sphere) (HnR) or v = e_j with
+ * j uniform in [n] (CHnR); (t-, t+) = INTERSECTION (one chord, Lemma 3); the next point is
+ * uniform on [p + t- v, p + t+ v]: p += (t- + eta (t+ - t-)) v, and F(p) is carried as
+ * F += t F1(v) (for e_j, F1 = A_j: the O(m^2) update of P:988-995). */
+static int hnr_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, uint32_t step, walk_ws* W,
+                    orc_stats* st) {
+    int n = L->n, m = L->mb[0];
+    size_t mm = (size_t)m * m;
+    double eta;
+    if (p->kind == ORC_HNR) {
+        orc_step_draws(p->seed, p->tag, chain, step, n, W->g, &eta);
+        double gn = 0.0;
+        for (int i = 0; i < n; ++i) gn += W->g[i] * W->g[i];
+        gn = sqrt(gn);
+        for (int i = 0; i < n; ++i) W->v[i] = W->g[i] / gn;
+    } else {
+        double u2;
+        orc_step_uniforms(p->seed, p->tag, chain, step, n, &eta, &u2);
+        int j = (int)(u2 * (double)n);
+        if (j > n - 1) j = n - 1;
+        for (int i = 0; i < n; ++i) W->v[i] = (i == j) ? 1.0 : 0.0;
+    }
+    st->steps += 1;
+    if (W->budget >= 0 && st->calls >= W->budget) return 5;
+    orc_dir_block(L, 0, W->v, W->F1);
+    orc_chord_res* r = W->res;
+    int rc = orc_chord(L, W->x, W->F, W->F1, W->v, -1, NULL, r);
+    st->calls += 1;
+    if (rc) return rc;
+    double t = r->t_minus + eta * (r->t_plus - r->t_minus);
+    for (int i = 0; i < n; ++i) W->x[i] += t * W->v[i];
+    for (size_t e = 0; e < mm; ++e) W->F[e] += t * W->F1[e];
+    return 0;
+}
+
 static int walk_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, uint32_t step,
                      walk_ws* W, orc_stats* st, trace_rec* tr) {
     int n = L->n, m = L->mb[0];
     size_t mm = (size_t)m * m;
     double eta;
+    if (p->kind == ORC_HNR || p->kind == ORC_CHNR) return hnr_step(L, p, chain, step, W, st);
     orc_step_draws(p->seed, p->tag, chain, step, n, W->g, &eta);
     double ell;
     if (p->kind == ORC_BILLIARD) {

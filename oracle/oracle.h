@@ -55,6 +55,9 @@ double orc_u01(uint32_t a, uint32_t b);
 /* per-(chain, step) draws: g (n normals, Box-Muller) and eta in (0,1). */
 void orc_step_draws(uint64_t seed, uint32_t tag, uint32_t chain, uint32_t step, int n,
                     double* g, double* eta);
+/* the two doubles of block ceil(n/2) of a step: eta and u2 (W-CHnR coordinate j = floor(u2 n)) */
+void orc_step_uniforms(uint64_t seed, uint32_t tag, uint32_t chain, uint32_t step, int n, double* eta,
+                       double* u2);
 
 /* ---- the boundary oracle ---- */
 typedef struct orc_chord_res {
@@ -87,7 +90,7 @@ void orc_reflect(int n, const double* u, const double* w, double* s);
 int orc_membership(const orc_lmi* L, const double* x);
 
 /* ---- walks ---- */
-enum { ORC_BILLIARD = 0, ORC_HMC = 1 };
+enum { ORC_BILLIARD = 0, ORC_HMC = 1, ORC_HNR = 2, ORC_CHNR = 3 }; /* HnR: Alg. 4; CHnR: P:985-996 */
 typedef struct orc_stats {
     int64_t calls, reflections, rejects, degenerates, steps, failures;
 } orc_stats;

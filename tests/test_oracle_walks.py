@@ -205,3 +205,49 @@ def test_replay_matches_walk_and_trace():
         x, calls = oracle.replay(lmi, oracle.BILLIARD, 7, chain, 50, L, rho, 6)
         assert calls == 6
         assert np.array_equal(x, tr["hit_x"][5])
+
+
+# ---------------------------------------------------------------- Hit-and-Run / coordinate Hit-and-Run
+@pytest.mark.parametrize("kind", [oracle.HNR, oracle.CHNR])
+def test_hnr_one_step_cube_closed_form(kind):
+    """One W-HnR / W-CHnR step (Alg. 4) on the cube [-1,1]^n from x0:
+    the chord through x0 along v has t+ = min_i (sgn v_i - x0_i)/v_i and
+    t- = max_i (-sgn v_i - x0_i)/v_i (closed form), the next point x0 + (t- + eta (t+ - t-)) v."""
+    n = 5
+    lmi = oracle.Lmi(specgen.cube_only(n))
+    x0 = np.array([0.3, -0.2, 0.0, 0.7, -0.9])
+    for chain in range(25):
+        if kind == oracle.HNR:
+            g, eta = oracle.step_draws(2, 0, chain, 0, n)
+            v = g / np.linalg.norm(g)
+        else:
+            eta, u2 = oracle.step_uniforms(2, 0, chain, 0, n)
+            v = np.zeros(n)
+            v[min(int(u2 * n), n - 1)] = 1.0
+        nz = v != 0
+        tp = np.min((np.sign(v[nz]) - x0[nz]) / v[nz])
+        tm = np.max((-np.sign(v[nz]) - x0[nz]) / v[nz])
+        X, st = oracle.walk(lmi, kind, 2, chain, chain + 1, 1, 1.0, 10, x0=x0, nthreads=1)
+        assert st["calls"] == 1 and st["reflections"] == 0
+        assert np.allclose(X[0], x0 + (tm + eta * (tp - tm)) * v, rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("kind", [oracle.HNR, oracle.CHNR])
+@pytest.mark.parametrize("body", ["cube_dense", "ball", "elliptope3"])
+def test_hnr_uniform_moments(kind, body):
+    """W-HnR / W-CHnR target the uniform law: E[x_i] = 0 and E[x_i^2] = 1/3 (cube), 1/(n+2)
+    (ball), 1/(k+1) (elliptope) over chain end points."""
+    if body == "cube_dense":
+        inst, ex2 = specgen.cube_dense(3), 1 / 3
+    elif body == "ball":
+        inst, ex2 = specgen.ball(4), 1 / 6
+    else:
+        inst, ex2 = specgen.elliptope(3), 1 / 4
+    lmi = oracle.Lmi(inst)
+    X, st = oracle.walk(lmi, kind, 21, 0, 3000, 40, 1.0, 10)
+    assert st["calls"] == 3000 * 40 and st["steps"] == 3000 * 40
+    x2 = (X ** 2).mean(1)
+    se = x2.std(ddof=1) / np.sqrt(len(x2))
+    assert abs(x2.mean() - ex2) <= 4 * se, (x2.mean(), ex2, se)
+    mx = X.mean(1)
+    assert abs(mx.mean()) <= 4 * mx.std(ddof=1) / np.sqrt(len(mx))
