@@ -9,9 +9,11 @@ K3 normal GEMM -> K4 reflect), i.e. one pass of the hot path over the batch.
 All 65536 chains stay active for the whole timed region (a chain needs ~27000
 rounds to finish its 100 steps), so every timed round processes the full batch.
 
-N > 1 (torchrun): every rank runs its own 65536 chains (global chain ids
-[rank*65536, (rank+1)*65536) key the RNG), no collective in the data path:
-"scaling": "weak" (per-GPU work fixed as N grows).
+N > 1 (torchrun): the 65536 chains of the workload are split into N contiguous
+global-id ranges (configs[4]: "65536 chains ... sharded across 1/2/4/8 B200"),
+rank r runs [r*65536/N, (r+1)*65536/N) (the ids key the RNG, so a chain's
+trajectory does not depend on N), no collective in the data path:
+"scaling": "strong" (total work fixed).  --scaling weak runs 65536 chains per rank.
 Timing: barrier + cuda synchronize on both sides, CUDA events on the library
 stream, max over ranks.
 
@@ -42,7 +44,7 @@ INSTANCE_SEED = 3  # BASELINE.json configs[3] instance (SURVEY 8(d).1 "M100")
 L_TAU = 2.0 * math.sqrt(N_DIM)
 RHO = 10 * N_DIM
 HMC_L = 1.09  # configs[3] HMC trajectory length: the diameter estimate
-LANCZOS_K = 55  # Lanczos iterations at m = 100 in the algorithmic flop model
+LANCZOS_K = 55  # SURVEY V9 prior; the bench uses the device-measured mean J of its timed rounds
 
 WORKLOAD = (f"M100: billiard walk (Alg. 5) on the BASELINE.json configs[3] instance (rand-cube n=m={N_DIM}, "
             f"seed {INSTANCE_SEED}), {CHAINS} chains x {STEPS_PER_CHAIN} steps, L=2sqrt(n), rho=10n, seed {SEED}")
@@ -77,9 +79,22 @@ def ncu_traffic_per_launch(tag: str):
             "source": os.path.relpath(files[-1], ROOT)}
 
 
+def measured_fp64() -> dict:
+    """The committed FP64 measurements of this pool's B200 (tools/fp64_peak.py on the box:
+    cuBLAS DGEMM 8192^3 burst / 4-s sustained, DFMA and DMMA issue loops)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*fp64_peak.json")))
+    if not files:
+        return {}
+    d = json.load(open(files[-1]))
+    d["source"] = os.path.relpath(files[-1], ROOT)
+    return d
+
+
 def fp64_peak_tflops() -> float:
     """FP64 FMA pipe peak derived from unit counts and clocks (B200: 148 SMs x 64
-    DFMA/clk x 2 flop x 1.965 GHz).  MEASURED_PEAKS.json carries no fp64 entry."""
+    DFMA/clk x 2 flop x 1.965 GHz).  MEASURED_PEAKS.json carries
+    no fp64 entry; the measured DGEMM / DMMA rates are reported beside it."""
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         mhz = float(mp.get("sm_max_mhz", 1965.0))
@@ -215,7 +230,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "boundary-oracle calls/s (billiard walk, n=m=100)", "value": value,
         "unit": "calls/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": wall * 1e3 / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": wall * 1e3 / max(args.steps, 1), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD, "n": N_DIM, "m": M_DIM,
                    "reference_step": f"{nthreads} M100 billiard chains (one per host core), the first {ref_calls} "
@@ -255,7 +270,13 @@ def run_ours(args):
     dev = torch.cuda.current_device()
     inst = specgen.config_instance(3)
     S = sw.Spectrahedron.from_instance(inst, device=dev)
-    local_chains = args.chains
+    strong = (args.scaling == "strong")
+    if strong:
+        if args.chains % world:
+            raise SystemExit(f"--chains {args.chains} does not split over {world} ranks")
+        local_chains = args.chains // world
+    else:
+        local_chains = args.chains
     begin = rank * local_chains
     chains = local_chains * world
     stream = torch.cuda.ExternalStream(S.stream(), device=dev)
@@ -270,6 +291,7 @@ def run_ours(args):
     S.walk_rounds(max(args.warmup, 3) if args.warmup > 0 else 0)
     st0 = S.walk_stats_now()
     S.kernel_timing(True)
+    S.lanczos_iterations(reset=True)
     launches0 = S.kernel_launches()
     barrier()
     with ClockSampler(dev) as clk:
@@ -283,6 +305,7 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     launches = S.kernel_launches() - launches0
     st1 = S.walk_stats_now()
+    lz = S.lanczos_iterations(reset=True)
     kt = S.kernel_times()
     S.kernel_timing(False)
     S.walk_end()
@@ -299,7 +322,8 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel, from its own events on the library stream:
     # K2b lanczos_kernel when K2 is split (m = 100), else the whole K2
-    f = flops_per_call(N_DIM, M_DIM)
+    J = lz["mean_j"] if lz["solves"] > 0 else float(LANCZOS_K)  # measured k of the flop model
+    f = flops_per_call(N_DIM, M_DIM, J)
     k2_ms = kt["ms"]["K2_chord"]
     k2_launches = kt["launches"]["K2_chord"]
     k2_items = kt["k2_items"]
@@ -308,6 +332,7 @@ def run_ours(args):
     k2_flops_per_launch = f["k2"] * items_per_launch
     k2_achieved = k2_flops_per_launch / (k2_avg_ms * 1e-3) / 1e12
     peak = fp64_peak_tflops()
+    meas = measured_fp64()
     phases = kt.get("k2_phases_ms", {})
     share = {k: v / max(sum(kt["ms"].values()), 1e-9) for k, v in kt["ms"].items()}
     tot_ms = max(sum(kt["ms"].values()), 1e-9)
@@ -326,7 +351,7 @@ def run_ours(args):
     # ---- end-to-end through the public host API (walk_sample with host buffers)
     e2e = None
     if args.e2e_chains > 0:
-        ec = args.e2e_chains
+        ec = args.e2e_chains // world if strong else args.e2e_chains
         eb = rank * ec
         x0 = np.zeros((ec, N_DIM))
         barrier()
@@ -362,6 +387,7 @@ def run_ours(args):
         S.walk_rounds(2)
         h0 = S.walk_stats_now()
         hl0 = S.kernel_launches()
+        S.lanczos_iterations(reset=True)
         barrier()
         he0 = torch.cuda.Event(enable_timing=True)
         he1 = torch.cuda.Event(enable_timing=True)
@@ -372,6 +398,7 @@ def run_ours(args):
         barrier()
         hms = he0.elapsed_time(he1)
         h1 = S.walk_stats_now()
+        hlz = S.lanczos_iterations(reset=True)
         S.walk_end()
         ht = torch.tensor([hms, float(h1["calls"] - h0["calls"])], dtype=torch.float64, device=coll_dev)
         if dist is not None:
@@ -381,8 +408,19 @@ def run_ours(args):
             hms, hcalls = float(hmax[0]), float(ht[1])
         else:
             hcalls = float(ht[1])
+        hcalls_local = float(h1["calls"] - h0["calls"])
+        iw = hlz["solves"] / max(hcalls_local, 1.0)  # Weyl iterations per call (one N_1 Lanczos solve each)
+        hJ = hlz["mean_j"]
+        m_ = M_DIM
+        hmc_flops = 2 * N_DIM * m_ * (m_ + 1) + iw * (m_ ** 3 / 3 + 2 * m_ ** 3 + 2 * hJ * m_ * m_)
+        h_ach = hmc_flops * hcalls / (hms * 1e-3) / 1e12
         hmc = {"metric": "HMC-r boundary-oracle calls/s (configs[3]: n=m=100, T=1, c~N(0,I) normalised)",
                "value": hcalls / (hms * 1e-3), "unit": "calls/s", "chains": chains, "rounds": args.hmc_rounds,
+               "roofline": {"bound": "alu", "achieved": h_ach, "peak": peak, "unit": "TFLOP/s", "frac": h_ach / peak,
+                            "kernel": "whole HMC-r round (K1 + K5 split kernels + K3 + K4)",
+                            "flops_per_call": hmc_flops, "weyl_iterations_per_call": iw, "lanczos_j": hJ,
+                            "flop_model": "SURVEY 8(d).2: 2 n m(m+1) + I_w (m^3/3 + 2 m^3 + 2 J m^2), I_w and J "
+                                          "measured on the device over the timed rounds"},
                "ms": hms, "calls": hcalls, "L": HMC_L, "gpu_launches": int(S.kernel_launches() - hl0),
                "note": "one quadratic-pencil chord per chain per round (Weyl stepping, ~5 Cholesky + Lanczos "
                        "iterations per call); device events on the library stream, max over ranks"}
@@ -398,6 +436,7 @@ def run_ours(args):
         S4.walk_rounds(2)
         g0 = S4.walk_stats_now()
         S4.kernel_timing(True)
+        S4.lanczos_iterations(reset=True)
         barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
@@ -408,6 +447,7 @@ def run_ours(args):
         barrier()
         fms = f0.elapsed_time(f1)
         g1 = S4.walk_stats_now()
+        lz4 = S4.lanczos_iterations(reset=True)
         kt4 = S4.kernel_times()
         S4.walk_end()
         del S4
@@ -419,7 +459,8 @@ def run_ours(args):
             fms, fcalls = float(fmax_[0]), float(ft[1])
         else:
             fcalls = float(ft[1])
-        f4 = flops_per_call(200, 200, 68)
+        J4 = lz4["mean_j"] if lz4["solves"] > 0 else 68.0
+        f4 = flops_per_call(200, 200, J4)
         k2ms4 = kt4["ms"]["K2_chord"]
         k2_ach4 = f4["k2"] * (kt4["k2_items"] / max(k2ms4 * 1e-3, 1e-12)) / 1e12
         m200 = {"metric": "boundary-oracle calls/s (billiard walk, n=m=200, configs[4])",
@@ -427,7 +468,8 @@ def run_ours(args):
                 "ms": fms, "calls": fcalls,
                 "roofline_k2": {"bound": "alu", "achieved": k2_ach4, "peak": fp64_peak_tflops(), "unit": "TFLOP/s",
                                 "frac": k2_ach4 / fp64_peak_tflops(), "flops_per_chain_call": f4["k2"],
-                                "flop_model": "SURVEY 8(d).2: m^3/3 + m^3 + 2 k m^2, k = 68 (V9)"},
+                                "lanczos_j": J4,
+                                "flop_model": "SURVEY 8(d).2: m^3/3 + m^3 + 2 J m^2, J measured on the device"},
                 "kernel_share": {k: v / max(sum(kt4["ms"].values()), 1e-9) for k, v in kt4["ms"].items()}}
 
     # ---- BASELINE metric, second half: volume time at n = m = 40 (configs[2], eps 0.1, 4096 chains/phase)
@@ -466,7 +508,7 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms_max / max(args.steps, 1),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling if world > 1 else "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
@@ -479,12 +521,17 @@ def run_ours(args):
                      "traffic": traffic, "kernel": dom,
                      "flops_per_chain_call": dom_flops, "chain_calls_per_launch": items_per_launch,
                      "avg_launch_ms": dom_avg_ms,
-                     "flop_model": "SURVEY 8(d).2: Lanczos 2 k m^2 (k = 55) for K2b; K2 total m^3/3 + m^3 + 2 k m^2",
+                     "lanczos_j": J,
+                     "flop_model": "SURVEY 8(d).2: Lanczos 2 J m^2 for K2b; K2 total m^3/3 + m^3 + 2 J m^2; J = "
+                                   "device-measured mean Lanczos iterations per solve over the timed rounds",
                      "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full "
                                       f"capture {tr['source'] if tr else '-'} (one 65536-chain round); algorithmic "
                                       f"bytes = M read once, {8 * M_DIM * M_DIM * items_per_launch:.3g} B/launch"),
-                     "peak_note": "fp64 FMA pipe 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (derived; measured DFMA "
-                                  "36.7, cuBLAS DGEMM 35.4 TF/s, tools/fp64_peak.py)"},
+                     "peak_note": "derived: fp64 pipe 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (MEASURED_PEAKS.json "
+                                  "has no fp64 entry)",
+                     "measured_fp64": meas,
+                     "frac_of_measured_dgemm_sustained": (achieved / meas["dgemm_tflops_sustained"])
+                     if meas.get("dgemm_tflops_sustained") else None},
         "roofline_k2_total": {"bound": "alu", "achieved": k2_achieved, "peak": peak, "unit": "TFLOP/s",
                               "frac": k2_achieved / peak, "flops_per_chain_call": f["k2"],
                               "avg_launch_ms": k2_avg_ms},
@@ -512,7 +559,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--chains", type=int, default=CHAINS, help="chains per GPU")
+    ap.add_argument("--chains", type=int, default=CHAINS,
+                    help="global chains (strong scaling, split over ranks) or chains per GPU (weak)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--e2e-chains", type=int, default=16384)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--volume-seeds", type=int, default=3)

@@ -121,10 +121,18 @@ int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, c
                double* t_plus, double* normal, double* kernel, int32_t* binding);
 
 /* ---- walks ---- */
-enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1 };
+/* BILLIARD: Alg. 5; HMC: reflective HMC for exp(-c^T x / T), Alg. 6
+ * (P:1079-1115); HNR: Hit-and-Run for the uniform law, Alg. 4 -- the next point
+ * is uniform on the chord [x + t- v, x + t+ v], v ~ U(sphere); CHNR: coordinate-directions
+ * Hit-and-Run, v = e_j with j uniform, A(v) = A_j read from the packed
+ * coefficients (no contraction).  Hit-and-Run makes exactly one boundary-oracle call per
+ * step and never reflects (L and rho are ignored); with 0 < T < inf it samples the
+ * Boltzmann law exp(-c^T x / T) (sec:optimization P:1408-1424; needs the objective): the
+ * point on the chord is a truncated exponential; T <= 0 or T = inf: the uniform law. */
+enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1, SPEC_WALK_HNR = 2, SPEC_WALK_CHNR = 3 };
 
 typedef struct spec_walk_params {
-    int kind;            /* SPEC_WALK_BILLIARD (Alg. 5) or SPEC_WALK_HMC (Alg. 6, Boltzmann) */
+    int kind;            /* SPEC_WALK_BILLIARD (Alg. 5), SPEC_WALK_HMC (Alg. 6, Boltzmann), SPEC_WALK_HNR, SPEC_WALK_CHNR */
     int64_t chain_begin; /* global id of this rank's first chain (keys the RNG) */
     int64_t chains;      /* number of chains run by this call */
     int64_t steps;       /* walk steps per chain (each ends in accept or reject) */
@@ -132,7 +140,8 @@ typedef struct spec_walk_params {
     int64_t rho;         /* reflection bound (reject the step when #refl > rho) */
     uint64_t seed;       /* Philox4x32-10 key */
     uint32_t tag;        /* counter word 3 (purpose << 28 | phase), 0 for plain walks */
-    double T;            /* HMC temperature (>0); ignored for billiard */
+    double T;            /* HMC temperature (>0); Hit-and-Run: 0 < T < inf Boltzmann, else uniform;
+                            ignored for billiard */
 } spec_walk_params;
 
 typedef struct spec_walk_stats {
@@ -188,6 +197,11 @@ int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st);
  * number of chain slots K2 processed (including finished ones not yet compacted). */
 int spec_kernel_timing(spec_ctx* ctx, int enable);
 int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items);
+/* Lanczos iterations per extreme-eigenvalue solve, counted on the device since creation or
+ * the last reset (every billiard chord makes one solve; an HMC-r chord one per Weyl
+ * iteration): *mean_j = sum J / solves.  reset != 0 zeroes the counters after reading.
+ * This is the measured k of the flop model 2 k m^2. */
+int spec_lanczos_iterations(spec_ctx* ctx, int reset, double* mean_j, int64_t* solves);
 /* With timing enabled and K2 split into factor / Lanczos / tail kernels (64 < m <= 128): the
  * accumulated ms of each phase (ms3[0..2], host buffer); zeros for the fused K2 variants. */
 int spec_k2_phase_times(spec_ctx* ctx, double* ms3);

@@ -26,7 +26,7 @@ _lp = C.POINTER(C.c_int64)
 
 SPEC_OK = 0
 ERRORS = {1: "EINVAL", 2: "EPRECOND", 3: "ERUNTIME", 4: "ECUDA", 5: "ENOMEM", 6: "EUNBOUNDED"}
-BILLIARD, HMC = 0, 1
+BILLIARD, HMC, HNR, CHNR = 0, 1, 2, 3  # Alg. 5, Alg. 6, Alg. 4, W-CHnR
 BIND_DENSE, BIND_BALL, BIND_NONE = 0, -1, -2
 
 # the symbols include/specwalk.h declares (checked by tests/test_abi.py)
@@ -35,6 +35,7 @@ EXPORTS = (
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
     "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
+    "spec_lanczos_iterations",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -128,6 +129,7 @@ def load(build_if_missing: bool = True):
     l.spec_kernel_timing.argtypes = [C.c_void_p, C.c_int]
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
     l.spec_k2_phase_times.argtypes = [C.c_void_p, _dp]
+    l.spec_lanczos_iterations.argtypes = [C.c_void_p, C.c_int, _dp, _lp]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
     l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
@@ -277,14 +279,16 @@ class Spectrahedron:
 
     # -------------------------------------------------------------- walks
     @staticmethod
-    def _params(kind, chains, steps, L, rho, seed, chain_begin=0, tag=0, T=1.0) -> WalkParams:
+    def _params(kind, chains, steps, L, rho, seed, chain_begin=0, tag=0, T=None) -> WalkParams:
+        if T is None:  # HMC: T = 1; Hit-and-Run: the uniform law (T = inf); ignored by the billiard
+            T = 1.0 if kind == HMC else float("inf")
         p = WalkParams()
         p.kind, p.chain_begin, p.chains, p.steps = kind, chain_begin, chains, steps
         p.L, p.rho, p.seed, p.tag, p.T = float(L), rho, seed, tag, float(T)
         return p
 
     def walk_sample(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD,
-                    x0=None, chain_begin: int = 0, tag: int = 0, T: float = 1.0, final: bool = True) -> dict:
+                    x0=None, chain_begin: int = 0, tag: int = 0, T: Optional[float] = None, final: bool = True) -> dict:
         p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
         per_chain = 0
         x0a = None
@@ -300,7 +304,7 @@ class Spectrahedron:
 
     def walk_sample_dev(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD,
                         x0=None, sum_x=None, sum_xx=None, final_x=None, chain_begin: int = 0, tag: int = 0,
-                        T: float = 1.0) -> dict:
+                        T: Optional[float] = None) -> dict:
         p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
         ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
         per_chain = 1 if (x0 is not None and x0.dim() == 2) else 0
@@ -311,7 +315,7 @@ class Spectrahedron:
 
     # resumable walk: begin / rounds / end (device buffers are torch CUDA tensors)
     def walk_begin(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD, x0=None,
-                   chain_begin: int = 0, tag: int = 0, T: float = 1.0):
+                   chain_begin: int = 0, tag: int = 0, T: Optional[float] = None):
         p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
         ptr = None if x0 is None else C.c_void_p(x0.data_ptr())
         per_chain = 1 if (x0 is not None and x0.dim() == 2) else 0
@@ -348,8 +352,14 @@ class Spectrahedron:
                     k2_items=items.value,
                     k2_phases_ms=dict(K2a_factor=k2[0], K2b_lanczos=k2[1], K2c_tail=k2[2]))
 
+    def lanczos_iterations(self, reset: bool = True) -> dict:
+        """Device-counted Lanczos iterations per extreme-eigenvalue solve since the last reset."""
+        mj, ns = C.c_double(), C.c_int64()
+        _check(_lib.spec_lanczos_iterations(self._h, 1 if reset else 0, C.byref(mj), C.byref(ns)))
+        return dict(mean_j=mj.value, solves=ns.value)
+
     def walk_trace(self, chain_ids, steps: int, L: float, rho: int, seed: int, max_refl: int,
-                   kind: int = BILLIARD, T: float = 1.0) -> list:
+                   kind: int = BILLIARD, T: Optional[float] = None) -> list:
         """First max_refl reflections of the given global chain ids (parity entry)."""
         ids = np.ascontiguousarray(np.asarray(chain_ids, dtype=np.int64))
         k = len(ids)

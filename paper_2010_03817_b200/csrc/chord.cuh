@@ -77,6 +77,10 @@ struct ChordParams {
     double Temp;
     double* tlast;  // t+ of the last hit (velocity at the hit = v - (c/T) t+)
     int* jlast;     // Lanczos iterations of the chain's previous call (first-check hint)
+    unsigned long long* jsum;  // [0] sum of Lanczos iterations J, [1] Lanczos solves (measured flop model)
+    int wkind;      // walk kind (SPEC_WALK_*): 2 = Hit-and-Run, 3 = coordinate Hit-and-Run
+    int need_tmin;  // the chord must return t- as well (oracle mode, Hit-and-Run walks)
+    int hnr_boltz;  // Hit-and-Run for exp(-c^T x / Temp) instead of the uniform law
     // K2 split into factor / Lanczos / tail kernels: per-slot work buffers
     double* wM;     // M = -L^{-1} A(v) L^{-T} (mdp x mdp rows, leading dimension ld)
     double* wL;     // L (lower incl. diagonal, rows of leading dimension ld)
@@ -239,8 +243,10 @@ __device__ void step_start(const Team& T, int slot, long long gidv, int step, in
     uint2 key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
     const double two_pi = 6.283185307179586476925286766559;
     double ss = 0.0;
-    double eta_local = 0.0;
+    double eta_local = 0.0, u2_local = 0.0;
+    // kind 3 (W-CHnR) needs no normals: only block nb (eta and the coordinate draw)
     for (int j = T.tid; j <= nb; j += T.nthr) {
+        if (kind == 3 && j < nb) continue;
         uint4 w = philox4x32_10(make_uint4((uint32_t)j, (uint32_t)step, (uint32_t)gidv, tag), key);
         if (j < nb) {
             double u0 = u01(w.x, w.y), u1 = u01(w.z, w.w);
@@ -256,20 +262,29 @@ __device__ void step_start(const Team& T, int slot, long long gidv, int step, in
             }
         } else {
             eta_local = u01(w.x, w.y);
+            u2_local = u01(w.z, w.w);
         }
     }
-    double eta;
+    double eta, u2;
     if (CTA) {
-        if (T.tid == nb % T.nthr) red[40] = eta_local;
+        if (T.tid == nb % T.nthr) {
+            red[40] = eta_local;
+            red[41] = u2_local;
+        }
         ss = block_sum(T, ss, red);
         eta = red[40];
+        u2 = red[41];
     } else {
         ss = warp_sum(ss);
         eta = __shfl_sync(0xffffffffu, eta_local, nb % 32);
+        u2 = __shfl_sync(0xffffffffu, u2_local, nb % 32);
     }
-    if (kind == 0) {
+    if (kind == 0 || kind == 2) {  // v ~ U(sphere): billiard (Alg. 5) and W-HnR (Alg. 4)
         double inv = 1.0 / sqrt(ss);
         for (int i = T.tid; i < n; i += T.nthr) v[i] *= inv;
+    } else if (kind == 3) {  // v = e_j, j = floor(u2 n) (R29)
+        const int jc = min(n - 1, (int)(u2 * (double)n));
+        for (int i = T.tid; i < n; i += T.nthr) v[i] = (i == jc) ? 1.0 : 0.0;
     }
     const double* x = X + (size_t)slot * np;
     double* xs = Xs + (size_t)slot * np;
@@ -277,8 +292,20 @@ __device__ void step_start(const Team& T, int slot, long long gidv, int step, in
     const double* ax = AX + (size_t)slot * mtp;
     double* axs = AXs + (size_t)slot * mtp;
     for (int i = T.tid; i < mt; i += T.nthr) axs[i] = ax[i];
-    if (T.tid == 0) ell[slot] = (kind == 0) ? -Lpar * log(eta) : Lpar * eta;
+    // ell: billiard -L ln eta, HMC L eta (Alg. 5 / Alg. 6 line 1); Hit-and-Run keeps eta (the
+    // position of the next point on the chord)
+    if (T.tid == 0) ell[slot] = (kind == 0) ? -Lpar * log(eta) : (kind == 1 ? Lpar * eta : eta);
     if (CTA) __syncthreads(); else __syncwarp();
+}
+
+// A point of the chord [tm, tp] from the restriction of exp(-c^T x / T) to the line x + t v,
+// a = c^T v / T (W-HnR for the Boltzmann law, sec:optimization P:1408-1424): truncated
+// exponential by its inverse CDF from the end of largest density (log1p / expm1 form);
+// |a| (tp - tm) < 1e-12: the uniform point.
+__device__ __forceinline__ double boltz_chord_point(double tm, double tp, double a, double eta) {
+    const double d = tp - tm, b = fabs(a) * d;
+    const double s = (b < 1e-12) ? eta * d : -log1p(eta * expm1(-b)) / fabs(a);
+    return a >= 0.0 ? tm + s : tp - s;
 }
 
 // ---------------------------------------------------------------- K2

@@ -1675,17 +1675,21 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
                 {
                     // vector area + 64 slack doubles: [0,32) partial sums, [32,40) check results
                     const int oVec = (int)(vec - smem_dyn), oRed = oVec + NVEC2 * vl;
-                    J = lanczos_reg<NT, KC>((int)(Bd - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.mode == 1, oVec,
+                    J = lanczos_reg<NT, KC>((int)(Bd - smem_dyn), (int)(Qm - smem_dyn), md, mdp, ld, P.need_tmin != 0, oVec,
                                             vl, oRed, 0, P.prof);
                     if (P.jlast && T.tid == 0) P.jlast[slot] = J;
                     theta_max = smem_dyn[oRed + 32 + 4];
                     theta_min = smem_dyn[oRed + 32 + 5];
                 }
                 else
-                    J = lanczos_run(T, Bd, Qm, md, mdp, ld, true, P.mode == 1, wv, hb, al, be, sv, sv2, dp, dm, red,
+                    J = lanczos_run(T, Bd, Qm, md, mdp, ld, true, P.need_tmin != 0, wv, hb, al, be, sv, sv2, dp, dm, red,
                                     &sh_i[3], &sh_d[4], P.prof, &theta_max, &theta_min, vec + 17 * vl, vec,
                                     vec + 4 * vl, vec + 9 * vl, (int)(vec - smem_dyn) + 48);
                 lanczos_J = J;
+                if (P.jsum && T.tid == 0) {
+                    atomicAdd(&P.jsum[0], (unsigned long long)J);
+                    atomicAdd(&P.jsum[1], 1ull);
+                }
                 if (P.prof && T.tid == 0) atomicAdd(&P.prof[10], (unsigned long long)J);
                 PROF_MARK(4);
                 if (T.tid == 0) {

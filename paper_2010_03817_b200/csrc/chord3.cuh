@@ -213,10 +213,14 @@ __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {
         }
         const int mdp = (md + 7) & ~7;
         const double* Mw = P.wM + (size_t)slot * P.w_mstride;
-        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.mode == 1 && !P.zall, oVec, vl, oRed,
+        const int J = lanczos_reg<NT, KC, true, false>(-1, oQ, md, mdp, ld, P.need_tmin && !P.zall, oVec, vl, oRed,
                                                        P.zall ? SW_FIRST_CHECK_PCT_HMC : 0,
                                                        P.prof, Mw, 0);
         if (P.jlast && tid == 0) P.jlast[slot] = J;
+        if (P.jsum && tid == 0) {
+            atomicAdd(&P.jsum[0], (unsigned long long)J);
+            atomicAdd(&P.jsum[1], 1ull);
+        }
         const double theta_max = smem_dyn[oRed + 32 + 4];
         const double theta_min = smem_dyn[oRed + 32 + 5];
         const double* al = smem_dyn + oVec + V_AL * vl;
@@ -417,7 +421,8 @@ __global__ void __launch_bounds__(NT, SW_TAIL_CTAS) tail_kernel(ChordParams P) {
         const bool defl = (bnd == 0);
         long long t_prof = clock64();
         __syncthreads();
-        const bool dense_y = !outward && !failed && md >= 1 && theta_max > 0.0;
+        // (Hit-and-Run walks never reflect: no kernel vector needed)
+        const bool dense_y = !outward && !failed && md >= 1 && theta_max > 0.0 && !(P.mode == 0 && P.wkind >= 2);
         if (dense_y) {
             // L (lower rows, 16-byte segments [0, i+1]) into shared memory asynchronously
             const int mdp = (md + 7) & ~7;

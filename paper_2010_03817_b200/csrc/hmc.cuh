@@ -410,6 +410,10 @@ __global__ void __launch_bounds__(NT, 1) hmc_kernel(ChordParams P) {
                         double th_top, th_bot;
                         int J = lanczos_run(T, Nw, Qb, m, mp, ld, false, true, wv, hb, al, be, sv, sv2, dp, dm, red,
                                             &sh_i[3], &sh_d[4], P.prof, &th_top, &th_bot);
+                        if (P.jsum && T.tid == 0) {
+                            atomicAdd(&P.jsum[0], (unsigned long long)J);
+                            atomicAdd(&P.jsum[1], 1ull);
+                        }
                         a_min = th_bot;
                         // z = Q s (bottom Ritz vector), y_k = K^{-T} z
                         for (int e = T.tid; e < mp; e += T.nthr) {

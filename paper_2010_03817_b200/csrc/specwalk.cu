@@ -127,6 +127,7 @@ struct spec_ctx {
     int chord_grid_max = 0;
     int num_sms = 0;
     long long* dstats = nullptr;
+    unsigned long long* jsum = nullptr;  // Lanczos iteration counters (spec_lanczos_iterations)
     unsigned long long* prof = nullptr;
     double* lsave = nullptr;
     long long lsave_stride = 0;
@@ -274,6 +275,7 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
     CK(zalloc(&ctx->ball_c, ctx->np));
     CK(zalloc(&ctx->c0, ctx->np));
     CK(zalloc(&ctx->dstats, 8));
+    CK(zalloc(&ctx->jsum, 2));
     if (getenv("SPECWALK_PROF")) CK(zalloc(&ctx->prof, 32));
     // K2 variant: M register-resident (m <= 128) with matrices in shared memory,
     // else matrices + Lanczos basis in a per-CTA global scratch slice.
@@ -390,7 +392,7 @@ extern "C" int spec_destroy(spec_ctx* ctx) {
         free_obuf(*(OracleBuf*)ctx->obuf);
         delete (OracleBuf*)ctx->obuf;
     }
-    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->c0, ctx->scratch, ctx->dstats, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->c0, ctx->scratch, ctx->dstats, ctx->jsum, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -476,11 +478,15 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.cvec = ctx->c;
     P.tlast = b.tlast;
     P.jlast = b.jlast;
+    P.jsum = ctx->jsum;
     P.wM = b.wM;
     P.wL = b.wL;
     P.wS = b.wS;
     P.w_mstride = (long long)roundup(ctx->m, 8) * ctx->ld;
     P.w_sstride = s_stride(roundup(ctx->m, 8));
+    P.need_tmin = (mode == 1);
+    P.wkind = 0;
+    P.hnr_boltz = 0;
     return P;
 }
 
@@ -890,6 +896,9 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
     P.chain_base = p->chain_begin;
     P.gid = dgid;
     P.Temp = p->T;
+    P.wkind = p->kind;
+    P.need_tmin = (p->kind == SPEC_WALK_HNR || p->kind == SPEC_WALK_CHNR) ? 1 : 0;
+    P.hnr_boltz = (P.need_tmin && p->T > 0.0 && std::isfinite(p->T)) ? 1 : 0;
     NormalParams& Q = W.Q;
     Q = normal_params(ctx, 0);
     Q.steps_total = (int)p->steps;
@@ -936,7 +945,13 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             cudaEvent_t* e = W.timing ? &ev[7 * k] : nullptr;
             CK(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));
             if (e) CK(cudaEventRecord(e[0], ctx->stream));
-            launch_gemm_av(ctx, b.V, list, b.counters, count, b.AV, nullptr);  // K1
+            if (W.p.kind == SPEC_WALK_CHNR) {  // A(e_j) = A_j: a row copy
+                coord_dir_kernel<<<std::min(count, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
+                    list, b.counters, count, b.V, ctx->np, ctx->n, ctx->Ahat, ctx->mtp, b.AV);
+                ctx->launches++;
+            } else {
+                launch_gemm_av(ctx, b.V, list, b.counters, count, b.AV, nullptr);  // K1
+            }
             if (e) CK(cudaEventRecord(e[1], ctx->stream));
             P.list = list;
             P.count_dev = b.counters;
@@ -946,15 +961,19 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
                 if (rc) return rc;
             } else launch_chord(ctx, P, count, (e && ctx->k2_split) ? &e[5] : nullptr);  // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
-            launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
-            if (e) CK(cudaEventRecord(e[3], ctx->stream));
-            Q.nlist = b.nlist;
-            Q.ncount = b.counters + 2;
-            Q.count_host = count;
-            int nb = (count + 7) / 8;
-            if (nb > 65535 * 4) nb = 65535 * 4;
-            normal_reflect_kernel<<<nb, 256, 0, ctx->stream>>>(Q);  // K4
-            ctx->launches++;
+            if (W.p.kind == SPEC_WALK_BILLIARD || W.p.kind == SPEC_WALK_HMC) {  // Hit-and-Run never reflects
+                launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
+                if (e) CK(cudaEventRecord(e[3], ctx->stream));
+                Q.nlist = b.nlist;
+                Q.ncount = b.counters + 2;
+                Q.count_host = count;
+                int nb = (count + 7) / 8;
+                if (nb > 65535 * 4) nb = 65535 * 4;
+                normal_reflect_kernel<<<nb, 256, 0, ctx->stream>>>(Q);  // K4
+                ctx->launches++;
+            } else if (e) {
+                CK(cudaEventRecord(e[3], ctx->stream));
+            }
             if (e) CK(cudaEventRecord(e[4], ctx->stream));
             W.k2_items += count;
             ++W.rounds;
@@ -1073,7 +1092,11 @@ static int run_walk(spec_ctx* ctx, const spec_walk_params* p, const double* dx0,
 static int gather_f64(spec_ctx* ctx, int rc_local, const std::vector<double>& local, std::vector<double>& global);
 static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
-    if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC) return fail(SPEC_EINVAL, "unknown walk kind");
+    if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC && p->kind != SPEC_WALK_HNR &&
+        p->kind != SPEC_WALK_CHNR)
+        return fail(SPEC_EINVAL, "unknown walk kind");
+    if ((p->kind == SPEC_WALK_HNR || p->kind == SPEC_WALK_CHNR) && p->T > 0.0 && std::isfinite(p->T) && !ctx->has_obj)
+        return fail(SPEC_EINVAL, "Hit-and-Run for exp(-c^T x / T) needs spec_set_objective (T = inf: uniform)");
     if (p->kind == SPEC_WALK_HMC) {
         if (!ctx->has_obj) return fail(SPEC_EINVAL, "HMC needs spec_set_objective");
         if (!(p->T > 0.0) || !std::isfinite(p->T)) return fail(SPEC_EINVAL, "HMC needs T > 0");
@@ -1310,6 +1333,18 @@ extern "C" int spec_kernel_timing(spec_ctx* ctx, int enable) {
     for (int i = 0; i < 4; ++i) W.kms[i] = 0.0, W.kcount[i] = 0;
     for (int i = 0; i < 3; ++i) W.k2ms[i] = 0.0;
     W.k2_items = 0;
+    return SPEC_OK;
+}
+
+extern "C" int spec_lanczos_iterations(spec_ctx* ctx, int reset, double* mean_j, int64_t* solves) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    CK(cudaSetDevice(ctx->dev));
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, ctx->jsum, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    if (reset) CK(cudaMemsetAsync(ctx->jsum, 0, sizeof(h), ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (mean_j) *mean_j = h[1] ? (double)h[0] / (double)h[1] : 0.0;
+    if (solves) *solves = (int64_t)h[1];
     return SPEC_OK;
 }
 

@@ -245,6 +245,29 @@ __global__ void stats_kernel(int chains, const long long* calls, const long long
     if (threadIdx.x < 7) atomicAdd((unsigned long long*)&out[threadIdx.x], (unsigned long long)acc[threadIdx.x]);
 }
 
+// W-CHnR direction contraction: v = e_j, so A(v) = A_j is row j of Ahat -- a
+// copy instead of the K1 GEMM (the O(m^2) construction of the pencil).  One CTA per chain.
+__global__ void __launch_bounds__(256) coord_dir_kernel(const int* list, const int* count_dev, int count_host,
+                                                        const double* V, int np, int n, const double* Ahat,
+                                                        int mtp, double* AV) {
+    __shared__ int jj;
+    const int count = count_dev ? min(*count_dev, count_host) : count_host;
+    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
+        const int slot = list ? list[rr] : rr;
+        if (slot < 0) continue;
+        if (threadIdx.x == 0) jj = 0;
+        __syncthreads();
+        const double* v = V + (size_t)slot * np;
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            if (v[i] != 0.0) jj = i;  // exactly one non-zero entry
+        __syncthreads();
+        const double2* src = (const double2*)(Ahat + (size_t)jj * mtp);
+        double2* dst = (double2*)(AV + (size_t)slot * mtp);
+        for (int e = threadIdx.x; e < (mtp >> 1); e += blockDim.x) dst[e] = src[e];
+        __syncthreads();
+    }
+}
+
 __global__ void iota_kernel(int* list, int count) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x) list[i] = i;
 }

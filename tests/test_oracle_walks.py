@@ -251,3 +251,21 @@ def test_hnr_uniform_moments(kind, body):
     assert abs(x2.mean() - ex2) <= 4 * se, (x2.mean(), ex2, se)
     mx = X.mean(1)
     assert abs(mx.mean()) <= 4 * mx.std(ddof=1) / np.sqrt(len(mx))
+
+
+@pytest.mark.parametrize("kind", [oracle.HNR, oracle.CHNR])
+def test_hnr_boltzmann_cube_moments(kind):
+    """W-HnR / W-CHnR with pi_l the restriction of exp(-c.x/T) (sec:optimization P:1408-1424)
+    on [-1,1]^n: independent truncated exponentials (P1, V7), moments by quadrature."""
+    n = 3
+    lmi = oracle.Lmi(specgen.cube_only(n))
+    c = np.array([1.0, -0.6, 2.5])
+    T = 0.7
+    X, st = oracle.walk(lmi, kind, 8, 0, 3000, 30, 1.0, 10, T=T, c=c)
+    assert st["calls"] == 3000 * 30
+    grid = np.linspace(-1, 1, 200001)
+    for i in range(n):
+        dens = np.exp(-c[i] * grid / T)
+        Z = np.trapezoid(dens, grid)
+        _check_moment(X[:, i], np.trapezoid(grid * dens, grid) / Z)
+        _check_moment(X[:, i] ** 2, np.trapezoid(grid ** 2 * dens, grid) / Z)

