@@ -268,6 +268,43 @@ typedef struct spec_expect_params {
 int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, const spec_expect_params* p, double* est,
                 double* stderr_out);
 
+/* sdp_anneal -- approximate min c^T x over S (eq:sdp P:1406, c from spec_set_objective) by
+ * simulated annealing (sec:optimization P:1408-1434, after Kalai-Vempala): sample
+ * pi_i ~ exp(-c^T x / T_i) with T_0 ~ R (S within the ball of radius R around the start) and
+ * T_{i+1} = max(T_i (1 - 1/sqrt(n)), 2^-40 T_0) (the floor: DESIGN.md R30), every chain
+ * warm-started from its previous point, the first
+ * (uniform) point from the billiard walk, the walk length 1 for HMC-r.
+ * p->chains independent chains (global, divisible by the world size; global ids key the
+ * RNG, tags purpose 4 / temperature index) -- the batched form of the paper's single chain.
+ *  best_x  : host, n doubles (may be NULL): the point of the smallest c^T x seen (end points of
+ *            every temperature, all chains).
+ *  history : host, p->iters doubles (may be NULL): that best value after each temperature.
+ * Stops after p->iters temperatures, or -- with a finite f_target -- once
+ * best - f_target <= eps |f_target| (the paper's protocol for Table tab:hmc_hnr).
+ * EINVAL: no objective, kind not HMC / HNR / CHNR, chains or iters out of range. */
+typedef struct spec_sdp_params {
+    int kind;          /* SPEC_WALK_HMC (the paper's W-HMC-r), SPEC_WALK_HNR or SPEC_WALK_CHNR */
+    int64_t chains;    /* independent annealing chains (global) */
+    int64_t iters;     /* number of temperatures (maximum) */
+    int64_t walk_len;  /* walk steps per temperature [1] */
+    int64_t burn;      /* billiard steps for the uniform start [10] */
+    double T0;         /* initial temperature [<= 0: R = max |x| over the start points] */
+    double L;          /* HMC-r trajectory length tau [<= 0: R] (ignored by Hit-and-Run) */
+    int64_t rho;       /* reflection bound [10 n] */
+    uint64_t seed;
+    double f_target;   /* known optimum, or NaN / inf for none */
+    double eps;        /* relative stop tolerance with f_target [0.05] */
+} spec_sdp_params;
+typedef struct spec_sdp_report {
+    double best;       /* smallest c^T x seen */
+    double last_min;   /* smallest c^T x among the last temperature's points */
+    double T0, T_final, L; /* T_final: the temperature after the last one run */
+    int64_t iters;     /* temperatures run */
+    int64_t calls;     /* boundary-oracle calls (all ranks) */
+    double device_ms;
+} spec_sdp_report;
+int sdp_anneal(spec_ctx* ctx, const spec_sdp_params* p, double* best_x, double* history, spec_sdp_report* out);
+
 /* Make the host wait for all work queued on the context stream. */
 int spec_sync(spec_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers timing with events. */

@@ -474,3 +474,47 @@ def expectation(inst, f_id: str, seed: int, chains: int, steps: int, L: float, r
     else:
         raise ValueError(f_id)
     return dict(est=float(vals.mean()), stderr=float(vals.std(ddof=1) / math.sqrt(chains)), calls=st["calls"])
+
+
+def sdp_anneal(inst, c, kind: int, chains: int, iters: int, walk_len: int = 1, burn: int = 10, T0: float = 0.0,
+               L: float = 0.0, rho: int = None, seed: int = 0, f_target: float = None, eps: float = 0.05,
+               nthreads: int = 0) -> dict:
+    """min c^T x over S (eq:sdp P:1406) by simulated annealing (sec:optimization P:1408-1434):
+    uniform start points by the billiard walk from 0 (`burn` steps), T_0 = R = the
+    largest |x| among them (S within R B_n) unless given, T_{i+1} = T_i (1 - 1/sqrt(n)),
+    `walk_len` steps of `kind` (HMC: Alg. 6 with tau = L, default R; HNR / CHNR: Hit-and-Run with
+    the Boltzmann pi_l) per temperature from each chain's previous point; best = the smallest
+    c^T x seen.  Stops early once best - f_target <= eps |f_target|.  The cooling
+    stops at T_0 2^-40 (R30: below it exp(-c^T x / T) lives under the rounding of x).
+    Tags: purpose 4, phase = temperature index + 1 (the start walk: phase 0)."""
+    n = inst.n
+    c = np.asarray(c, dtype=np.float64)
+    rho = 10 * n if rho is None else rho
+    lmi = Lmi(inst)
+    X, st = walk(lmi, BILLIARD, seed, 0, chains, burn, 2.0 * math.sqrt(n), rho, tag=4 << 28, nthreads=nthreads)
+    calls = st["calls"]
+    R = float(np.max(np.linalg.norm(X, axis=1)))
+    f = X @ c
+    best = float(f.min())
+    bx = X[int(np.argmin(f))].copy()
+    T = T0 if T0 > 0 else R
+    T0f = T
+    Lh = L if L > 0 else R
+    cool = 1.0 - 1.0 / math.sqrt(n)
+    hist = []
+    it = 0
+    while it < iters:
+        X, st = walk(lmi, kind, seed, 0, chains, walk_len, Lh, rho, x0=X, T=T, c=c, tag=(4 << 28) | (it + 1),
+                     nthreads=nthreads)
+        calls += st["calls"]
+        f = X @ c
+        if f.min() < best:
+            best = float(f.min())
+            bx = X[int(np.argmin(f))].copy()
+        hist.append(best)
+        T = max(T * cool, T0f * 2.0 ** -40)  # cooling floor (DESIGN.md R30)
+        it += 1
+        if f_target is not None and best - f_target <= eps * abs(f_target):
+            break
+    return dict(best=best, best_x=bx, history=hist, iters=it, T0=T0 if T0 > 0 else R, L=Lh, calls=calls,
+                last_min=float(f.min()))

@@ -1006,10 +1006,28 @@ typedef struct {
 /* One step of the Billiard walk (Alg. 5; readings R4, R5) or
  * of HMC-r (Alg. 6; eq:boltz_ode).  Returns 0, or 2 if the start
  * point is not interior. */
+/* A point of the chord [t-, t+] drawn from pi_l (Alg. 4 line 4) for the Boltzmann law
+ * pi ~ exp(-c^T x / T) (sec:optimization P:1420-1424): along x + t v the density is
+ * proportional to exp(-a t), a = c^T v / T, i.e. a truncated exponential; inverse CDF with
+ * s = -log(1 - eta (1 - exp(-|a| d))) / |a| measured from the end where the density is largest
+ * (d = t+ - t-), written with log1p / expm1.  |a| d < 1e-12: the uniform point s = eta d.
+ * s is kept in [2^-40 d, (1 - 2^-40) d] (R30): at temperatures where T / |a| falls
+ * below the rounding of x the drawn point would otherwise land ON the boundary. */
+static double boltz_chord_point(double tm, double tp, double a, double eta) {
+    double d = tp - tm, b = fabs(a) * d, s;
+    if (b < 1e-12)
+        s = eta * d;
+    else
+        s = -log1p(eta * expm1(-b)) / fabs(a);
+    s = fmin(fmax(s, 0x1p-40 * d), (1.0 - 0x1p-40) * d);
+    return a >= 0.0 ? tm + s : tp - s;
+}
+
 /* One step of Hit-and-Run (Alg. 4 alg:hitandrun P:939-965) or of coordinate-directions
  * Hit-and-Run (W-CHnR) for the uniform law: v ~ U(sphere) (HnR) or v = e_j with
  * j uniform in [n] (CHnR); (t-, t+) = INTERSECTION (one chord, Lemma 3); the next point is
- * uniform on [p + t- v, p + t+ v]: p += (t- + eta (t+ - t-)) v, and F(p) is carried as
+ * drawn from pi restricted to [p + t- v, p + t+ v] -- uniform: p += (t- + eta (t+ - t-)) v;
+ * Boltzmann (c given, 0 < T < inf): boltz_chord_point -- and F(p) is carried as
  * F += t F1(v) (for e_j, F1 = A_j: the O(m^2) update of P:988-995). */
 static int hnr_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, uint32_t step, walk_ws* W,
                     orc_stats* st) {
@@ -1036,7 +1054,14 @@ static int hnr_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, 
     int rc = orc_chord(L, W->x, W->F, W->F1, W->v, -1, NULL, r);
     st->calls += 1;
     if (rc) return rc;
-    double t = r->t_minus + eta * (r->t_plus - r->t_minus);
+    double t;
+    if (p->c && p->T > 0.0 && isfinite(p->T)) { /* Boltzmann pi_l (sec:optimization) */
+        double cv = 0.0;
+        for (int i = 0; i < n; ++i) cv += p->c[i] * W->v[i];
+        t = boltz_chord_point(r->t_minus, r->t_plus, cv / p->T, eta);
+    } else { /* uniform pi_l */
+        t = r->t_minus + eta * (r->t_plus - r->t_minus);
+    }
     for (int i = 0; i < n; ++i) W->x[i] += t * W->v[i];
     for (size_t e = 0; e < mm; ++e) W->F[e] += t * W->F1[e];
     return 0;

@@ -35,7 +35,7 @@ EXPORTS = (
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
     "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
-    "spec_lanczos_iterations",
+    "spec_lanczos_iterations", "sdp_anneal",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -61,6 +61,17 @@ class VolumeReport(C.Structure):
 class ExpectParams(C.Structure):
     _fields_ = [("chains", C.c_int64), ("steps", C.c_int64), ("L", C.c_double), ("rho", C.c_int64),
                 ("b1", C.c_double), ("b2", C.c_double)]
+
+
+class SdpParams(C.Structure):
+    _fields_ = [("kind", C.c_int), ("chains", C.c_int64), ("iters", C.c_int64), ("walk_len", C.c_int64),
+                ("burn", C.c_int64), ("T0", C.c_double), ("L", C.c_double), ("rho", C.c_int64), ("seed", C.c_uint64),
+                ("f_target", C.c_double), ("eps", C.c_double)]
+
+
+class SdpReport(C.Structure):
+    _fields_ = [("best", C.c_double), ("last_min", C.c_double), ("T0", C.c_double), ("T_final", C.c_double),
+                ("L", C.c_double), ("iters", C.c_int64), ("calls", C.c_int64), ("device_ms", C.c_double)]
 
 
 class SpecError(RuntimeError):
@@ -130,6 +141,7 @@ def load(build_if_missing: bool = True):
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
     l.spec_k2_phase_times.argtypes = [C.c_void_p, _dp]
     l.spec_lanczos_iterations.argtypes = [C.c_void_p, C.c_int, _dp, _lp]
+    l.sdp_anneal.argtypes = [C.c_void_p, C.POINTER(SdpParams), _dp, _dp, C.POINTER(SdpReport)]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
     l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
@@ -225,6 +237,19 @@ class Spectrahedron:
         est, se = C.c_double(), C.c_double()
         _check(_lib.expectation(self._h, f_id, float(T), seed, C.byref(p), C.byref(est), C.byref(se)))
         return dict(est=est.value, stderr=se.value)
+
+    def sdp_anneal(self, kind: int, chains: int, iters: int, seed: int = 0, walk_len: int = 0, burn: int = 0,
+                   T0: float = 0.0, L: float = 0.0, rho: int = 0, f_target: Optional[float] = None,
+                   eps: float = 0.0) -> dict:
+        """min c^T x over S by simulated annealing (eq:sdp P:1406, sec:optimization P:1408-1434)."""
+        p = SdpParams(kind, chains, iters, walk_len, burn, float(T0), float(L), rho, seed,
+                      float("nan") if f_target is None else float(f_target), float(eps))
+        bx = np.empty(self.n)
+        hist = np.full(iters, np.nan)
+        r = SdpReport()
+        _check(_lib.sdp_anneal(self._h, C.byref(p), _p(bx), _p(hist), C.byref(r)))
+        return dict(best=r.best, best_x=bx, history=hist[: r.iters], iters=r.iters, T0=r.T0, T_final=r.T_final,
+                    L=r.L, calls=r.calls, device_ms=r.device_ms, last_min=r.last_min)
 
     def kernel_launches(self) -> int:
         return int(_lib.spec_kernel_launches(self._h))

@@ -32,7 +32,9 @@ constexpr int NVEC2 = 20;
 #define SW_PRO_RUN 1
 #endif
 #ifndef SW_PRO_TAU
-#define SW_PRO_TAU 1e-10  // reorthogonalise once an omega estimate exceeds this (sqrt(eps) ~ 1.5e-8)
+#define SW_PRO_TAU 1e-13  // reorthogonalise once an omega estimate exceeds this: at 1e-10 the Ritz
+                          // vector (the normal) carried errors up to 4e-9 at m = 200 and 13 of 64
+                          // configs[4] trajectories left 1e-8 by reflection 20 (profiles/r2c_*); -1.2%
 #endif
 #ifndef SW_CHECK_STEP0
 #define SW_CHECK_STEP0 4    // iterations from the first check to the second (no rate known yet; measured)

@@ -1708,3 +1708,152 @@ extern "C" int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, con
     if (stderr_out) *stderr_out = std::sqrt(ss / (Nd - 1.0) / Nd);
     return SPEC_OK;
 }
+
+// ---------------------------------------------------------------- SDP by simulated annealing (sec:optimization)
+// min c^T x over S (eq:sdp P:1406) by sampling exp(-c^T x / T_i) with T_0 ~ R and
+// T_{i+1} = T_i (1 - 1/sqrt(n)), warm-starting every chain from its previous
+// point, walk length 1 for HMC-r (Fig. hmc_hnr), the first (uniform)
+// point by the billiard walk.  chains run independently; the reported point is the
+// best c^T x over all chains and temperatures.  Tags: purpose 4, phase = temperature index + 1.
+extern "C" int sdp_anneal(spec_ctx* ctx, const spec_sdp_params* sp, double* best_x, double* history,
+                          spec_sdp_report* out) {
+    if (!ctx || !sp || !out) return fail(SPEC_EINVAL, "null argument");
+    SW_NOT_DURING_WALK(ctx);
+    if (!ctx->has_obj) return fail(SPEC_EINVAL, "sdp_anneal needs the objective (spec_set_objective)");
+    if (sp->kind != SPEC_WALK_HMC && sp->kind != SPEC_WALK_HNR && sp->kind != SPEC_WALK_CHNR)
+        return fail(SPEC_EINVAL, "sdp_anneal: kind must be HMC, HNR or CHNR");
+    if (sp->iters < 1 || sp->iters > (1 << 27)) return fail(SPEC_EINVAL, "sdp_anneal: iters out of range");
+    const int n = ctx->n, np = ctx->np;
+    const int W = ctx->has_comm ? ctx->comm.world : 1, R = ctx->has_comm ? ctx->comm.rank : 0;
+    if (sp->chains < 1 || sp->chains % W) return fail(SPEC_EINVAL, "chains must be >= 1 and divisible by world");
+    const long long Cl = sp->chains / W, begin = (long long)R * Cl;
+    const long long walk_len = sp->walk_len > 0 ? sp->walk_len : 1;
+    const long long burn = sp->burn > 0 ? sp->burn : 10;
+    const long long rho = sp->rho > 0 ? sp->rho : 10LL * n;
+    const double eps = sp->eps > 0.0 ? sp->eps : 0.05;
+    CK(cudaSetDevice(ctx->dev));
+    std::vector<double> hc(n);
+    CK(cudaMemcpyAsync(hc.data(), ctx->c, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    struct EventGuard {
+        cudaEvent_t e = nullptr;
+        ~EventGuard() {
+            if (e) cudaEventDestroy(e);
+        }
+    } g0, g1;
+    CK(cudaEventCreate(&g0.e));
+    CK(cudaEventCreate(&g1.e));
+    CK(cudaEventRecord(g0.e, ctx->stream));
+    DevBuf dX, df;
+    CK(dX.alloc(sizeof(double) * (size_t)Cl * n));
+    CK(df.alloc(sizeof(double) * (size_t)Cl));
+    long long calls = 0;
+    auto run = [&](int kind, long long steps, double L, double T, uint32_t tag, bool start_origin) -> int {
+        spec_walk_params p;
+        p.kind = kind; p.chain_begin = begin; p.chains = Cl; p.steps = steps; p.L = L; p.rho = rho;
+        p.seed = sp->seed; p.tag = tag; p.T = T;
+        spec_walk_stats st;
+        int rc2 = walk_entry(ctx, &p, start_origin ? nullptr : dX.as<double>(), 1, nullptr, nullptr, dX.as<double>(),
+                             &st, false);
+        calls += st.calls;
+        return rc2;
+    };
+    // local best (value, x) of the current end points -> gathered, min in rank order
+    double best = HUGE_VAL, fmin_now = HUGE_VAL;
+    std::vector<double> bx(n, 0.0);
+    auto update_best = [&](int rc_in) -> int {
+        std::vector<double> loc(n + 1, 0.0), glob;
+        int rc2 = rc_in;
+        if (!rc2) {
+            rc2 = [&]() -> int {
+                fvalue_kernel<<<(int)std::min<long long>((Cl + 7) / 8, 65535), 256, 0, ctx->stream>>>(
+                    (int)Cl, n, np, ctx->cb.X, ctx->c, SPEC_F_LINEAR_C, 0.0, 0.0, df.as<double>());
+                ctx->launches++;
+                std::vector<double> fl((size_t)Cl);
+                CK(cudaMemcpyAsync(fl.data(), df.p, sizeof(double) * Cl, cudaMemcpyDeviceToHost, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+                long long a = 0;
+                for (long long j = 1; j < Cl; ++j)
+                    if (fl[(size_t)j] < fl[(size_t)a]) a = j;
+                loc[0] = fl[(size_t)a];
+                CK(cudaMemcpyAsync(loc.data() + 1, dX.as<double>() + (size_t)a * n, sizeof(double) * n,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+                return SPEC_OK;
+            }();
+        }
+        rc2 = gather_f64(ctx, rc2, loc, glob);
+        if (rc2) return rc2;
+        int rb = 0;
+        for (int r = 1; r < W; ++r)
+            if (glob[(size_t)r * (n + 1)] < glob[(size_t)rb * (n + 1)]) rb = r;
+        fmin_now = glob[(size_t)rb * (n + 1)];
+        if (fmin_now < best) {
+            best = fmin_now;
+            std::copy(glob.begin() + (size_t)rb * (n + 1) + 1, glob.begin() + (size_t)(rb + 1) * (n + 1), bx.begin());
+        }
+        return SPEC_OK;
+    };
+    // 1. uniform starting points (billiard from the origin)
+    int rc = run(SPEC_WALK_BILLIARD, burn, 2.0 * std::sqrt((double)n), 1.0, (4u << 28), true);
+    // T_0 = R: the largest distance of a burned-in point from the start (S within R B_n)
+    double Rn = 0.0;
+    {
+        std::vector<double> loc(1, 0.0), glob;
+        if (!rc) {
+            rc = [&]() -> int {
+                std::vector<double> X((size_t)Cl * n);
+                CK(cudaMemcpyAsync(X.data(), dX.p, sizeof(double) * X.size(), cudaMemcpyDeviceToHost, ctx->stream));
+                CK(cudaStreamSynchronize(ctx->stream));
+                for (long long j = 0; j < Cl; ++j) {
+                    double s2 = 0.0;
+                    for (int i = 0; i < n; ++i) s2 += X[(size_t)j * n + i] * X[(size_t)j * n + i];
+                    loc[0] = std::fmax(loc[0], std::sqrt(s2));
+                }
+                return SPEC_OK;
+            }();
+        }
+        rc = gather_f64(ctx, rc, loc, glob);
+        if (rc) return rc;
+        for (double v : glob) Rn = std::fmax(Rn, v);
+    }
+    rc = update_best(SPEC_OK);
+    if (rc) return rc;
+    double T = sp->T0 > 0.0 ? sp->T0 : Rn;
+    const double T0v = T;
+    const double L = sp->L > 0.0 ? sp->L : Rn;
+    const double cool = 1.0 - 1.0 / std::sqrt((double)n);
+    long long it = 0;
+    const bool have_target = std::isfinite(sp->f_target);
+    for (; it < sp->iters; ++it) {
+        rc = run(sp->kind, walk_len, L, T, (4u << 28) | (uint32_t)(it + 1), false);
+        rc = update_best(rc);
+        if (rc) return rc;
+        if (history) history[it] = best;
+        T = std::fmax(T * cool, T0v * 0x1p-40);  // cooling floor (R30)
+        if (have_target && best - sp->f_target <= eps * std::fabs(sp->f_target)) {
+            ++it;
+            break;
+        }
+    }
+    CK(cudaEventRecord(g1.e, ctx->stream));
+    CK(cudaEventSynchronize(g1.e));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, g0.e, g1.e));
+    std::vector<double> cl(1, (double)calls), clg;
+    rc = gather_f64(ctx, SPEC_OK, cl, clg);
+    if (rc) return rc;
+    double calls_tot = 0.0;
+    for (double v : clg) calls_tot += v;
+    memset(out, 0, sizeof(*out));
+    out->best = best;
+    out->last_min = fmin_now;
+    out->T0 = sp->T0 > 0.0 ? sp->T0 : Rn;
+    out->T_final = T;
+    out->L = L;
+    out->iters = it;
+    out->calls = (int64_t)calls_tot;
+    out->device_ms = ms;
+    if (best_x) std::copy(bx.begin(), bx.end(), best_x);
+    return SPEC_OK;
+}

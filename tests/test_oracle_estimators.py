@@ -99,3 +99,19 @@ def test_expectation_closed_forms():
     r = oracle.expectation(inst, "linear_c", 3, 800, 20, 2.0, 100, T=1.0, c=cc)
     truth = float(np.sum(cc * (1 / cc - 1 / np.tanh(cc))))
     assert abs(r["est"] - truth) <= 4 * r["stderr"], (r, truth)
+
+
+@pytest.mark.parametrize("kind", [oracle.HMC, oracle.HNR])
+@pytest.mark.parametrize("body", ["cube", "ball"])
+def test_sdp_anneal_lp_closed_forms(kind, body):
+    """SDP by simulated annealing (eq:sdp P:1406, sec:optimization P:1408-1434) on LPs with
+    closed-form optima (SURVEY 8(f)#2 pins): min c^T x over [-1,1]^n is -|c|_1 (at -sign c),
+    over the unit ball -|c|_2 (at -c/|c|).  The paper's stop rule: relative error <= 0.05."""
+    n = 5
+    c = np.array([0.9, -0.4, 0.2, 1.3, -0.7])
+    inst, fstar = (specgen.cube_dense(n), -np.abs(c).sum()) if body == "cube" else (specgen.ball(n), -np.linalg.norm(c))
+    r = oracle.sdp_anneal(inst, c, kind, 16, 80, walk_len=1 if kind == oracle.HMC else 4 * n, seed=3)
+    assert r["best"] >= fstar - 1e-9  # never below the optimum (every point is in S)
+    assert r["best"] - fstar <= 0.05 * abs(fstar), (r["best"], fstar)
+    assert abs(r["best_x"] @ c - r["best"]) <= 1e-12
+    assert all(a >= b for a, b in zip(r["history"], r["history"][1:]))  # monotone best
