@@ -57,7 +57,7 @@ def flops_per_call(n: int, m: int, k: int = LANCZOS_K) -> dict:
     return dict(total=contr + k2, k2=k2, k1=n * m * (m + 1), k3=n * m * (m + 1), lanczos=2 * k * m * m)
 
 
-def ncu_traffic_per_launch(tag: str):
+def ncu_traffic_per_launch(tag: str, kernel: str = ""):
     """DRAM bytes (read + write) of one launch of the dominant kernel, from the latest
     committed ncu --set full summary profiles/*<tag>.txt (tools/summarize_ncu.py), or None."""
     import glob
@@ -66,7 +66,13 @@ def ncu_traffic_per_launch(tag: str):
         return None
     vals = {}
     units = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    cur = ""
     for line in open(files[-1]):
+        if line.startswith("# kernel:"):
+            cur = line
+            continue
+        if kernel and cur and kernel not in cur:
+            continue
         parts = [p.strip() for p in line.split("|")]
         if len(parts) == 4 and parts[0] == "raw" and parts[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             try:
@@ -490,7 +496,11 @@ def run_ours(args):
             times.append(time.time() - t0)
             vols.append(r)
         vol = {"metric": "volume time at n=m=40 (configs[2], eps=0.1, 4096 chains/phase)", "unit": "s",
-               "seconds_mean": float(np.mean(times)), "seconds": times,
+               "seconds_mean": float(np.mean(times)),
+               "seconds_sd": float(np.std(times, ddof=1)) if len(times) > 1 else None,
+               "seeds": list(range(args.volume_seeds)), "seconds": times,
+               "volume_mean": float(np.mean([v["volume"] for v in vols])),
+               "volume_sd": float(np.std([v["volume"] for v in vols], ddof=1)) if len(vols) > 1 else None,
                "volume": [v["volume"] for v in vols], "std_rel": [v["std_rel"] for v in vols],
                "phases": [v["phases"] for v in vols], "oracle_calls": [v["calls"] for v in vols],
                "paper_context": "PAPER Table 2 S-40-40: 6.7 s on an i7-6700 for the paper's own (elongated) instance"}
@@ -564,7 +574,7 @@ def main():
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--e2e-chains", type=int, default=16384)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--volume-seeds", type=int, default=3)
+    ap.add_argument("--volume-seeds", type=int, default=10)
     ap.add_argument("--hmc-rounds", type=int, default=4)
     ap.add_argument("--m200-rounds", type=int, default=3)
     args = ap.parse_args()

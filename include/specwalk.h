@@ -271,7 +271,7 @@ int expectation(spec_ctx* ctx, int f_id, double T, uint64_t seed, const spec_exp
 /* sdp_anneal -- approximate min c^T x over S (eq:sdp P:1406, c from spec_set_objective) by
  * simulated annealing (sec:optimization P:1408-1434, after Kalai-Vempala): sample
  * pi_i ~ exp(-c^T x / T_i) with T_0 ~ R (S within the ball of radius R around the start) and
- * T_{i+1} = max(T_i (1 - 1/sqrt(n)), 2^-40 T_0) (the floor: DESIGN.md R30), every chain
+ * T_{i+1} = max(T_i (1 - 1/sqrt(n)), 2^-20 T_0) (the floor: DESIGN.md R30), every chain
  * warm-started from its previous point, the first
  * (uniform) point from the billiard walk, the walk length 1 for HMC-r.
  * p->chains independent chains (global, divisible by the world size; global ids key the

@@ -485,7 +485,8 @@ def sdp_anneal(inst, c, kind: int, chains: int, iters: int, walk_len: int = 1, b
     `walk_len` steps of `kind` (HMC: Alg. 6 with tau = L, default R; HNR / CHNR: Hit-and-Run with
     the Boltzmann pi_l) per temperature from each chain's previous point; best = the smallest
     c^T x seen.  Stops early once best - f_target <= eps |f_target|.  The cooling
-    stops at T_0 2^-40 (R30: below it exp(-c^T x / T) lives under the rounding of x).
+    stops at T_0 2^-20 (R30: the chord ends' accuracy near a face bounds how close to the
+    boundary the law can be followed).
     Tags: purpose 4, phase = temperature index + 1 (the start walk: phase 0)."""
     n = inst.n
     c = np.asarray(c, dtype=np.float64)
@@ -512,7 +513,7 @@ def sdp_anneal(inst, c, kind: int, chains: int, iters: int, walk_len: int = 1, b
             best = float(f.min())
             bx = X[int(np.argmin(f))].copy()
         hist.append(best)
-        T = max(T * cool, T0f * 2.0 ** -40)  # cooling floor (R30)
+        T = max(T * cool, T0f * 2.0 ** -20)  # cooling floor (R30)
         it += 1
         if f_target is not None and best - f_target <= eps * abs(f_target):
             break

@@ -1011,15 +1011,15 @@ typedef struct {
  * proportional to exp(-a t), a = c^T v / T, i.e. a truncated exponential; inverse CDF with
  * s = -log(1 - eta (1 - exp(-|a| d))) / |a| measured from the end where the density is largest
  * (d = t+ - t-), written with log1p / expm1.  |a| d < 1e-12: the uniform point s = eta d.
- * s is kept in [2^-40 d, (1 - 2^-40) d] (R30): at temperatures where T / |a| falls
- * below the rounding of x the drawn point would otherwise land ON the boundary. */
+ * s is kept in [2^-26 d, (1 - 2^-26) d] (R30): near a face the chord ends carry
+ * relative errors up to ~eps |M| / |theta|, and a closer point would land on the boundary. */
 static double boltz_chord_point(double tm, double tp, double a, double eta) {
     double d = tp - tm, b = fabs(a) * d, s;
     if (b < 1e-12)
         s = eta * d;
     else
         s = -log1p(eta * expm1(-b)) / fabs(a);
-    s = fmin(fmax(s, 0x1p-40 * d), (1.0 - 0x1p-40) * d);
+    s = fmin(fmax(s, 0x1p-26 * d), (1.0 - 0x1p-26) * d);
     return a >= 0.0 ? tm + s : tp - s;
 }
 

@@ -301,12 +301,13 @@ __device__ void step_start(const Team& T, int slot, long long gidv, int step, in
 // A point of the chord [tm, tp] from the restriction of exp(-c^T x / T) to the line x + t v,
 // a = c^T v / T (W-HnR for the Boltzmann law, sec:optimization P:1408-1424): truncated
 // exponential by its inverse CDF from the end of largest density (log1p / expm1 form);
-// |a| (tp - tm) < 1e-12: the uniform point.  s is kept in [2^-40 d, (1 - 2^-40) d] (DESIGN.md
-// R30: at T / |a| below the rounding of x the point would otherwise land on the boundary).
+// |a| (tp - tm) < 1e-12: the uniform point.  s is kept in [2^-26 d, (1 - 2^-26) d] (DESIGN.md
+// R30: near a face the chord ends carry relative errors up to ~eps |M| / |theta|, and a point
+// drawn closer than that would land on or outside the boundary).
 __device__ __forceinline__ double boltz_chord_point(double tm, double tp, double a, double eta) {
     const double d = tp - tm, b = fabs(a) * d;
     double s = (b < 1e-12) ? eta * d : -log1p(eta * expm1(-b)) / fabs(a);
-    s = fmin(fmax(s, 0x1p-40 * d), (1.0 - 0x1p-40) * d);
+    s = fmin(fmax(s, 0x1p-26 * d), (1.0 - 0x1p-26) * d);
     return a >= 0.0 ? tm + s : tp - s;
 }
 

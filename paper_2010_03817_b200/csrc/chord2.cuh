@@ -677,8 +677,13 @@ __device__ __noinline__ void lanczos_check(const int tid, const int oAl, const i
     sm[oShd + CK_RTOP] = res;
     sm[oShd + CK_TBOT] = thb;
     sm[oShd + CK_RBOT] = resb;
+    // both ends requested (t- and t+: oracle mode, Hit-and-Run): each residual relative to its
+    // own Ritz value (floored at 1e-6 |T|): near a face |T| is set by the near end, and a
+    // tolerance on |T| alone would leave the far end's t inaccurate (R30)
     const double tol = SW_LANCZOS_TOL * tnorm;
-    const bool done = exhausted || (res <= tol && resb <= tol);
+    const double tol_t = need_bot ? SW_LANCZOS_TOL * fmax(fabs(th), 1e-6 * tnorm) : tol;
+    const double tol_b = need_bot ? SW_LANCZOS_TOL * fmax(fabs(thb), 1e-6 * tnorm) : tol;
+    const bool done = exhausted || (res <= tol_t && resb <= tol_b);
     sm[oShd + CK_DONE] = done ? 1.0 : 0.0;
     if (done) return;
     // Ritz values of T_J are inner bounds for those of every larger T

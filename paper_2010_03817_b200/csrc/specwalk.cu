@@ -20,6 +20,7 @@
 #include "walk.cuh"
 #include "chord2.cuh"
 #include "chord3.cuh"
+#include "lanczos2.cuh"
 #include "hmc.cuh"
 #include "hmc2.cuh"
 #include "estimators.cuh"
@@ -120,6 +121,8 @@ struct spec_ctx {
     int k2_variant = 0;
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
+    int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    size_t l2_smem = 0;
     size_t f_smem = 0, l_smem = 0, t_smem = 0;
     size_t smem_bytes = 0;
     size_t g_smem = 0;  // global-scratch K2 variant: vector area in shared memory
@@ -374,6 +377,19 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->f_grid = of * ctx->num_sms;
         ctx->l_grid = ol * ctx->num_sms;
         ctx->t_grid = ot * ctx->num_sms;
+        // billiard / oracle K2b with two chains per SM (lanczos2.cuh) where M fits half an SM's
+        // shared memory; SPECWALK_LZ_OLD=1 keeps the register-resident lanczos_kernel (A/B)
+        if (ctx->k2_variant == 1 && !getenv("SPECWALK_LZ_OLD")) {
+            const Lz2Layout lo(mp, ctx->ld);
+            ctx->l2_smem = sizeof(double) * (size_t)lo.total;
+            int o2 = 0;
+            CK(cudaFuncSetAttribute(lanczos2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->l2_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, lanczos2_kernel, LZ2_NT, ctx->l2_smem));
+            if (o2 >= 1) {
+                ctx->lz2 = 1;
+                ctx->l2_grid = o2 * ctx->num_sms;
+            }
+        }
     }
     ctx->lsave_stride = (long long)mp * ctx->ld;
     CK(zalloc(&ctx->lsave, (size_t)ctx->lsave_stride * ctx->chord_grid_max));
@@ -500,7 +516,10 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
         } else if (ctx->k2_variant == 1) {
             factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
             if (sub) cudaEventRecord(sub[0], ctx->stream);
-            lanczos_kernel<512, 13><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
+            if (ctx->lz2)
+                lanczos2_kernel<<<g(ctx->l2_grid), LZ2_NT, ctx->l2_smem, ctx->stream>>>(P);
+            else
+                lanczos_kernel<512, 13><<<g(ctx->l_grid), 512, ctx->l_smem, ctx->stream>>>(P);
         } else {
             factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
             if (sub) cudaEventRecord(sub[0], ctx->stream);
@@ -652,6 +671,8 @@ static int launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
             lanczos_kernel<256, 8><<<g(ctx->hl_grid), 256, ctx->hl_smem, ctx->stream>>>(Pk);
         } else if (ctx->hmc_kc == 13) {
             hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
+            // (lanczos2_kernel's partially reorthogonalised Ritz vectors of -N_1 near the root were
+            // measured less accurate than the HMC parity bound: the fully reorthogonalised kernel)
             lanczos_kernel<512, 13><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
         } else {
             hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
@@ -1830,7 +1851,7 @@ extern "C" int sdp_anneal(spec_ctx* ctx, const spec_sdp_params* sp, double* best
         rc = update_best(rc);
         if (rc) return rc;
         if (history) history[it] = best;
-        T = std::fmax(T * cool, T0v * 0x1p-40);  // cooling floor (R30)
+        T = std::fmax(T * cool, T0v * 0x1p-20);  // cooling floor (R30)
         if (have_target && best - sp->f_target <= eps * std::fabs(sp->f_target)) {
             ++it;
             break;

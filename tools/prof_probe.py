@@ -14,11 +14,14 @@ for c in sys.argv[1:] or ["100:100:8192:40"]:
     S.walk_rounds(3)
     st0 = S.walk_stats_now()
     S.kernel_timing(True)
+    S.lanczos_iterations(reset=True)
     S.walk_rounds(rounds)
     st1 = S.walk_stats_now()
+    lz = S.lanczos_iterations(reset=True)
     kt = S.kernel_times()
     S.walk_end()
     calls = st1["calls"] - st0["calls"]
     k2 = kt["ms"]["K2_chord"]
     print(json.dumps(dict(n=n, m=m, chains=chains, rounds=rounds, calls=calls,
-                          k2_calls_per_s=calls / (k2 * 1e-3), kernel_ms=kt["ms"])), flush=True)
+                          k2_calls_per_s=calls / (k2 * 1e-3), kernel_ms=kt["ms"], k2_phases_ms=kt["k2_phases_ms"],
+                          lanczos=lz)), flush=True)

@@ -64,9 +64,12 @@ def full(path, out, header):
             "gpu__time_duration.sum", "sm__warps_active"]
     if len(rr) >= 3:
         h, units, vals = rr[0], rr[1], rr[2:]
+        kn = h.index("Kernel Name") if "Kernel Name" in h else None
         for v in vals:
+            kname = v[kn][:60] if kn is not None and kn < len(v) else ""
+            lines.append(f"# kernel: {kname}")
             for i, col in enumerate(h):
-                if any(col.startswith(w) for w in want):
+                if any(col.startswith(w) for w in want) and i < len(v):
                     lines.append(f"raw | {col} | {units[i]} | {v[i]}")
     with open(out, "w") as f:
         f.write(f"# {header}\n")
