@@ -344,14 +344,17 @@ def run_ours(args):
     tot_ms = max(sum(kt["ms"].values()), 1e-9)
     for k, v in phases.items():
         share[k] = v / tot_ms
+    k2cfg = S.k2_config()
     if phases.get("K2b_lanczos", 0.0) > 0.0:
-        dom, dom_ms = "K2b lanczos_kernel<512,13>", phases["K2b_lanczos"]
+        dom = "K2b " + ("lanczos2_kernel (256 threads, 2 CTAs/SM)" if "lanczos2" in k2cfg else "lanczos_kernel<512,13>")
+        dom_ms = phases["K2b_lanczos"]
         dom_flops = f["lanczos"]
     else:
         dom, dom_ms, dom_flops = "K2 chord_kernel2 (fused)", k2_ms, f["k2"]
     dom_avg_ms = dom_ms / max(k2_launches, 1)
     achieved = dom_flops * items_per_launch / (dom_avg_ms * 1e-3) / 1e12
-    tr = ncu_traffic_per_launch("lanczos_full_ncu") if dom.startswith("K2b") else None
+    tr = (ncu_traffic_per_launch("lanczos2_full_ncu" if "lanczos2" in dom else "lanczos_full_ncu")
+          if dom.startswith("K2b") else None)
     traffic = tr["bytes"] if tr else None
 
     # ---- end-to-end through the public host API (walk_sample with host buffers)
@@ -528,7 +531,7 @@ def run_ours(args):
                    "chains_per_gpu": local_chains,
                    "parallelism": f"{world} GPU(s) x {local_chains} chains, sharded by global chain id"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": dom,
+                     "traffic": traffic, "kernel": dom, "k2_config": k2cfg,
                      "flops_per_chain_call": dom_flops, "chain_calls_per_launch": items_per_launch,
                      "avg_launch_ms": dom_avg_ms,
                      "lanczos_j": J,

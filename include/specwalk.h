@@ -197,6 +197,8 @@ int spec_walk_stats_now(spec_ctx* ctx, spec_walk_stats* st);
  * number of chain slots K2 processed (including finished ones not yet compacted). */
 int spec_kernel_timing(spec_ctx* ctx, int enable);
 int spec_kernel_times(spec_ctx* ctx, double* ms4, int64_t* launches4, int64_t* k2_items);
+/* The chord (K2) launch configuration of this context, as text (evidence / logs). */
+const char* spec_k2_config(spec_ctx* ctx);
 /* Lanczos iterations per extreme-eigenvalue solve, counted on the device since creation or
  * the last reset (every billiard chord makes one solve; an HMC-r chord one per Weyl
  * iteration): *mean_j = sum J / solves.  reset != 0 zeroes the counters after reading.

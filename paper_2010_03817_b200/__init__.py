@@ -35,7 +35,7 @@ EXPORTS = (
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
     "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
-    "spec_lanczos_iterations", "sdp_anneal",
+    "spec_lanczos_iterations", "sdp_anneal", "spec_k2_config",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -141,6 +141,8 @@ def load(build_if_missing: bool = True):
     l.spec_kernel_times.argtypes = [C.c_void_p, _dp, _lp, _lp]
     l.spec_k2_phase_times.argtypes = [C.c_void_p, _dp]
     l.spec_lanczos_iterations.argtypes = [C.c_void_p, C.c_int, _dp, _lp]
+    l.spec_k2_config.argtypes = [C.c_void_p]
+    l.spec_k2_config.restype = C.c_char_p
     l.sdp_anneal.argtypes = [C.c_void_p, C.POINTER(SdpParams), _dp, _dp, C.POINTER(SdpReport)]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
@@ -250,6 +252,9 @@ class Spectrahedron:
         _check(_lib.sdp_anneal(self._h, C.byref(p), _p(bx), _p(hist), C.byref(r)))
         return dict(best=r.best, best_x=bx, history=hist[: r.iters], iters=r.iters, T0=r.T0, T_final=r.T_final,
                     L=r.L, calls=r.calls, device_ms=r.device_ms, last_min=r.last_min)
+
+    def k2_config(self) -> str:
+        return _lib.spec_k2_config(self._h).decode()
 
     def kernel_launches(self) -> int:
         return int(_lib.spec_kernel_launches(self._h))

@@ -23,6 +23,10 @@
 #pragma once
 #include "chord3.cuh"
 
+#ifndef SW_PRO_TAU2
+#define SW_PRO_TAU2 SW_PRO_TAU  // lanczos2's partial-reorthogonalisation threshold
+#endif
+
 namespace sw {
 
 constexpr int LZ2_NT = 256;
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
                                      ((k > 0) ? bkm * sm[oR1 + k - 1] : 0.0) - sm[Lo.oBe + j - 2] * sm[oR2 + k];
                         num += copysign(eps1 * (bk + bjm1), num);
                         v = num * sj;
-                        if (fabs(v) > SW_PRO_TAU) sm[Lo.oPart + 40 + (j & 1)] = 1.0;
+                        if (fabs(v) > SW_PRO_TAU2) sm[Lo.oPart + 40 + (j & 1)] = 1.0;
                     }
                     sm[oRj + k] = v;
                 }
@@ -227,24 +231,59 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
                     if (owner) sm[Lo.oW + tid] = wr;
                     if (tid == 0) sm[Lo.oPart + 40 + ((j + 1) & 1)] = 0.0;
                     __syncthreads();
-                    // h_i = q_i . w, i <= j: warp per dot (Q rows from global / L2)
-                    for (int i = warp; i <= j; i += NW) {
-                        const double* qi = Qg + (size_t)i * ld;
-                        double s = 0.0;
-                        for (int e = lane; e < md; e += 32) s = fma(qi[e], sm[Lo.oW + e], s);
-                        s = warp_sum(s);
-                        if (lane == 0) sm[Lo.oPart + 64 + i] = s;
+                    // h_i = q_i . w, i <= j (Q rows from global / L2): 8 threads per dot, 32 dots per
+                    // pass, each thread's 7 double2 loads issued together
+                    for (int i0 = 0; i0 <= j; i0 += LZ2_NT / 8) {
+                        const int i = i0 + (tid >> 3), sub = tid & 7;
+                        double s0 = 0.0, s1 = 0.0;
+                        if (i <= j) {
+                            const double* qi = Qg + (size_t)i * ld;
+                            double2 q2[7];
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) {
+                                const int c = 2 * sub + 16 * k;
+                                q2[k] = (c < mdp) ? *reinterpret_cast<const double2*>(qi + c) : make_double2(0.0, 0.0);
+                            }
+#pragma unroll
+                            for (int k = 0; k < 7; ++k) {
+                                const int c = 2 * sub + 16 * k;
+                                if (c < mdp) {
+                                    const double2 w2 = *reinterpret_cast<const double2*>(sm + Lo.oW + c);
+                                    s0 = fma(q2[k].x, w2.x, s0);
+                                    s1 = fma(q2[k].y, w2.y, s1);
+                                }
+                            }
+                        }
+                        double sd = s0 + s1;
+                        sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+                        sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+                        sd += __shfl_xor_sync(0xffffffffu, sd, 4);
+                        if (sub == 0 && i <= j) sm[Lo.oPart + 64 + i] = sd;
                     }
                     __syncthreads();
-                    double qh0 = 0.0, qh1 = 0.0;
-                    if (rowok) {
-                        int i = 0;
-                        for (; i + 1 <= j; i += 2) {
-                            qh0 = fma(sm[Lo.oPart + 64 + i], Qg[(size_t)i * ld + tid], qh0);
-                            qh1 = fma(sm[Lo.oPart + 64 + i + 1], Qg[(size_t)(i + 1) * ld + tid], qh1);
+                    // w -= Q h: row r = tid & 127, the two thread halves take alternate rows of Q
+                    // (8 loads in flight each), the upper half's partial through shared memory
+                    const int rq = tid & 127, hq = tid >> 7;
+                    double qa[4] = {0.0, 0.0, 0.0, 0.0};
+                    if (rq < md) {
+                        for (int i = hq; i <= j; i += 16) {
+                            double qv[8];
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int ii = i + 2 * u;
+                                qv[u] = (ii <= j) ? Qg[(size_t)ii * ld + rq] : 0.0;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 8; ++u) {
+                                const int ii = i + 2 * u;
+                                if (ii <= j) qa[u & 3] = fma(sm[Lo.oPart + 64 + ii], qv[u], qa[u & 3]);
+                            }
                         }
-                        if (i <= j) qh0 = fma(sm[Lo.oPart + 64 + i], Qg[(size_t)i * ld + tid], qh0);
                     }
+                    const double qpart = (qa[0] + qa[1]) + (qa[2] + qa[3]);
+                    if (hq == 1 && rq < mdp) sm[Lo.oW + rq] = qpart;  // w itself is no longer needed
+                    __syncthreads();
+                    const double qh0 = qpart, qh1 = (rowok && tid < 128) ? sm[Lo.oW + tid] : 0.0;
                     wr = rowok ? wr - (qh0 + qh1) : 0.0;
                     alpha += sm[Lo.oPart + 64 + j];
                 }

@@ -1357,6 +1357,21 @@ extern "C" int spec_kernel_timing(spec_ctx* ctx, int enable) {
     return SPEC_OK;
 }
 
+extern "C" const char* spec_k2_config(spec_ctx* ctx) {
+    static thread_local std::string s;
+    if (!ctx) return "";
+    char buf[256];
+    if (ctx->k2_split)
+        snprintf(buf, sizeof(buf), "split: factor_kernel<512> (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->f_grid, ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
+                 ctx->lz2 ? ctx->l2_grid : ctx->l_grid, ctx->t_grid);
+    else
+        snprintf(buf, sizeof(buf), "fused: chord_kernel2<%d, %s> (%d CTAs)", ctx->chord_threads,
+                 ctx->smem_path ? "shared" : "global scratch", ctx->chord_grid_max);
+    s = buf;
+    return s.c_str();
+}
+
 extern "C" int spec_lanczos_iterations(spec_ctx* ctx, int reset, double* mean_j, int64_t* solves) {
     if (!ctx) return fail(SPEC_EINVAL, "null ctx");
     CK(cudaSetDevice(ctx->dev));
