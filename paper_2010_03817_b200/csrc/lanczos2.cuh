@@ -23,6 +23,9 @@
 #pragma once
 #include "chord3.cuh"
 
+#ifndef SW_LZ2_HMC_FULL
+#define SW_LZ2_HMC_FULL 1
+#endif
 #ifndef SW_PRO_TAU2
 #define SW_PRO_TAU2 SW_PRO_TAU  // lanczos2's partial-reorthogonalisation threshold
 #endif
@@ -212,7 +215,9 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
             // ---- B: alpha, beta; q_{j+1}
             const double alpha0 = (sm[Lo.oPart + 0] + sm[Lo.oPart + 1]) + (sm[Lo.oPart + 2] + sm[Lo.oPart + 3]);
             const double nny = (sm[Lo.oPart + 8] + sm[Lo.oPart + 9]) + (sm[Lo.oPart + 10] + sm[Lo.oPart + 11]);
-            bool reorth = (j == 0);  // w_0 against q_0 exactly (no recurrence history)
+            // w_0 against q_0 exactly (no recurrence history); HMC-r's -N_1 solves (P.zall) take a full
+            // Gram-Schmidt pass every iteration (their Ritz vector is the hit's kernel vector)
+            bool reorth = (j == 0) || (P.zall && SW_LZ2_HMC_FULL);
             if (reorth_left > 0) {
                 reorth = true;
                 --reorth_left;

@@ -341,6 +341,7 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chord_kernel2<512, false, 16>, 512, ctx->g_smem));
         if (occ < 1) occ = 1;
         if (occ > 2) occ = 2;
+        if (getenv("SPECWALK_G_CTAS")) occ = std::max(1, std::min(occ, atoi(getenv("SPECWALK_G_CTAS"))));  // A/B
         ctx->chord_grid_max = occ * ctx->num_sms;
         ctx->scratch_stride = (long long)roundup((int)(per_cta + 8 * (size_t)mp), 32);  // + inverse diagonal blocks
         ctx->scratch_ctas = ctx->chord_grid_max;
@@ -671,9 +672,13 @@ static int launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
             lanczos_kernel<256, 8><<<g(ctx->hl_grid), 256, ctx->hl_smem, ctx->stream>>>(Pk);
         } else if (ctx->hmc_kc == 13) {
             hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
-            // (lanczos2_kernel's partially reorthogonalised Ritz vectors of -N_1 near the root were
-            // measured less accurate than the HMC parity bound: the fully reorthogonalised kernel)
-            lanczos_kernel<512, 13><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
+            // lanczos2_kernel with a full Gram-Schmidt pass every iteration for the -N_1 solves
+            // (partially reorthogonalised Ritz vectors near the root missed the HMC parity bound);
+            // SPECWALK_HMC_LZ_OLD=1: the register-resident kernel (A/B)
+            if (ctx->lz2 && !getenv("SPECWALK_HMC_LZ_OLD"))
+                lanczos2_kernel<<<g(ctx->l2_grid), LZ2_NT, ctx->l2_smem, ctx->stream>>>(Pk);
+            else
+                lanczos_kernel<512, 13><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
         } else {
             hmc_factor_kernel<512><<<g(ctx->hf_grid), 512, ctx->hf_smem, ctx->stream>>>(Pk);
             lanczos_kernel<512, 16><<<g(ctx->hl_grid), 512, ctx->hl_smem, ctx->stream>>>(Pk);
