@@ -10,6 +10,11 @@
 
 namespace sw {
 
+// per-slot scalar/vector area (doubles), vl = mp + 8
+enum : int { S_A = 0, S_BH = 1, S_MD = 2, S_ST = 3, S_TMAX = 4, S_TMIN = 5, S_DEG = 6, S_J = 7, S_VEC = 8 };
+enum : int { ST_OUTWARD = 1, ST_FAILED = 2, ST_DEFL = 4 };
+__host__ __device__ __forceinline__ long long s_stride(int mp) { return S_VEC + 4LL * (mp + 8); }
+
 
 struct ChordParams {
     int n, np, m, mt, mtp, ld;
@@ -81,6 +86,7 @@ struct ChordParams {
     int wkind;      // walk kind (SPEC_WALK_*): 2 = Hit-and-Run, 3 = coordinate Hit-and-Run
     int need_tmin;  // the chord must return t- as well (oracle mode, Hit-and-Run walks)
     int hnr_boltz;  // Hit-and-Run for exp(-c^T x / Temp) instead of the uniform law
+    int gsplit;     // global-scratch chord_kernel2 as the factor phase only (m > 112 split, lanczos_cl.cuh)
     // K2 split into factor / Lanczos / tail kernels: per-slot work buffers
     double* wM;     // M = -L^{-1} A(v) L^{-T} (mdp x mdp rows, leading dimension ld)
     double* wL;     // L (lower incl. diagonal, rows of leading dimension ld)

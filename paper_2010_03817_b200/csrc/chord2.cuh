@@ -1640,6 +1640,44 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <=
         __syncthreads();
         PROF_MARK(1);
 
+        if (!SMEM && P.gsplit) {
+            // ---- factor phase of the m > 112 split (as factor_kernel): Cholesky, congruence,
+            // M and packed L to the slot's work buffers, the deflation data to its small area;
+            // lanczos_cl_kernel and tail_kernel finish the call
+            int status = (defl ? ST_DEFL : 0) | (outward ? ST_OUTWARD : 0);
+            if (!outward && md >= 1) {
+                double* Lv = vec + NVEC2 * vl + 64;
+                const bool okc = cholesky_inv_blocked(T, Gd, mdp, ld, rdiag, Lv, &sh_i[2]);
+                PROF_MARK(2);
+                if (!okc) {
+                    status |= ST_FAILED;
+                } else {
+                    congruence_inv(T, Gd, Lv, Bd, mdp, ld);
+                    PROF_MARK(3);
+                    double* Mw = P.wM + (size_t)slot * P.w_mstride;
+                    double* Lw = P.wL + (size_t)slot * P.w_mstride;
+                    for (int i = T.warp; i < mdp; i += T.nwarps)
+                        for (int jx = T.lane; jx < mdp; jx += 32) {
+                            Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
+                            if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];
+                        }
+                }
+            }
+            double* S = P.wS + (size_t)slot * P.w_sstride;
+            if (T.tid == 0) {
+                S[S_A] = a_schur;
+                S[S_BH] = beta_h;
+                S[S_MD] = (double)md;
+                S[S_ST] = (double)status;
+            }
+            for (int i = T.tid; i < mp; i += T.nthr) {
+                S[S_VEC + i] = hh[i];
+                S[S_VEC + vl + i] = bv[i];
+                S[S_VEC + 2 * vl + i] = rdiag[i];
+            }
+            continue;
+        }
+
         // ---- 2. dense chord
         double theta_max = -SW_INF, theta_min = SW_INF;
         bool degenerate = false, failed = false;

@@ -25,10 +25,7 @@
 
 namespace sw {
 
-// per-slot scalar/vector area (doubles), vl = mp + 8
-enum : int { S_A = 0, S_BH = 1, S_MD = 2, S_ST = 3, S_TMAX = 4, S_TMIN = 5, S_DEG = 6, S_J = 7, S_VEC = 8 };
-enum : int { ST_OUTWARD = 1, ST_FAILED = 2, ST_DEFL = 4 };
-__host__ __device__ __forceinline__ long long s_stride(int mp) { return S_VEC + 4LL * (mp + 8); }
+// (the per-slot scalar/vector area S_* / ST_* and s_stride live in chord.cuh)
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);

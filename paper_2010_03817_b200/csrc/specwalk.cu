@@ -21,6 +21,7 @@
 #include "chord2.cuh"
 #include "chord3.cuh"
 #include "lanczos2.cuh"
+#include "lanczos_cl.cuh"
 #include "hmc.cuh"
 #include "hmc2.cuh"
 #include "estimators.cuh"
@@ -122,6 +123,8 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    int g_split = 0, cl_grid = 0;  // m > 112: factor (global scratch) | lanczos_cl_kernel (2-CTA cluster) | tail
+    size_t cl_smem = 0;
     size_t l2_smem = 0;
     size_t f_smem = 0, l_smem = 0, t_smem = 0;
     size_t smem_bytes = 0;
@@ -174,7 +177,7 @@ static int ensure_chains(spec_ctx* ctx, long long C) {
     ZA(AV, cap * mtp) ZA(Yh, cap * mtp) ZA(U, cap * m) ZA(ell, cap) ZA(tlast, cap) ZA(steps_done, cap) ZA(refl, cap)
     ZA(bound, cap) ZA(flags, cap) ZA(nrej, cap) ZA(ndeg, cap) ZA(ncap, cap) ZA(calls, cap) ZA(nrefl, cap) ZA(list, cap)
     ZA(list2, cap) ZA(nlist, cap) ZA(counters, 8) ZA(gid, cap) ZA(jlast, cap)
-    if (ctx->k2_split) {
+    if (ctx->k2_split || ctx->g_split) {
         const size_t mp = (size_t)roundup(ctx->m, 8);
         ZA(wM, cap * mp * ctx->ld) ZA(wL, cap * mp * ctx->ld) ZA(wS, cap * (size_t)s_stride((int)mp))
     }
@@ -347,6 +350,41 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->scratch_ctas = ctx->chord_grid_max;
         CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
         ctx->smem_bytes = 0;
+        // m > 112 split (SPECWALK_G_FUSED=1: the fused global-scratch kernel): the fused kernel as
+        // the factor phase, Lanczos on a 2-CTA cluster with M in the pair's shared memory
+        // (lanczos_cl.cuh, mp <= 2 x 104), the split tail kernel
+        const LclLayout lcl(mp, ctx->ld);
+        const size_t t_smem =
+            sizeof(double) * ((((size_t)mp * (mp + 1) / 2 + 1) & ~(size_t)1) + 5 * (size_t)(mp + 8) + 64);
+        if (mp <= 2 * LCL_ROWS && sizeof(double) * (size_t)lcl.total <= 227 * 1024 && t_smem <= 227 * 1024 &&
+            !getenv("SPECWALK_G_FUSED")) {
+            ctx->cl_smem = sizeof(double) * (size_t)lcl.total;
+            ctx->t_smem = t_smem;
+            CK(cudaFuncSetAttribute(lanczos_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->cl_smem));
+            CK(cudaFuncSetAttribute(tail_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->t_smem));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(2 * ctx->num_sms, 1, 1);
+            cfg.blockDim = dim3(LCL_NT, 1, 1);
+            cfg.dynamicSmemBytes = ctx->cl_smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0, ot = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, lanczos_cl_kernel, &cfg) != cudaSuccess) {
+                cudaGetLastError();  // no cluster occupancy: keep the fused kernel
+                ncl = 0;
+            }
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, tail_kernel<256>, 256, ctx->t_smem));
+            if (ncl >= 1 && ot >= 1) {
+                ctx->g_split = 1;
+                ctx->cl_grid = 2 * ncl;
+                ctx->t_grid = ot * ctx->num_sms;
+            }
+        }
     }
     // K2 split (chord3.cuh) for 64 < m <= 128 unless SPECWALK_K2_FUSED is set (for m <= 64 the
     // fused kernel was measured faster: 1.9M vs 1.4M calls/s at m = 40; it does not spill there)
@@ -504,10 +542,25 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
     P.need_tmin = (mode == 1);
     P.wkind = 0;
     P.hnr_boltz = 0;
+    P.gsplit = 0;
     return P;
 }
 
 static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cudaEvent_t* sub = nullptr) {
+    if (ctx->g_split) {
+        ChordParams Pf = P;
+        Pf.gsplit = 1;
+        int grid = std::max(1, std::min(count_host, ctx->chord_grid_max));
+        chord_kernel2<512, false, 16><<<grid, 512, ctx->g_smem, ctx->stream>>>(Pf);
+        if (sub) cudaEventRecord(sub[0], ctx->stream);
+        // clusters: one per chain (grid rounded to whole clusters)
+        const int cg2 = std::max(2, std::min(2 * count_host, ctx->cl_grid));
+        lanczos_cl_kernel<<<cg2, LCL_NT, ctx->cl_smem, ctx->stream>>>(P);
+        if (sub) cudaEventRecord(sub[1], ctx->stream);
+        tail_kernel<256><<<std::max(1, std::min(count_host, ctx->t_grid)), 256, ctx->t_smem, ctx->stream>>>(P);
+        ctx->launches += 3;
+        return;
+    }
     if (ctx->k2_split) {
         auto g = [&](int gmax) { return std::max(1, std::min(count_host, gmax)); };
         if (ctx->k2_variant == 0) {
@@ -985,7 +1038,7 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             if (W.p.kind == SPEC_WALK_HMC) {  // K5
                 int rc = launch_hmc(ctx, P, count);
                 if (rc) return rc;
-            } else launch_chord(ctx, P, count, (e && ctx->k2_split) ? &e[5] : nullptr);  // K2
+            } else launch_chord(ctx, P, count, (e && (ctx->k2_split || ctx->g_split)) ? &e[5] : nullptr);  // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
             if (W.p.kind == SPEC_WALK_BILLIARD || W.p.kind == SPEC_WALK_HMC) {  // Hit-and-Run never reflects
                 launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
@@ -1022,7 +1075,7 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
                     W.kms[i] += t;
                     W.kcount[i] += 1;
                 }
-                if (ctx->k2_split && W.p.kind != SPEC_WALK_HMC) {
+                if ((ctx->k2_split || ctx->g_split) && W.p.kind != SPEC_WALK_HMC) {
                     float t0 = 0.f, t1 = 0.f, t2 = 0.f;
                     CK(cudaEventElapsedTime(&t0, ev[7 * k + 1], ev[7 * k + 5]));
                     CK(cudaEventElapsedTime(&t1, ev[7 * k + 5], ev[7 * k + 6]));
@@ -1366,7 +1419,11 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
     static thread_local std::string s;
     if (!ctx) return "";
     char buf[256];
-    if (ctx->k2_split)
+    if (ctx->g_split)
+        snprintf(buf, sizeof(buf), "split (m > 112): chord_kernel2<512, global scratch> factor phase (%d CTAs) | "
+                 "lanczos_cl_kernel (2-CTA clusters, %d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->chord_grid_max, ctx->cl_grid, ctx->t_grid);
+    else if (ctx->k2_split)
         snprintf(buf, sizeof(buf), "split: factor_kernel<512> (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->f_grid, ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
                  ctx->lz2 ? ctx->l2_grid : ctx->l_grid, ctx->t_grid);
