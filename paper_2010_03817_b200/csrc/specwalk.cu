@@ -350,14 +350,17 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->scratch_ctas = ctx->chord_grid_max;
         CK(zalloc(&ctx->scratch, (size_t)ctx->scratch_stride * ctx->scratch_ctas));
         ctx->smem_bytes = 0;
-        // m > 112 split (SPECWALK_G_FUSED=1: the fused global-scratch kernel): the fused kernel as
-        // the factor phase, Lanczos on a 2-CTA cluster with M in the pair's shared memory
-        // (lanczos_cl.cuh, mp <= 2 x 104), the split tail kernel
+        // m > 112 split, opt-in (SPECWALK_G_SPLIT=1): the fused kernel as the factor phase, Lanczos
+        // on a 2-CTA cluster with M in the pair's shared memory (lanczos_cl.cuh, mp <= 2 x 104), the
+        // split tail kernel.  Measured slower than the fused kernel at m = 200 (116.1k vs 123.6k
+        // K2 calls/s) and m = 136 (206k vs 250k): one chain per SM pair with three cluster barriers
+        // per iteration (~13k cycles) does not beat two L2-bound chains per SM, and the factor
+        // phase pays the M / L round trip through HBM (profiles/r2k_m200_split)
         const LclLayout lcl(mp, ctx->ld);
         const size_t t_smem =
             sizeof(double) * ((((size_t)mp * (mp + 1) / 2 + 1) & ~(size_t)1) + 5 * (size_t)(mp + 8) + 64);
         if (mp <= 2 * LCL_ROWS && sizeof(double) * (size_t)lcl.total <= 227 * 1024 && t_smem <= 227 * 1024 &&
-            !getenv("SPECWALK_G_FUSED")) {
+            getenv("SPECWALK_G_SPLIT")) {
             ctx->cl_smem = sizeof(double) * (size_t)lcl.total;
             ctx->t_smem = t_smem;
             CK(cudaFuncSetAttribute(lanczos_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->cl_smem));

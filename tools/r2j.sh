@@ -1,5 +1,5 @@
 #!/bin/bash
-# m > 112 split (factor phase | lanczos_cl_kernel 2-CTA cluster | tail) vs the fused global-scratch kernel
+# m > 112 split (factor phase, lanczos_cl_kernel 2-CTA cluster, tail; opt-in SPECWALK_G_SPLIT=1) vs the fused kernel
 T=${1:-r2j}; O=gpurun_out/$T; mkdir -p $O
 export SPECWALK_PARITY_REPORT=$O/parity
 python -c "
