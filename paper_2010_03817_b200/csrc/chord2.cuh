@@ -22,12 +22,6 @@ constexpr int NVEC2 = 20;
 #ifndef SW_GLOBAL_LL
 #define SW_GLOBAL_LL 1  // global-scratch variant (m > 112): left-looking congruence
 #endif
-#ifndef SW_PRO
-// partial reorthogonalisation: correct (82% of the iterations plain at m = 100, parity green) but
-// measured 0.7% slower: a plain iteration's two barrier stages cost about what the three of the
-// full Gram-Schmidt iteration do (the loop is bound by per-stage latency, not by the O(j) work)
-#define SW_PRO 0
-#endif
 #ifndef SW_PRO_RUN
 #define SW_PRO_RUN 1
 #endif
@@ -609,10 +603,7 @@ __device__ double tri_laguerre_warp(const int oA, const int oB2, const int J, co
 // bookkeeping of lanczos_reg kept out of registers, and the decision.
 enum : int { CK_TTOP = 0, CK_RTOP = 1, CK_TBOT = 2, CK_RBOT = 3, CK_TNORM = 10 /* 2 slots (parity) */,
              CK_GHI = 12, CK_GLO = 13, CK_INTOP = 14, CK_INBOT = 15, CK_LRES = 16, CK_JPREV = 17, CK_NEXT = 18,
-             CK_DONE = 19, CK_HINTED = 20,
-             // asynchronous checks (lanczos_reg with a spare warp): J available to check, first
-             // converged J (0 = none yet), J of exhaustion, the stop decision for the compute warps
-             CK_JAV = 21, CK_STOPJ = 22, CK_EXH = 23, CK_DEC = 24 };
+             CK_DONE = 19, CK_HINTED = 20 };
 
 // Lanczos convergence check, run by warp 0 (lane 0 does the bookkeeping): Ritz
 // value(s) by the warp-parallel Laguerre between the inner bound (previous Ritz
@@ -1086,12 +1077,6 @@ enum : int { V_UU = 0, V_HH = 1, V_PW = 2, V_RDIAG = 3, V_RBE = 4, V_HB = 5, V_A
 #ifndef SW_RSQRT_BETA
 #define SW_RSQRT_BETA 1
 #endif
-#ifndef SW_ASYNC_CHECK
-// measured 3% slower at m = 100: a check takes ~33k cycles next to the iterating warps, so
-// convergence is seen ~8 iterations late (56 run for 48 used), which costs more than the
-// synchronous checks' idle time
-#define SW_ASYNC_CHECK 0
-#endif
 // sum over the row-owner lanes (g = lane & 3 == 0) of a warp: the other lanes hold zeros, so
 // the xor-1 / xor-2 levels of a full warp_sum add exact zeros and can be skipped (same value)
 __device__ __forceinline__ double owner_sum(double v) {
@@ -1106,53 +1091,6 @@ __device__ __forceinline__ double tree_sum(const double* p) {
     if constexpr (N == 1) return p[0];
     else return tree_sum<N / 2>(p) + tree_sum<N - N / 2>(p + N / 2);
 }
-__device__ __forceinline__ double vload(const double* p) { return *reinterpret_cast<const volatile double*>(p); }
-__device__ __forceinline__ void vstore(double* p, double v) { *reinterpret_cast<volatile double*>(p) = v; }
-
-// The checker warp of lanczos_reg's asynchronous mode: checks T_J at the same J sequence as the
-// synchronous mode (first check by size, later ones predicted from the residual rate), each as
-// soon as the compute warps have published alpha / beta up to J, while they keep iterating.
-// Stops at the first converged J (CK_STOPJ), which makes the result independent of timing.
-__device__ __noinline__ void lanczos_checker(const int lane, const int oAl, const int oBe, const int oB2,
-                                             const int oRbe, const bool need_bot, const int md, const int oShd,
-                                             int next, unsigned long long* prof) {
-    extern __shared__ __align__(16) double sm[];
-    while (true) {
-        int target = next;
-        const int exh = (int)vload(sm + oShd + CK_EXH);
-        if (exh > 0 && exh < target) target = exh;
-        if ((int)vload(sm + oShd + CK_JAV) < target) {
-            __nanosleep(64);
-            continue;
-        }
-        __threadfence_block();
-        const int J = target;
-        // |T_J| and beta_{J-1} exactly as the compute warps form them (max is exact)
-        double tn = 0.0;
-        for (int i = lane; i < J; i += 32)
-            tn = fmax(tn, fabs(sm[oAl + i]) + sm[oBe + i] + (i > 0 ? sm[oBe + i - 1] : 0.0));
-        tn = warp_max(tn);
-        const double beta = sm[oBe + J - 1];
-        const bool exhausted = (J == md) || !(beta > 1e-15 * tn);
-        const long long t0 = clock64();
-        lanczos_check(lane, oAl, oBe, oB2, oRbe, J, beta, tn, need_bot, exhausted, md, oShd, prof);
-        __syncwarp();
-        if (prof && lane == 0) {
-            atomicAdd(&prof[19], (unsigned long long)(clock64() - t0));
-            atomicAdd(&prof[28], 1ull);
-        }
-        const bool done = sm[oShd + CK_DONE] != 0.0;
-        if (done) {
-            if (lane == 0) {
-                __threadfence_block();
-                vstore(sm + oShd + CK_STOPJ, (double)J);
-            }
-            return;
-        }
-        next = (int)sm[oShd + CK_NEXT];
-    }
-}
-
 template <int NT, int KC, bool GM = false, bool USEQT = true>
 __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int md, const int mdp, const int ld,
                                            const bool need_bot, const int oVec, const int vl, const int oRed,
@@ -1163,28 +1101,14 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     static_assert(KC <= NT / 32, "M row segment of a thread: 8 KC columns <= NT / 4 rows");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = NT / 32;
-    // asynchronous checks when a whole warp has no M rows (m = 65..104 on 512 threads): the
-    // last warp runs the convergence checks while the others iterate (named barrier 1)
-    constexpr bool ASYNC = SW_ASYNC_CHECK && (NT - 32 >= 32 * KC);
-    constexpr int NWC = ASYNC ? NW - 1 : NW;  // compute warps
-    // partial reorthogonalisation (Simon's omega recurrence) for m > 64: most iterations are the
-    // plain three-term recurrence (2 barrier stages instead of 3, no O(j) dots / updates)
-    constexpr bool PRO = SW_PRO && (KC >= 13) && !ASYNC;
+    constexpr int NWC = NW;  // compute warps
     const int oAl = oVec + V_AL * vl, oBe = oVec + V_BE * vl, oRbe = oVec + V_RBE * vl, oHb = oVec + V_HB * vl;
     const int oB2 = oVec + V_B2 * vl;
     const int oWu = oVec + V_LZ * vl;  // wu0, wu1 (ping-pong), wp: 3 x (mdp + 8)
     const int oWp = oWu + 2 * (mdp + 8);
     const int oRB = oRed + 16;         // per-warp partial norms
     const int oShd = oRed + 32;        // check results (4) and thetas (2)
-    // PRO scratch in vector slots the callers leave free during the Lanczos run: omega rows
-    // (ring of 3) and the per-warp partials of alpha, |y'|^2 and max |omega|
-    const int oPart = oVec + V_UU * vl;
-    auto orow = [&](int i) { const int q = i % 3; return oVec + (q == 0 ? V_WV : q == 1 ? V_WV + 1 : V_PW) * vl; };
-    const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
-    auto csync = [&]() {
-        if (ASYNC) asm volatile("bar.sync 1, %0;\n" ::"n"(NT - 32) : "memory");
-        else __syncthreads();
-    };
+    auto csync = [&]() { __syncthreads(); };
     // transposed basis: in M's shared space once M is in registers, or a given region
     const int oQT = (oQTin >= 0) ? oQTin : oM;
     const int r = tid >> 2, g = tid & 3;
@@ -1227,24 +1151,12 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         sm[oShd + CK_TTOP] = -SW_INF;
         sm[oShd + CK_TBOT] = SW_INF;
         sm[oShd + CK_HINTED] = 0.0;
-        sm[oShd + CK_JAV] = 0.0;
-        sm[oShd + CK_STOPJ] = 0.0;
-        sm[oShd + CK_EXH] = 0.0;
-        sm[oShd + CK_DEC] = 0.0;
-        if (PRO) {
-            sm[orow(0)] = 1.0;  // omega_{0,0}
-            sm[oPart + 40] = 0.0;
-            sm[oPart + 41] = 0.0;
-        }
     }
     __syncthreads();  // also: every thread has its M row in registers (QT may overwrite M)
     double nn0 = 0.0;
     nn0 = tree_sum<NW>(sm + oRB);
     double sj = 1.0 / sqrt(nn0);  // q_j = u_j * sj
     double bjm1 = 0.0;
-    double qprev = 0.0;      // q_{j-1}[r] (PRO)
-    int reorth_left = 0;     // PRO: further iterations to reorthogonalise fully
-    bool was_full = true;    // PRO: the previous w was fully orthogonalised (omega row reset)
     // first check: 2 before the chain's previous iteration count (consecutive calls
     // of a chain need similar J), else at 40% of md; later checks from the observed rate
     // (a per-chain hint from the previous call was measured to RAISE J: consecutive calls of a
@@ -1258,9 +1170,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
     if (first_pct > 0 && md > SW_FIRST_PCT_MIN_MD) next_check = max(12, (md * first_pct) / 100);  // caller's rule (HMC-r)
     int J = 0;
     double tnorm = 0.0;
-    if (ASYNC && warp == NW - 1) {
-        lanczos_checker(lane, oAl, oBe, oB2, oRbe, need_bot, md, oShd, next_check, prof);
-    } else {
+    {
 #if SW_PROF_LANCZOS
     long long c_mv = 0, c_dot = 0, c_upd = 0, c_chk = 0, c_t = clock64();
 #define SW_LZ_STAMP(acc) if (prof) { long long c = clock64(); acc += c - c_t; c_t = c; }
@@ -1294,36 +1204,6 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         y += __shfl_xor_sync(0xffffffffu, y, 2);
         const double wpr = rowok ? y * sj : 0.0;
         const double qj = rowok ? wr * sj : 0.0;  // q_j[r] (all 4 lanes of the row)
-        double ypr = 0.0;                          // PRO: y' = M q_j - beta_{j-1} q_{j-1}
-        if (PRO) {
-            ypr = rowok ? wpr - bjm1 * qprev : 0.0;
-            double ap = (g == 0) ? qj * ypr : 0.0;
-            ap = owner_sum(ap);
-            if (lane == 0) sm[oPart + warp] = ap;
-            if (tid == 0) sm[oPart + 40 + ((j + 1) & 1)] = 0.0;  // next iteration's trigger flag
-            // omega_{j,k} = q_j . q_k estimates (Simon 1984) by the last 3 warps (no M rows for
-            // m <= 104): recurrence from the rows j-1, j-2, or the rounding level after a full
-            // orthogonalisation of w_{j-1}; any estimate above tau raises this iteration's flag
-            if (j >= 1) {
-                const int t = tid - (NT - 96);
-                for (int k = (t >= 0) ? t : md; k <= j; k += 96) {
-                    double v;
-                    if (k == j) v = 1.0;
-                    else if (k == j - 1) v = eps1 * tnorm * sj;
-                    else if (was_full) v = eps1;
-                    else {
-                        const int oP = orow(j - 1), oQq = orow(j - 2);
-                        const double bk = sm[oBe + k], bkm = (k > 0) ? sm[oBe + k - 1] : 0.0;
-                        double num = bk * sm[oP + k + 1] + (sm[oAl + k] - sm[oAl + j - 1]) * sm[oP + k] +
-                                     ((k > 0) ? bkm * sm[oP + k - 1] : 0.0) - sm[oBe + j - 2] * sm[oQq + k];
-                        num += copysign(eps1 * (bk + bjm1), num);
-                        v = num * sj;  // / beta_{j-1}
-                        if (fabs(v) > SW_PRO_TAU) sm[oPart + 40 + (j & 1)] = 1.0;
-                    }
-                    sm[orow(j) + k] = v;
-                }
-            }
-        }
         if (owner) {
             const double q = qj;  // q_j (wr = u_j[r])
             sm[oQ + j * ld + r] = q;
@@ -1335,47 +1215,10 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         }
         csync();
         SW_LZ_STAMP(c_mv)
-        if (ASYNC) {  // a check has converged at an earlier J: stop (this matvec is discarded)
-            const int dec = (int)sm[oShd + CK_DEC];
-            if (dec > 0) {
-                if (prof && tid == 0) atomicAdd(&prof[18], (unsigned long long)j);
-                J = dec;
-                break;
-            }
-        }
         // ---- (2)+(3) classical Gram-Schmidt of w' against q_0..q_j; a second pass
         // (DGKS) only on severe cancellation (|w| < 1e-6 |w'|, e.g. an invariant subspace).
-        // PRO (j >= 1): the three-term recurrence w = y' - alpha q_j; once an omega estimate of
-        // q_j exceeds tau, w_j and w_{j+1} also get one Gram-Schmidt pass against all q (after the
-        // recurrence removed the large local components, so the pass leaves w orthogonal to
-        // working precision and the omega row restarts at the rounding level).  q_j itself, already
-        // multiplied, stays semi-orthogonal (tau << sqrt(eps)).
         double wcur = wpr, alpha = 0.0, nnb = 0.0, nn = 0.0;
-        int pass0 = 0;
-        bool full = true;
-        if (PRO && j >= 1) {
-            bool reorth;
-            if (reorth_left > 0) { reorth = true; --reorth_left; }
-            else if (sm[oPart + 40 + (j & 1)] != 0.0) { reorth = true; reorth_left = 1; }
-            else reorth = false;
-            alpha = tree_sum<NW>(sm + oPart);
-            wcur = rowok ? ypr - alpha * qj : 0.0;
-            double pb = (g == 0) ? wcur * wcur : 0.0;
-            pb = owner_sum(pb);
-            if (lane == 0) sm[oRB + warp] = pb;
-            if (owner) sm[oUn + r] = wcur;
-            csync();
-            nn = tree_sum<NWC>(sm + oRB);
-            nnb = alpha * alpha + nn;  // |y'|^2 (y' = alpha q_j + w)
-            if (!reorth && nn >= 1e-12 * nnb) {
-                pass0 = 2;  // done: no Gram-Schmidt pass
-                full = false;
-            } else {
-                if (owner) sm[oWp + r] = wcur;  // one full pass on w (reorthogonalisation / cancellation)
-                csync();
-                pass0 = 1;
-            }
-        }
+        const int pass0 = 0;
         for (int pass = pass0; pass < 2; ++pass) {
             // (2) h_i = q_i . w for i <= j, and |w|^2 (slot j + 1): 8 lanes per dot, 4 dots per warp
             for (int ib = 4 * warp; ib <= j + 1; ib += 4 * NWC) {
@@ -1444,11 +1287,6 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             csync();
         }
         wr = wcur;
-        if (PRO) {
-            qprev = qj;
-            was_full = full;
-            if (prof && full && tid == 0) atomicAdd(&prof[29], 1ull);
-        }
 #if SW_RSQRT_BETA
         // 1/beta by the hardware reciprocal square root (+ Newton, ~1 ulp) and beta = nn / beta:
         // no correctly-rounded sqrt and division sequences on the iteration's critical path
@@ -1463,11 +1301,6 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
             sm[oBe + j] = beta;
             sm[oB2 + j] = nn;
             sm[oRbe + j] = rsb;
-            if (ASYNC) {  // publish T_{j+1}; pick up a converged check for the next iteration
-                __threadfence_block();
-                vstore(sm + oShd + CK_JAV, (double)(j + 1));
-                sm[oShd + CK_DEC] = vload(sm + oShd + CK_STOPJ);
-            }
         }
         tnorm = fmax(tnorm, fabs(alpha) + beta + bjm1);
         bjm1 = beta;
@@ -1475,20 +1308,7 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
         J = j + 1;
         const bool exhausted = (J == md) || !(beta > 1e-15 * tnorm);
         SW_LZ_STAMP(c_upd)
-        if (ASYNC) {
-            if (exhausted) {  // nothing left to iterate: wait for the checker (it checks here at the latest)
-                if (tid == 0) {
-                    vstore(sm + oShd + CK_EXH, (double)J);
-                    double st;
-                    while ((st = vload(sm + oShd + CK_STOPJ)) == 0.0) __nanosleep(64);
-                    sm[oShd + CK_DEC] = st;
-                }
-                csync();
-                if (prof && tid == 0) atomicAdd(&prof[18], (unsigned long long)J);
-                J = (int)sm[oShd + CK_DEC];
-                break;
-            }
-        } else if (exhausted || J >= next_check) {
+        if (exhausted || J >= next_check) {
             __syncthreads();  // al / be / b2 / rbe and the bookkeeping of this step visible
             lanczos_check(tid, oAl, oBe, oB2, oRbe, J, beta, tnorm, need_bot, exhausted, md, oShd, prof);
             __syncthreads();
