@@ -575,7 +575,7 @@ def main():
     ap.add_argument("--chains", type=int, default=CHAINS,
                     help="global chains (strong scaling, split over ranks) or chains per GPU (weak)")
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
-    ap.add_argument("--e2e-chains", type=int, default=16384)
+    ap.add_argument("--e2e-chains", type=int, default=65536)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--volume-seeds", type=int, default=10)
     ap.add_argument("--hmc-rounds", type=int, default=4)
