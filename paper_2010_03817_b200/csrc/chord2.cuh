@@ -1347,8 +1347,19 @@ __device__ __forceinline__ int lanczos_reg(const int oM, const int oQ, const int
 #include "chol_inv.cuh"
 namespace sw {
 
+// resident CTAs per SM the fused kernels are compiled for (the register cap follows)
+#ifndef SW_MINB128
+#define SW_MINB128 4
+#endif
+#ifndef SW_MINB192
+#define SW_MINB192 4  // m = 33..48: 4 CTAs/SM at 80 registers (some spills) measured +3% (m = 40) over 3;
+                      // the 128- and 256-thread variants lost 32% / 9% at their caps (profiles/r2m_minb)
+#endif
+#ifndef SW_MINB256
+#define SW_MINB256 2
+#endif
 template <int NT, bool SMEM, int KC>
-__global__ void __launch_bounds__(NT, (NT <= 128) ? 4 : (NT <= 192) ? 3 : (NT <= 256) ? 2 : 1) chord_kernel2(ChordParams P) {
+__global__ void __launch_bounds__(NT, (NT <= 128) ? SW_MINB128 : (NT <= 192) ? SW_MINB192 : (NT <= 256) ? SW_MINB256 : 1) chord_kernel2(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
     T.tid = threadIdx.x;
