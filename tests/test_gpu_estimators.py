@@ -93,3 +93,16 @@ def test_volume_elliptope_large_n_closed_form(k, seeds):
     for s in seeds:
         r = S.volume(0.1, s, 4096)
         assert abs(r["volume"] / exact - 1.0) <= 3.0 * r["std_rel"], (k, s, r["volume"], exact, r["std_rel"])
+
+
+def test_volume_ball_m161_global_scratch_membership():
+    """Membership (Alg. 1) for m > 160 runs its Cholesky in the global-scratch slices (A(x) no longer
+    fits shared memory): the volume of the unit ball as the arrow LMI with n = 160, m = 161 against
+    omega_n, within 3 of the estimator's sigma."""
+    import paper_2010_03817_b200 as sw
+    n = 160
+    S = sw.Spectrahedron.from_instance(specgen.ball(n))
+    r = S.volume(0.3, 0, 512, walk_len=4, burn=6)
+    exact = oracle.ball_volume(n)
+    assert r["q"] > 0.0
+    assert abs(r["volume"] / exact - 1.0) <= 3.0 * r["std_rel"] + 1e-12, (r["volume"], exact, r["std_rel"], r["phases"])
