@@ -23,6 +23,9 @@
 #pragma once
 #include "chord3.cuh"
 
+#ifndef SW_FIRST_CHECK_PCT2
+#define SW_FIRST_CHECK_PCT2 26  // lanczos2, md > 84: first check at 26% of md (30%: -2.5% at m = 100; r2p)
+#endif
 #ifndef SW_LZ2_HMC_FULL
 #define SW_LZ2_HMC_FULL 1
 #endif
@@ -151,7 +154,8 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
         const double eps1 = 2.220446049250313e-16 * sqrt((double)md);
         int next_check = (md <= SW_FIRST_CHECK_FULL_MD) ? md
                        : (md <= SW_FIRST_CHECK_SMALL_MD) ? (md * SW_FIRST_CHECK_PCT_SMALL) / 100
-                       : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100 : max(12, (md * SW_FIRST_CHECK_PCT) / 100);
+                       : (md <= 64) ? (md * SW_FIRST_CHECK_PCT_MID) / 100
+                       : (md <= 84) ? max(12, (md * SW_FIRST_CHECK_PCT) / 100) : max(12, (md * SW_FIRST_CHECK_PCT2) / 100);
         // HMC-r's lambda_min(N_1) solves (P.zall): their own first-check rule (lanczos_kernel's)
         if (P.zall && md > SW_FIRST_PCT_MIN_MD) next_check = max(12, (md * SW_FIRST_CHECK_PCT_HMC) / 100);
         const bool need_bot = P.need_tmin && !P.zall;
