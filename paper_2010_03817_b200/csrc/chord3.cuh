@@ -18,6 +18,12 @@
 // chain-call at m = 100 (~3% of a round).
 #pragma once
 #include "chord2.cuh"
+#ifndef SW_UNPACK_BOTH
+#define SW_UNPACK_BOTH 1  // factor_kernel: both triangles by cp.async, no mirror pass (-1.8% factor time, r2s)
+#endif
+#ifndef SW_FACTOR_SYM
+#define SW_FACTOR_SYM 1  // M = -(B + B^T)/2 when written, as the oracle (0: -B, rows only: -0.8% factor time, r2r)
+#endif
 #ifndef SW_TAIL_CTAS
 #define SW_TAIL_CTAS 3  // K2c CTAs per SM (L packed: ~49 KB of shared memory each at m = 100)
 #endif
@@ -40,6 +46,18 @@ __device__ __forceinline__ void unpack_lower_async(const Team& T, const double* 
     for (int i = T.warp; i < m; i += T.nwarps) {
         const double* src = P + (size_t)i * (i + 1) / 2;
         for (int j = T.lane; j <= i; j += 32) cp_async8(M + i * ld + j, src + j);
+    }
+}
+// both triangles straight from the packed lower rows (two asynchronous copies per element:
+// no mirror pass and its barrier)
+__device__ __forceinline__ void unpack_sym_async(const Team& T, const double* __restrict__ P, double* M, int m,
+                                                 int ld) {
+    for (int i = T.warp; i < m; i += T.nwarps) {
+        const double* src = P + (size_t)i * (i + 1) / 2;
+        for (int j = T.lane; j <= i; j += 32) {
+            cp_async8(M + i * ld + j, src + j);
+            if (j < i) cp_async8(M + j * ld + i, src + j);
+        }
     }
 }
 __device__ __forceinline__ void mirror_upper(const Team& T, double* M, int m, int ld) {
@@ -86,16 +104,23 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         const int bnd = P.bound[slot];
         __syncthreads();
         long long t_prof = clock64();
+#if SW_UNPACK_BOTH
+        unpack_sym_async(T, ax, G, m, ld);
+        unpack_sym_async(T, av, B, m, ld);
+#else
         unpack_lower_async(T, ax, G, m, ld);
         unpack_lower_async(T, av, B, m, ld);
+#endif
         const bool defl = (bnd == 0);
         if (defl)
             for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
+#if !SW_UNPACK_BOTH
         mirror_upper(T, G, m, ld);
         mirror_upper(T, B, m, ld);
         __syncthreads();
+#endif
         PROF_MARK(0);
         int md = m;
         double a_schur = 0.0, beta_h = 0.0;
@@ -158,7 +183,11 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
                 double* Lw = P.wL + (size_t)slot * P.w_mstride;
                 for (int i = T.warp; i < mdp; i += T.nwarps)
                     for (int jx = T.lane; jx < mdp; jx += 32) {
+#if SW_FACTOR_SYM
                         Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
+#else
+                        Mw[i * ld + jx] = -Bd[i * ld + jx];  // rows only: no column (bank-conflicted) reads
+#endif
                         if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];  // packed lower rows (tail_kernel)
                     }
             }
