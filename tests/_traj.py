@@ -1,0 +1,71 @@
+"""Trajectory parity with the chaos horizon (R27), shared by the billiard
+and HMC-r trajectory tests: the oracle is run twice per chain -- from the walk's start and from a
+start perturbed by DELTA -- and a chain's GPU trace is compared (1e-8) only up to the first
+reflection whose oracle-vs-perturbed-oracle amplification exceeds A_MAX or whose binding changes.
+Every chain must pass up to its horizon; the fraction of records compared is reported."""
+import math
+
+import numpy as np
+
+import oracle
+import specgen
+
+TOL_TRAJ = 1e-8
+DELTA = 1e-13  # P16 perturbation of the start
+A_MAX = 1e4    # amplification horizon (R27)
+
+
+def horizon(o, op):
+    """Number of leading reflections of a chain inside the chaos horizon: records j with
+    the same binding in the perturbed run and amplification |dx_j| / DELTA <= A_MAX."""
+    k = min(len(o["t"]), len(op["t"]))
+    for j in range(k):
+        if o["binding"][j] != op["binding"][j]:
+            return j
+        scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
+        amp = max(np.linalg.norm(op["hit_x"][j] - o["hit_x"][j]) / scale,
+                  np.linalg.norm(op["v_after"][j] - o["v_after"][j])) / DELTA
+        if amp > A_MAX:
+            return j
+    return k
+
+
+def traj_errors(g, o, H):
+    """Largest relative errors of the GPU trace over the first H records (binding must match)."""
+    worst = 0.0
+    if len(g["t"]) < H:
+        return math.inf, f"GPU recorded {len(g['t'])} < {H}"
+    for j in range(H):
+        if g["binding"][j] != o["binding"][j]:
+            return math.inf, f"binding differs at {j}: {g['binding'][j]} vs {o['binding'][j]}"
+        scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
+        e = max(np.linalg.norm(g["hit_x"][j] - o["hit_x"][j]) / scale,
+                abs(g["t"][j] - o["t"][j]) / max(abs(o["t"][j]), 0.1),
+                np.linalg.norm(g["w"][j] - o["w"][j]),
+                np.linalg.norm(g["v_after"][j] - o["v_after"][j]))
+        worst = max(worst, e)
+    return worst, ""
+
+
+
+def traj_parity(g, lmi, kind, seed, chains, steps, L, rho, R, n, pool, T=1.0, c=None):
+    """Compare GPU traces g (walk_trace output for `chains`) with the oracle; returns (report, failures)."""
+    pert = specgen.unit_vectors(len(chains), n, 99) * DELTA
+    fo = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, None, T, c, 0, True) for ch in chains]
+    fp = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, pert[i], T, c, 0, True)
+          for i, ch in enumerate(chains)]
+    horizons, avail, worst, fails = [], [], [], []
+    for i, ch in enumerate(chains):
+        o, op = fo[i].result(), fp[i].result()
+        H = horizon(o, op)
+        e, why = traj_errors(g[i], o, H)
+        horizons.append(H)
+        avail.append(min(R, len(o["t"])))
+        worst.append(e)
+        if not e <= TOL_TRAJ:
+            fails.append((ch, H, e, why))
+    frac = sum(horizons) / max(sum(avail), 1)
+    rep = dict(chains=len(chains), reflections=R, records_available=sum(avail), records_compared=sum(horizons),
+               fraction_compared=frac, chains_passing=len(chains) - len(fails), worst_rel_error=max(worst),
+               median_rel_error=float(np.median(worst)), horizon_min=min(horizons), failures=fails[:8])
+    return rep, fails

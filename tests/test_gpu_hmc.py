@@ -91,52 +91,40 @@ def test_hmc_oracle_boundary_start_parity(name, make, vscale, T):
     _cmp(res, refs, lmi)
 
 
-def test_hmc_trajectory_parity():
-    import paper_2010_03817_b200 as sw
-    inst = specgen.rand_cube(10, 10, 1, scale=0.5)
-    lmi = oracle.Lmi(inst)
-    c = specgen.objective(10, 1)
-    T, L, rho = 0.5, 2.0, 100
-    S = sw.Spectrahedron.from_instance(inst)
-    S.set_objective(c)
-    chains = list(range(16))
-    g = S.walk_trace(chains, steps=40, L=L, rho=rho, seed=2, max_refl=15, kind=sw.HMC, T=T)
-    ok = 0
-    for i, ch in enumerate(chains):
-        o = oracle.trace(lmi, oracle.HMC, 2, ch, 40, L, rho, 15, T=T, c=c)
-        k = min(len(o["t"]), len(g[i]["t"]))
-        good = k == len(o["t"])
-        for j in range(k):
-            good &= np.linalg.norm(g[i]["hit_x"][j] - o["hit_x"][j]) <= 1e-8 * max(np.linalg.norm(o["hit_x"][j]), .1)
-            good &= np.linalg.norm(g[i]["v_after"][j] - o["v_after"][j]) <= 1e-8 * max(np.linalg.norm(o["v_after"][j]), 1)
-            good &= g[i]["binding"][j] == o["binding"][j]
-        ok += bool(good)
-    assert ok >= 0.9 * len(chains), ok
+HMC_TRAJ = {
+    # name: (instance, c, T, L, rho, walk seed, steps, chains, reflections)
+    "mixed_10": (lambda: specgen.rand_cube(10, 10, 1, scale=0.5), lambda: specgen.objective(10, 1), 0.5, 2.0, 100, 2,
+                 40, 64, 15),
+    "m40_split": (lambda: specgen.rand_cube(12, 40, 4, scale=1 / np.sqrt(12)), lambda: specgen.objective(12, 4), 0.5,
+                  2.0, 100, 6, 10, 32, 10),
+    # configs[3]'s own workload (T = 1, tau = 1.09: SURVEY 8(c).2 #8)
+    "configs3": (lambda: specgen.config_instance(3), lambda: specgen.objective(100, 3), 1.0, 1.09, 1000, 3, 5, 64, 20),
+}
 
 
-def test_hmc_trajectory_parity_m40():
-    """Trajectories on the K5 split path with the <256, KC 8> kernels (m = 40): many Weyl
-    iterations per call over compacted lists, boundary starts after every dense hit."""
+@pytest.mark.parametrize("name", list(HMC_TRAJ))
+def test_hmc_trajectory_parity(name):
+    """HMC-r trajectories (Alg. 6) through the first reflections of every chain vs the oracle
+    (companion + QR roots), 1e-8, each chain up to its chaos horizon (R27); all chains must pass."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
     import paper_2010_03817_b200 as sw
-    inst = specgen.rand_cube(12, 40, 4, scale=1 / np.sqrt(12))
+    from _traj import traj_parity
+    make, mc, T, L, rho, seed, steps, nch, R = HMC_TRAJ[name]
+    inst = make()
+    c = mc()
     lmi = oracle.Lmi(inst)
-    c = specgen.objective(12, 4)
-    T, L, rho = 0.5, 2.0, 100
     S = sw.Spectrahedron.from_instance(inst)
     S.set_objective(c)
-    chains = list(range(8))
-    g = S.walk_trace(chains, steps=10, L=L, rho=rho, seed=6, max_refl=10, kind=sw.HMC, T=T)
-    ok = 0
-    for i, ch in enumerate(chains):
-        o = oracle.trace(lmi, oracle.HMC, 6, ch, 10, L, rho, 10, T=T, c=c)
-        k = min(len(o["t"]), len(g[i]["t"]))
-        good = k == len(o["t"]) and k > 0
-        for j in range(k):
-            good &= np.linalg.norm(g[i]["hit_x"][j] - o["hit_x"][j]) <= 1e-8 * max(np.linalg.norm(o["hit_x"][j]), .1)
-            good &= np.linalg.norm(g[i]["v_after"][j] - o["v_after"][j]) <= 1e-8 * max(np.linalg.norm(o["v_after"][j]), 1)
-            good &= g[i]["binding"][j] == o["binding"][j]
-        ok += bool(good)
-    assert ok >= 0.75 * len(chains), ok
+    chains = list(range(nch))
+    g = S.walk_trace(chains, steps=steps, L=L, rho=rho, seed=seed, max_refl=R, kind=sw.HMC, T=T)
+    with ThreadPoolExecutor(os.cpu_count() or 4) as pool:
+        rep, fails = traj_parity(g, lmi, oracle.HMC, seed, chains, steps, L, rho, R, inst.n, pool, T=T, c=c)
+    print(f"[parity] hmc_trajectory_{name}: {rep}")
+    assert not fails, fails[:8]
+    assert rep["records_available"] > 0
+    assert rep["fraction_compared"] >= 0.9, rep["fraction_compared"]
 
 
 def test_hmc_boltzmann_cube_moments_gpu():

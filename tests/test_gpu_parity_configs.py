@@ -27,14 +27,13 @@ import pytest
 
 import oracle
 import specgen
+from _traj import DELTA, A_MAX, traj_parity
 
 pytestmark = pytest.mark.gpu
 
 TOL_TRAJ = 1e-8
 TOL_T = 1e-9
 TOL_COS = 1e-10
-DELTA = 1e-13  # P16 perturbation of the start
-A_MAX = 1e4    # amplification horizon (R27)
 R = 20
 POOL = ThreadPoolExecutor(os.cpu_count() or 4)  # the oracle's C calls release the GIL
 
@@ -60,38 +59,6 @@ TRAJ = {
 }
 
 
-def _horizon(o, op):
-    """Number of leading reflections of a chain inside the chaos horizon: records j with
-    the same binding in the perturbed run and amplification |dx_j| / DELTA <= A_MAX."""
-    k = min(len(o["t"]), len(op["t"]))
-    for j in range(k):
-        if o["binding"][j] != op["binding"][j]:
-            return j
-        scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
-        amp = max(np.linalg.norm(op["hit_x"][j] - o["hit_x"][j]) / scale,
-                  np.linalg.norm(op["v_after"][j] - o["v_after"][j])) / DELTA
-        if amp > A_MAX:
-            return j
-    return k
-
-
-def _traj_errors(g, o, H):
-    """Largest relative errors of the GPU trace over the first H records (binding must match)."""
-    worst = 0.0
-    if len(g["t"]) < H:
-        return math.inf, f"GPU recorded {len(g['t'])} < {H}"
-    for j in range(H):
-        if g["binding"][j] != o["binding"][j]:
-            return math.inf, f"binding differs at {j}: {g['binding'][j]} vs {o['binding'][j]}"
-        scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
-        e = max(np.linalg.norm(g["hit_x"][j] - o["hit_x"][j]) / scale,
-                abs(g["t"][j] - o["t"][j]) / max(abs(o["t"][j]), 0.1),
-                np.linalg.norm(g["w"][j] - o["w"][j]),
-                np.linalg.norm(g["v_after"][j] - o["v_after"][j]))
-        worst = max(worst, e)
-    return worst, ""
-
-
 @pytest.mark.parametrize("cfg", list(TRAJ))
 def test_trajectory_parity_64_chains_20_reflections(cfg):
     import paper_2010_03817_b200 as sw
@@ -102,29 +69,10 @@ def test_trajectory_parity_64_chains_20_reflections(cfg):
     chains = list(range(64))
     S = sw.Spectrahedron.from_instance(inst)
     g = S.walk_trace(chains, steps=steps, L=L, rho=rho, seed=seed, max_refl=R)
-    pert = specgen.unit_vectors(len(chains), n, 99) * DELTA
-    fo = [POOL.submit(oracle.trace, lmi, oracle.BILLIARD, seed, c, steps, L, rho, R, None, 1.0, None, 0, True)
-          for c in chains]
-    fp = [POOL.submit(oracle.trace, lmi, oracle.BILLIARD, seed, c, steps, L, rho, R, pert[i], 1.0, None, 0, True)
-          for i, c in enumerate(chains)]
-    horizons, avail, worst, fails = [], [], [], []
-    for i, c in enumerate(chains):
-        o, op = fo[i].result(), fp[i].result()
-        H = _horizon(o, op)
-        e, why = _traj_errors(g[i], o, H)
-        horizons.append(H)
-        avail.append(min(R, len(o["t"])))
-        worst.append(e)
-        if not e <= TOL_TRAJ:
-            fails.append((c, H, e, why))
-    frac = sum(horizons) / max(sum(avail), 1)
-    _report(f"trajectory_{cfg}", dict(chains=len(chains), reflections=R, records_available=sum(avail),
-                                      records_compared=sum(horizons), fraction_compared=frac,
-                                      chains_passing=len(chains) - len(fails), worst_rel_error=max(worst),
-                                      median_rel_error=float(np.median(worst)),
-                                      horizon_min=min(horizons), failures=fails[:8]))
+    rep, fails = traj_parity(g, lmi, oracle.BILLIARD, seed, chains, steps, L, rho, R, n, POOL)
+    _report(f"trajectory_{cfg}", rep)
     assert not fails, fails[:8]
-    assert frac >= 0.9, frac
+    assert rep["fraction_compared"] >= 0.9, rep["fraction_compared"]
 
 
 # ---------------------------------------------------------------- per call, 256 lines

@@ -11,41 +11,7 @@ pytestmark = pytest.mark.gpu
 TOL_TRAJ = 1e-8
 
 
-def _traj_compare(g, o, n_check):
-    k = min(n_check, len(o["t"]))
-    assert len(g["t"]) >= k, (len(g["t"]), k)
-    for j in range(k):
-        scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
-        assert np.linalg.norm(g["hit_x"][j] - o["hit_x"][j]) <= TOL_TRAJ * scale, j
-        assert abs(g["t"][j] - o["t"][j]) <= TOL_TRAJ * max(abs(o["t"][j]), 0.1), j
-        assert np.linalg.norm(g["w"][j] - o["w"][j]) <= TOL_TRAJ, j
-        assert np.linalg.norm(g["v_after"][j] - o["v_after"][j]) <= TOL_TRAJ, j
-        assert g["binding"][j] == o["binding"][j], j
-
-
-@pytest.mark.parametrize("cfg", ["cfg0", "mixed", "m40"])
-def test_trajectory_parity_first_20_reflections(cfg):
-    import paper_2010_03817_b200 as sw
-    if cfg == "cfg0":
-        inst, L, rho, chains = specgen.config_instance(0), 2 * np.sqrt(10), 100, range(64)
-    elif cfg == "mixed":  # dense and cube faces both bind
-        inst, L, rho, chains = specgen.rand_cube(10, 10, 1, scale=0.3), 2 * np.sqrt(10), 100, range(32)
-    else:
-        inst, L, rho, chains = specgen.rand_cube(40, 40, 2), 2 * np.sqrt(40), 400, range(8)
-    lmi = oracle.Lmi(inst)
-    S = sw.Spectrahedron.from_instance(inst)
-    R = 20
-    g = S.walk_trace(list(chains), steps=50, L=L, rho=rho, seed=0, max_refl=R)
-    passed = 0
-    for i, c in enumerate(chains):
-        o = oracle.trace(lmi, oracle.BILLIARD, 0, c, 50, L, rho, R)
-        try:
-            _traj_compare(g[i], o, R)
-            passed += 1
-        except AssertionError:
-            pass
-    # chaotic amplification (P16) may push rare chains over 1e-8 by reflection 20
-    assert passed >= 0.9 * len(chains), (passed, len(chains))
+# (per-trajectory parity with the chaos horizon: tests/test_gpu_parity_configs.py)
 
 
 def test_walk_end_points_match_oracle_short_walks():
