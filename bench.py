@@ -353,8 +353,8 @@ def run_ours(args):
         dom, dom_ms, dom_flops = "K2 chord_kernel2 (fused)", k2_ms, f["k2"]
     dom_avg_ms = dom_ms / max(k2_launches, 1)
     achieved = dom_flops * items_per_launch / (dom_avg_ms * 1e-3) / 1e12
-    tr = (ncu_traffic_per_launch("lanczos2_full_ncu" if "lanczos2" in dom else "lanczos_full_ncu")
-          if dom.startswith("K2b") else None)
+    tr = ((ncu_traffic_per_launch("lanczos2_full_ncu", "lanczos2_kernel") if "lanczos2" in dom
+           else ncu_traffic_per_launch("lanczos_full_ncu", "lanczos_kernel")) if dom.startswith("K2b") else None)
     traffic = tr["bytes"] if tr else None
 
     # ---- end-to-end through the public host API (walk_sample with host buffers)

@@ -1,0 +1,7 @@
+#!/bin/bash
+T=${1:-r2t}; O=gpurun_out/$T; mkdir -p $O
+export SPECWALK_PARITY_REPORT=$O/parity
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider -s > $O/gpu_tests.log 2>&1; echo "exit $?" >> $O/gpu_tests.log
+timeout 900 python bench.py > $O/bench.json 2> $O/bench.err
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "exit $?" >> $O/smoke.log
+bash tools/r2o.sh $T
