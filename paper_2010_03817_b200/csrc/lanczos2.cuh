@@ -234,7 +234,11 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
             double nn = nny - alpha0 * alpha0;  // |w|^2 by Pythagoras (q_j unit, w = y' - alpha q_j)
             bool full = false;
             if (reorth || !(nn >= 0.25 * nny)) {
-                // exact path: one Gram-Schmidt pass of w against q_0..q_j when due, exact |w|^2
+                // exact |w|^2 when the three-term step cancelled more than 3/4 of |y'|^2; one
+                // Gram-Schmidt pass of w against q_0..q_j when due, and whenever it cancelled all
+                // but 1e-6 of |y'| (the residual is then mostly rounding and has lost orthogonality,
+                // as at an invariant subspace of a low-rank M: lanczos_run's criterion)
+                if (!(nn >= 1e-12 * nny)) reorth = true;
                 full = reorth;
                 if (reorth) {
                     if (owner) sm[Lo.oW + tid] = wr;
@@ -303,6 +307,8 @@ __global__ void __launch_bounds__(LZ2_NT, 2) lanczos2_kernel(ChordParams P) {
                 nn = 0.0;
 #pragma unroll
                 for (int w = 0; w < NW; ++w) nn += sm[Lo.oPart + 16 + w];
+                // nothing but rounding left after the pass: the Krylov space is invariant (beta = 0)
+                if (nn < 1e-28 * nny) nn = 0.0;
             } else if (tid == 0) {
                 sm[Lo.oPart + 40 + ((j + 1) & 1)] = 0.0;
             }

@@ -63,6 +63,9 @@ CASES = [
     ("mixed_binding_12_30", lambda: specgen.rand_cube(12, 30, 5, scale=1 / np.sqrt(12))),
     ("cube_dense_5", lambda: specgen.cube_dense(5)),
     ("ball_7", lambda: specgen.ball(7)),
+    # a rank-2 pencil A(v) on the split path (m = 101: factor | lanczos2 | tail): the Lanczos
+    # space becomes invariant after 2-3 steps (the residual is rounding, lanczos2's DGKS pass)
+    ("ball_100", lambda: specgen.ball(100)),
     ("paper_example", specgen.paper_example),
     ("rand_3_1", lambda: specgen.rand_cube(3, 1, 9)),
 ]
@@ -100,7 +103,10 @@ def test_boundary_oracle_interior_parity(name, make):
             assert abs(np.linalg.eigvalsh(F)[0]) <= 1e-12 * scale
 
 
-@pytest.mark.parametrize("name,make", CASES[:6] + VARIANTS, ids=[c[0] for c in CASES[:6] + VARIANTS])
+BCASES = CASES[:6] + [c for c in CASES if c[0] == "ball_100"] + VARIANTS
+
+
+@pytest.mark.parametrize("name,make", BCASES, ids=[c[0] for c in BCASES])
 def test_boundary_oracle_boundary_start_parity(name, make):
     """Segments that start on the dense boundary (after a reflection): Schur deflation (R6)."""
     import paper_2010_03817_b200 as sw

@@ -10,7 +10,7 @@ same seeded inputs; tolerances from BASELINE.json north_star):
   reflection whose oracle-vs-perturbed-oracle amplification exceeds 1e4 (beyond
   it a per-call difference of 1e-12 -- 1000x below the 1e-9 per-call bound -- can
   legitimately exceed 1e-8).  The fraction of records compared is reported and
-  must stay >= 0.9.
+  must stay >= 0.9.  (R27: the horizon is TOL / the per-call budget the per-call tests assert.)
 * per call: 256 interior and 256 boundary-start lines at m = 100 and m = 200 for
   the billiard chord (Alg. 2, Schur deflation R6) and the HMC-r chord (Alg. 6,
   eq:boltz_ode): t+ (and t-) to 1e-9 relative, normals cos >= 1 - 1e-10, binding exact.
@@ -27,7 +27,7 @@ import pytest
 
 import oracle
 import specgen
-from _traj import DELTA, A_MAX, traj_parity
+from _traj import PER_CALL_BUDGET, PER_CALL_BUDGET_HMC, traj_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -189,3 +189,6 @@ def test_per_call_parity_256_interior_and_boundary(kind, name):
     assert len(keep) >= 200, len(keep)
     assert not bad_i, bad_i[:8]
     assert not bad_b, bad_b[:8]
+    # the per-call budget the trajectory horizon assumes (tests/_traj.py, R27)
+    budget = PER_CALL_BUDGET_HMC if hmc else PER_CALL_BUDGET
+    assert max(dw_i + dw_b) <= budget, (max(dw_i + dw_b), budget)
