@@ -984,6 +984,10 @@ __device__ int lanczos_run(const Team& T, const double* M, double* Q, int md, in
             // keeps theta_max within ~20 eps |M|; the 0.5 criterion fired on 2/3 of the iterations)
             if (!(nn < 1e-12 * nn_before)) break;
         }
+        // only rounding left after the Gram-Schmidt pass(es): the Krylov space is invariant
+        // (low-rank pencils, e.g. the ball); continuing would orthogonalise noise once and breed
+        // ghost Ritz values
+        if (nn < 1e-28 * nn_before) nn = 0.0;
         const double beta = sqrt(nn);
         if (T.tid == 0) {
             al[j] = alpha;

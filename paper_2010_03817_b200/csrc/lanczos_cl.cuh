@@ -213,6 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LCL_NT, 1) lanczos_c
             double nn = nny - alpha0 * alpha0;
             bool full = false;
             if (reorth || !(nn >= 0.25 * nny)) {
+                if (!(nn >= 1e-12 * nny)) reorth = true;  // severe cancellation: a Gram-Schmidt pass (lanczos2)
                 full = reorth;
                 if (reorth) {
                     if (owner) sm[Lo.oW + tid] = wr;  // own rows, local index
@@ -280,6 +281,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(LCL_NT, 1) lanczos_c
                 }
                 cluster.sync();
                 nn = sm[Lo.oPart + 12] + sm[Lo.oPart + 13];
+                if (nn < 1e-28 * nny) nn = 0.0;  // only rounding left: invariant Krylov space
             } else if (tid == 0) {
                 sm[Lo.oPart + 40 + ((j + 1) & 1)] = 0.0;
             }

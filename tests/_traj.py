@@ -30,8 +30,9 @@ def horizon(o, op, a_max=A_MAX):
         if o["binding"][j] != op["binding"][j]:
             return j
         scale = max(np.linalg.norm(o["hit_x"][j]), 0.1)
+        vscale = max(np.linalg.norm(o["v_after"][j]), 1.0)  # HMC velocities are not unit
         amp = max(np.linalg.norm(op["hit_x"][j] - o["hit_x"][j]) / scale,
-                  np.linalg.norm(op["v_after"][j] - o["v_after"][j])) / DELTA
+                  np.linalg.norm(op["v_after"][j] - o["v_after"][j]) / vscale) / DELTA
         if amp > a_max:
             return j
     return k
@@ -49,7 +50,7 @@ def traj_errors(g, o, H):
         e = max(np.linalg.norm(g["hit_x"][j] - o["hit_x"][j]) / scale,
                 abs(g["t"][j] - o["t"][j]) / max(abs(o["t"][j]), 0.1),
                 np.linalg.norm(g["w"][j] - o["w"][j]),
-                np.linalg.norm(g["v_after"][j] - o["v_after"][j]))
+                np.linalg.norm(g["v_after"][j] - o["v_after"][j]) / max(np.linalg.norm(o["v_after"][j]), 1.0))
         worst = max(worst, e)
     return worst, ""
 

@@ -1,0 +1,6 @@
+#!/bin/bash
+T=${1:-r2y}; O=gpurun_out/$T; mkdir -p $O
+export SPECWALK_PARITY_REPORT=$O/parity
+timeout 600 python tools/dbg_ball.py 160 > $O/ball_160.log 2>&1
+timeout 1500 python -m pytest tests/test_gpu_hmc.py tests/test_gpu_parity_configs.py tests/test_gpu_estimators.py -m gpu -q -p no:cacheprovider -s -k "trajectory or m161 or per_call" > $O/tests.log 2>&1; echo "exit $?" >> $O/tests.log
+echo done > $O/DONE
