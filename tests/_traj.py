@@ -17,9 +17,9 @@ DELTA = 1e-13  # P16 perturbation of the start
 # measured 9e-13 for the billiard chord and 9e-11 for the HMC-r chord -- both far inside
 # north_star's per-call cos >= 1 - 1e-10)
 PER_CALL_BUDGET = 2e-12
-PER_CALL_BUDGET_HMC = 2e-10
+PER_CALL_BUDGET_HMC = 1e-10
 A_MAX = TOL_TRAJ / PER_CALL_BUDGET          # 5e3
-A_MAX_HMC = TOL_TRAJ / PER_CALL_BUDGET_HMC  # 50
+A_MAX_HMC = TOL_TRAJ / PER_CALL_BUDGET_HMC  # 100
 
 
 def horizon(o, op, a_max=A_MAX):
