@@ -38,7 +38,8 @@ _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liborc.so")
 
 INF = float("inf")
-BILLIARD, HMC, HNR, CHNR = 0, 1, 2, 3  # HnR: Alg. 4; CHnR: P:985-996
+BILLIARD, HMC, HNR, CHNR, CHMC = 0, 1, 2, 3, 4  # HnR: Alg. 4; CHnR: P:985-996; CHMC: P:1146-1158
+POT_LINEAR, POT_GAUSS, POT_LOGCOSH = 0, 1, 2
 TAG_WALK = 0 << 28
 TAG_VOLUME = 1 << 28
 TAG_PILOT = 3 << 28
@@ -78,6 +79,7 @@ class _WalkParams(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("seed", C.c_uint64), ("tag", C.c_uint32), ("steps", C.c_int64),
         ("L", C.c_double), ("rho", C.c_int64), ("T", C.c_double), ("c", _dp),
+        ("pot", C.c_int), ("mu", _dp), ("sigma", C.c_double), ("q", C.c_int), ("h", C.c_double),
     ]
 
 
@@ -114,6 +116,11 @@ def lib():
         l.orc_qep_root.argtypes = [C.c_int, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp]
         l.orc_hmc_chord.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, C.c_double, C.c_int, _dp,
                                     C.POINTER(_ChordRes)]
+        l.orc_colloc_basis.argtypes = [C.c_int, _dp, _dp]
+        l.orc_colloc_poly.argtypes = [C.c_int, C.POINTER(_WalkParams), _dp, _dp, C.c_double, _dp]
+        l.orc_pep_root.argtypes = [C.c_int, C.c_int, _dp, C.c_int, _dp, C.c_double, _dp, _dp]
+        l.orc_colloc_chord.argtypes = [C.c_void_p, _dp, _dp, C.c_int, C.c_double, C.c_int, _dp,
+                                       C.POINTER(_ChordRes)]
         _lib = l
     return _lib
 
@@ -273,23 +280,81 @@ def hmc_chord(lmi: Lmi, x, v, c, T, F0=None, bound=-1, u=None) -> dict:
     return dict(t_plus=r.t_plus, block=r.binding, outward=bool(r.outward), y=np.array(r.y[: r.ylen]))
 
 
-def _params(kind, seed, tag, steps, L, rho, T=1.0, c=None):
+def _params(kind, seed, tag, steps, L, rho, T=1.0, c=None, colloc=None):
+    """colloc (kind CHMC): dict(pot=POT_*, mu=array or None, sigma=float, q=int, h=float)."""
     p = _WalkParams()
     p.kind, p.seed, p.tag, p.steps, p.L, p.rho, p.T = kind, seed, tag, steps, float(L), rho, float(T)
     keep = _arr(c) if c is not None else None
     p.c = _p(keep)
-    return p, keep
+    keep_mu = None
+    if colloc is not None:
+        p.pot = int(colloc.get("pot", POT_GAUSS))
+        keep_mu = _arr(colloc["mu"]) if colloc.get("mu") is not None else None
+        p.mu = _p(keep_mu)
+        p.sigma = float(colloc.get("sigma", 1.0))
+        p.q = int(colloc.get("q", 3))
+        p.h = float(colloc["h"])
+    return p, (keep, keep_mu)
+
+
+def colloc_basis(q: int):
+    """Chebyshev nodes of [0, 1] and Lagrange monomial coefficients lcoef[j, k] (R33)."""
+    nodes = np.zeros(q)
+    lc = np.zeros((q, q))
+    if lib().orc_colloc_basis(q, _p(nodes), _p(lc)):
+        raise ValueError("q out of range")
+    return nodes, lc
+
+
+def colloc_poly(x0, v0, h: float, colloc: dict, c=None, T: float = 1.0):
+    """Collocation polynomial of p'' = -grad f on [0, h]: coef[k] = t^k
+    coefficient (q+2 rows), and the Picard iterations used (negative: not converged)."""
+    x0, v0 = _arr(x0), _arr(v0)
+    n = x0.shape[0]
+    p, keep = _params(CHMC, 0, 0, 1, 1.0, 0, T, c, colloc)
+    coef = np.zeros((p.q + 2, n))
+    it = lib().orc_colloc_poly(n, C.byref(p), _p(x0), _p(v0), float(h), _p(coef))
+    return coef, it
+
+
+def pep_root(Bs, tmax: float = INF, u=None):
+    """First root in (0, tmax] of det(sum_k t^k B_k) (degree-d companion + Francis QR);
+    +inf if none.  u: unit kernel vector of B_0 (boundary start).  Returns (t_plus, kernel
+    vector); raises on rc != 0 (2: B_0 not PD, 3: outward)."""
+    B = _arr(np.stack([_arr(b) for b in Bs]))
+    d = B.shape[0] - 1
+    mb = B.shape[1]
+    tp = C.c_double()
+    y = np.zeros(mb)
+    ua = _arr(u) if u is not None else None
+    rc = lib().orc_pep_root(mb, d, _p(B), 1 if u is not None else 0, _p(ua), float(tmax), C.byref(tp), _p(y))
+    if rc:
+        raise ValueError(f"pep_root rc={rc}")
+    return tp.value, y
+
+
+def colloc_chord(lmi: Lmi, coef, tmax: float, F0=None, bound: int = -1, u=None) -> dict:
+    """Chord of the curve sum_k coef[k] t^k over every block, t in (0, tmax]."""
+    r = _ChordRes()
+    coef = _arr(coef)
+    d = coef.shape[0] - 1
+    F0a = _arr(F0) if F0 is not None else None
+    ua = _arr(u) if u is not None else None
+    rc = lib().orc_colloc_chord(lmi._h, _p(F0a), _p(coef), d, float(tmax), int(bound), _p(ua), C.byref(r))
+    if rc:
+        raise ValueError(f"colloc_chord rc={rc}")
+    return dict(t_plus=r.t_plus, block=r.binding, outward=bool(r.outward), y=np.array(r.y[: r.ylen]))
 
 
 def walk(lmi: Lmi, kind: int, seed: int, chain_begin: int, chain_end: int, steps: int, L: float, rho: int,
-         x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, nthreads: int = 0):
+         x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, nthreads: int = 0, colloc=None):
     """Run chains [chain_begin, chain_end) (global ids key the RNG). Returns (final_x, stats)."""
     n = lmi.n
     if x0 is None:
         x0 = np.zeros(n)
     x0 = _arr(x0)
     stride = 0 if x0.ndim == 1 else n
-    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c, colloc)
     out = np.zeros((chain_end - chain_begin, n))
     st = _Stats()
     if nthreads <= 0:
@@ -302,13 +367,13 @@ def walk(lmi: Lmi, kind: int, seed: int, chain_begin: int, chain_end: int, steps
 
 
 def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_refl: int,
-          x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, stop: bool = False) -> dict:
+          x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, stop: bool = False, colloc=None) -> dict:
     """First max_refl reflections of one chain.  stop=True ends the walk right after the last
     record (orc_trace; calls = None), else the step of the last record is completed
     (orc_trace_stats; calls = every oracle call made)."""
     n = lmi.n
     x0 = _arr(np.zeros(n) if x0 is None else x0)
-    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c, colloc)
     hit = np.zeros((max_refl, n))
     t = np.zeros(max_refl)
     w = np.zeros((max_refl, n))
@@ -331,11 +396,11 @@ def trace(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho:
 
 
 def replay(lmi: Lmi, kind: int, seed: int, chain: int, steps: int, L: float, rho: int, max_calls: int,
-           x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK):
+           x0=None, T: float = 1.0, c=None, tag: int = TAG_WALK, colloc=None):
     """x of one chain after exactly max_calls chord calls (GPU state after that many rounds)."""
     n = lmi.n
     x0 = _arr(np.zeros(n) if x0 is None else x0)
-    p, keep = _params(kind, seed, tag, steps, L, rho, T, c)
+    p, keep = _params(kind, seed, tag, steps, L, rho, T, c, colloc)
     x = np.zeros(n)
     calls = C.c_int64()
     rc = lib().orc_replay(lmi._h, C.byref(p), chain, _p(x0), max_calls, _p(x), C.byref(calls))

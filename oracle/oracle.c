@@ -961,6 +961,309 @@ out:
 }
 
 /* ------------------------------------------------------------------------ */
+/* Collocation HMC-r (sec:hmcr P:1116-1158; R33)                    */
+/* ------------------------------------------------------------------------ */
+
+/* Chebyshev nodes of [0, 1] and the monomial coefficients of the Lagrange basis:
+ * column j of V^{-1}, V[i][k] = s_i^k, by Gaussian elimination with partial pivoting. */
+int orc_colloc_basis(int q, double* nodes, double* lcoef) {
+    if (q < 1 || q > 16) return 1;
+    const double pi = 3.14159265358979323846;
+    for (int j = 0; j < q; ++j) nodes[j] = 0.5 * (1.0 - cos((2.0 * j + 1.0) * pi / (2.0 * q)));
+    double* A = dalloc((size_t)q * q);
+    double* b = dalloc(q);
+    for (int j = 0; j < q; ++j) {
+        for (int i = 0; i < q; ++i) {
+            double p = 1.0;
+            for (int k = 0; k < q; ++k) {
+                A[IDX(i, k, q)] = p;
+                p *= nodes[i];
+            }
+            b[i] = (i == j) ? 1.0 : 0.0;
+        }
+        for (int c = 0; c < q; ++c) {
+            int piv = c;
+            for (int r = c + 1; r < q; ++r)
+                if (fabs(A[IDX(r, c, q)]) > fabs(A[IDX(piv, c, q)])) piv = r;
+            if (piv != c) {
+                for (int k = 0; k < q; ++k) {
+                    double t = A[IDX(c, k, q)];
+                    A[IDX(c, k, q)] = A[IDX(piv, k, q)];
+                    A[IDX(piv, k, q)] = t;
+                }
+                double t = b[c]; b[c] = b[piv]; b[piv] = t;
+            }
+            for (int r = c + 1; r < q; ++r) {
+                double f = A[IDX(r, c, q)] / A[IDX(c, c, q)];
+                for (int k = c; k < q; ++k) A[IDX(r, k, q)] -= f * A[IDX(c, k, q)];
+                b[r] -= f * b[c];
+            }
+        }
+        for (int k = q - 1; k >= 0; --k) {
+            double s = b[k];
+            for (int r = k + 1; r < q; ++r) s -= A[IDX(k, r, q)] * lcoef[(size_t)j * q + r];
+            lcoef[(size_t)j * q + k] = s / A[IDX(k, k, q)];
+        }
+    }
+    free(A); free(b);
+    return 0;
+}
+
+/* grad f (ORC_POT_*) */
+static void pot_grad(const orc_walk_params* p, int n, const double* x, double* g) {
+    for (int i = 0; i < n; ++i) {
+        if (p->pot == ORC_POT_LINEAR) g[i] = p->c[i] / p->T;
+        else if (p->pot == ORC_POT_GAUSS) g[i] = (x[i] - p->mu[i]) / (p->sigma * p->sigma);
+        else g[i] = tanh((x[i] - p->mu[i]) / p->sigma) / p->sigma;
+    }
+}
+
+/* coefficients of p(t) from the node forces G (q x n):
+ * p(t) = x0 + v0 t + sum_k (sum_j l_jk G_j) t^(k+2) / (h^k (k+1)(k+2)) */
+static void colloc_coef(int n, int q, const double* lcoef, const double* G, const double* x0, const double* v0,
+                        double h, double* coef) {
+    for (int i = 0; i < n; ++i) {
+        coef[i] = x0[i];
+        coef[n + i] = v0[i];
+    }
+    double hk = 1.0;
+    for (int k = 0; k < q; ++k) {
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < q; ++j) s += lcoef[(size_t)j * q + k] * G[(size_t)j * n + i];
+            coef[(size_t)(k + 2) * n + i] = s / (hk * (double)(k + 1) * (double)(k + 2));
+        }
+        hk *= h;
+    }
+}
+
+/* p(t) by Horner (coef of degree d, n columns) */
+static void poly_eval(int n, int d, const double* coef, double t, double* out) {
+    for (int i = 0; i < n; ++i) {
+        double a = coef[(size_t)d * n + i];
+        for (int k = d - 1; k >= 0; --k) a = a * t + coef[(size_t)k * n + i];
+        out[i] = a;
+    }
+}
+
+/* p'(t) by Horner */
+static void poly_deriv(int n, int d, const double* coef, double t, double* out) {
+    for (int i = 0; i < n; ++i) {
+        double a = (double)d * coef[(size_t)d * n + i];
+        for (int k = d - 1; k >= 1; --k) a = a * t + (double)k * coef[(size_t)k * n + i];
+        out[i] = a;
+    }
+}
+
+int orc_colloc_poly(int n, const orc_walk_params* p, const double* x0, const double* v0, double h,
+                    double* coef) {
+    int q = p->q, d = q + 1;
+    double nodes[16], lcoef[256];
+    if (orc_colloc_basis(q, nodes, lcoef)) return 0;
+    double* G = dalloc((size_t)q * n);
+    double* xj = dalloc(n);
+    double* gj = dalloc(n);
+    pot_grad(p, n, x0, gj);
+    for (int j = 0; j < q; ++j)
+        for (int i = 0; i < n; ++i) G[(size_t)j * n + i] = -gj[i];
+    int used = -ORC_COLLOC_MAXIT;
+    for (int it = 0; it < ORC_COLLOC_MAXIT; ++it) {
+        colloc_coef(n, q, lcoef, G, x0, v0, h, coef);
+        double delta = 0.0, gmax = 0.0;
+        for (int j = 0; j < q; ++j) {
+            poly_eval(n, d, coef, nodes[j] * h, xj);
+            pot_grad(p, n, xj, gj);
+            for (int i = 0; i < n; ++i) {
+                double gn = -gj[i];
+                delta = fmax(delta, fabs(gn - G[(size_t)j * n + i]));
+                gmax = fmax(gmax, fabs(gn));
+                G[(size_t)j * n + i] = gn;
+            }
+        }
+        if (delta <= 1e-14 * (1.0 + gmax)) {
+            used = it + 1;
+            break;
+        }
+    }
+    colloc_coef(n, q, lcoef, G, x0, v0, h, coef);
+    free(G); free(xj); free(gj);
+    return used;
+}
+
+/* largest real positive eigenvalue of the degree-d mu-companion
+ * [[-N_1, -N_2, ..., -N_d], [I, 0, ..., 0], ..., [0, ..., I, 0]] (P:320-354 for the reversed
+ * polynomial mu^d I + mu^(d-1) N_1 + ... + N_d) */
+static int companion_max_pos_d(int md, int d, double* const* Nk, double* mu_out) {
+    int N = d * md;
+    double* Cm = dalloc((size_t)N * N);
+    for (int i = 0; i < md; ++i) {
+        for (int k = 0; k < d; ++k)
+            for (int j = 0; j < md; ++j) Cm[IDX(i, (size_t)k * md + j, N)] = -Nk[k][IDX(i, j, md)];
+    }
+    for (int r = md; r < N; ++r) Cm[IDX(r, r - md, N)] = 1.0;
+    hessenberg(N, Cm);
+    double* wr = dalloc(N);
+    double* wi = dalloc(N);
+    int rc = francis_qr(N, Cm, wr, wi);
+    double best = 0.0;
+    int found = 0;
+    for (int i = 0; i < N; ++i) {
+        if (fabs(wi[i]) <= 1e-8 * (1.0 + fabs(wr[i])) && wr[i] > 0.0) {
+            if (!found || wr[i] > best) best = wr[i];
+            found = 1;
+        }
+    }
+    *mu_out = found ? best : 0.0;
+    free(Cm); free(wr); free(wi);
+    return rc;
+}
+
+int orc_pep_root(int mb, int d, const double* B, int bound, const double* u, double tmax, double* t_plus,
+                 double* y) {
+    size_t ss = (size_t)mb * mb;
+    int rc = 0;
+    double mu = 0.0;
+    if (d < 1) return 1;
+    double** Nk = (double**)xmalloc(sizeof(double*) * d);
+    for (int k = 0; k < d; ++k) Nk[k] = dalloc(ss);
+    double* col = dalloc(mb);
+    double* z = dalloc(mb);
+    double* z2 = dalloc(mb);
+    if (!bound) {
+        /* L L^T = B_0, N_k = L^{-1} B_k L^{-T} */
+        double* Lw = dalloc(ss);
+        double* X = dalloc(ss);
+        if (orc_cholesky(mb, B, Lw)) rc = 2;
+        for (int k = 1; k <= d && !rc; ++k) {
+            const double* Bk = B + (size_t)k * ss;
+            for (int j = 0; j < mb; ++j) {
+                for (int i = 0; i < mb; ++i) col[i] = Bk[IDX(i, j, mb)];
+                forward_sub(mb, Lw, col, z);
+                for (int i = 0; i < mb; ++i) X[IDX(i, j, mb)] = z[i];
+            }
+            for (int j = 0; j < mb; ++j) {
+                for (int i = 0; i < mb; ++i) col[i] = X[IDX(j, i, mb)];
+                forward_sub(mb, Lw, col, z);
+                for (int i = 0; i < mb; ++i) Nk[k - 1][IDX(j, i, mb)] = z[i];
+            }
+        }
+        if (!rc) rc = companion_max_pos_d(mb, d, Nk, &mu);
+        free(Lw); free(X);
+    } else {
+        /* P_k = H B_k H; the first row of P(t) divided by t: G~_k row 0 = P_(k+1) row 0
+         * (k < d; 0 for k = d), rows >= 1 = those of P_k; G~_0 = [[a1, b1^T], [0, Bh]] */
+        double* H = dalloc(ss);
+        householder_matrix(mb, u, H);
+        double** P = (double**)xmalloc(sizeof(double*) * (d + 1));
+        for (int k = 0; k <= d; ++k) {
+            P[k] = dalloc(ss);
+            congruence_H(mb, H, B + (size_t)k * ss, P[k]);
+        }
+        double a1 = P[1][0];
+        int mh = mb - 1;
+        double* Lw = dalloc((size_t)(mh > 0 ? mh : 1) * (mh > 0 ? mh : 1));
+        double* Bh = dalloc((size_t)(mh > 0 ? mh : 1) * (mh > 0 ? mh : 1));
+        double* Gk = dalloc(ss);
+        if (!(a1 > 0.0)) {
+            rc = 3;
+        } else {
+            for (int i = 0; i < mh; ++i)
+                for (int j = 0; j < mh; ++j) Bh[IDX(i, j, mh)] = P[0][IDX(i + 1, j + 1, mb)];
+            if (mh > 0 && orc_cholesky(mh, Bh, Lw)) rc = 2;
+        }
+        for (int k = 1; k <= d && !rc; ++k) {
+            for (int j = 0; j < mb; ++j) {
+                Gk[IDX(0, j, mb)] = (k < d) ? P[k + 1][IDX(0, j, mb)] : 0.0;
+                for (int i = 1; i < mb; ++i) Gk[IDX(i, j, mb)] = P[k][IDX(i, j, mb)];
+            }
+            /* N_k = G~_0^{-1} G~_k by block back substitution */
+            for (int j = 0; j < mb; ++j) {
+                for (int i = 1; i < mb; ++i) col[i - 1] = Gk[IDX(i, j, mb)];
+                if (mh > 0) {
+                    forward_sub(mh, Lw, col, z);
+                    back_sub_T(mh, Lw, z, z2);
+                }
+                double s = Gk[IDX(0, j, mb)];
+                for (int i = 0; i < mh; ++i) s -= P[1][IDX(0, i + 1, mb)] * z2[i];
+                Nk[k - 1][IDX(0, j, mb)] = s / a1;
+                for (int i = 0; i < mh; ++i) Nk[k - 1][IDX(i + 1, j, mb)] = z2[i];
+            }
+        }
+        if (!rc) rc = companion_max_pos_d(mb, d, Nk, &mu);
+        for (int k = 0; k <= d; ++k) free(P[k]);
+        free(P); free(H); free(Lw); free(Bh); free(Gk);
+    }
+    for (int k = 0; k < d; ++k) free(Nk[k]);
+    free(Nk); free(col); free(z); free(z2);
+    if (rc == 3) {
+        *t_plus = 0.0;
+        return 3;
+    }
+    if (rc) return rc;
+    *t_plus = (mu > 0.0 && 1.0 / mu <= tmax) ? 1.0 / mu : INFINITY;
+    if (y) {
+        if (isfinite(*t_plus)) {
+            double tp = *t_plus;
+            double* G = dalloc(ss);
+            for (size_t e = 0; e < ss; ++e) {
+                double a = B[(size_t)d * ss + e];
+                for (int k = d - 1; k >= 0; --k) a = a * tp + B[(size_t)k * ss + e];
+                G[e] = a;
+            }
+            null_vector(mb, G, y);
+            free(G);
+        } else {
+            for (int i = 0; i < mb; ++i) y[i] = 0.0;
+        }
+    }
+    return 0;
+}
+
+int orc_colloc_chord(const orc_lmi* L, const double* F0, const double* coef, int d, double tmax, int bound,
+                     const double* u, orc_chord_res* r) {
+    int n = L->n;
+    r->t_plus = INFINITY;
+    r->t_minus = -INFINITY;
+    r->binding = -1;
+    r->degenerate = 0;
+    r->outward = 0;
+    r->ylen = 0;
+    int maxmb = 0;
+    for (int b = 0; b < L->nblocks; ++b)
+        if (L->mb[b] > maxmb) maxmb = L->mb[b];
+    if (maxmb > 1024) return 1;
+    size_t mm = (size_t)maxmb * maxmb;
+    double* B = dalloc((size_t)(d + 1) * mm);
+    double* y = dalloc(maxmb);
+    int rc = 0;
+    for (int b = 0; b < L->nblocks; ++b) {
+        int s = L->mb[b];
+        size_t ss = (size_t)s * s;
+        if (b == 0 && F0) memcpy(B, F0, sizeof(double) * ss);
+        else orc_eval_block(L, b, coef, B);
+        for (int k = 1; k <= d; ++k) orc_dir_block(L, b, coef + (size_t)k * n, B + (size_t)k * ss);
+        double tp;
+        int brc = orc_pep_root(s, d, B, b == bound, (b == bound) ? u : NULL, tmax, &tp, y);
+        if (brc == 3) {
+            r->t_plus = 0.0;
+            r->binding = b;
+            r->outward = 1;
+            goto out;
+        }
+        if (brc) { rc = 2; goto out; }
+        if (tp < r->t_plus) {
+            r->t_plus = tp;
+            r->binding = b;
+            r->ylen = s;
+            memcpy(r->y, y, sizeof(double) * s);
+        }
+    }
+out:
+    free(B); free(y);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Walks                                                                      */
 /* ------------------------------------------------------------------------ */
 
@@ -977,6 +1280,8 @@ typedef struct {
     double* u;    /* unit kernel vector of the bound block */
     orc_chord_res* res;
     int64_t budget; /* stop after this many chord calls (-1: none) */
+    double* coef; /* collocation polynomial, (q+2) x n (q <= 6) */
+    double* Fk;   /* dense-block F1(coef_k), k = 1..q+1 */
 } walk_ws;
 
 static void ws_init(walk_ws* W, const orc_lmi* L) {
@@ -990,10 +1295,12 @@ static void ws_init(walk_ws* W, const orc_lmi* L) {
     W->u = dalloc(maxmb);
     W->res = (orc_chord_res*)xmalloc(sizeof(orc_chord_res));
     W->budget = -1;
+    W->coef = dalloc((size_t)8 * n);
+    W->Fk = dalloc((size_t)7 * m * m);
 }
 static void ws_free(walk_ws* W) {
     free(W->x); free(W->xs); free(W->v); free(W->g); free(W->w); free(W->F); free(W->Fs);
-    free(W->F1); free(W->F2c); free(W->u); free(W->res);
+    free(W->F1); free(W->F2c); free(W->u); free(W->res); free(W->coef); free(W->Fk);
 }
 
 typedef struct {
@@ -1067,12 +1374,101 @@ static int hnr_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, 
     return 0;
 }
 
+/* One step of collocation HMC-r (Alg. 6 P:1079-1115 with the polynomial trajectories of
+ * P:1146-1158; R33): l = tau eta, v ~ N(0, I); then, while l > 0, the segment
+ * [0, h'] with h' = min(h, l) follows the collocation polynomial p(t) from (x, v); its chord
+ * is the first root of det F(p(t)) in (0, h'] over every block (Lemma 3 for degree d = q + 1).
+ * No root: x = p(h'), v = p'(h'), l -= h' (not a reflection).  Root t+: x = p(t+), the
+ * velocity p'(t+) is reflected at the hit (Alg. 3), l -= t+, and the reflection counts
+ * towards rho.  F(x) is carried as F += sum_k t^k F1(coef_k). */
+static int chmc_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, uint32_t step, walk_ws* W,
+                     orc_stats* st, trace_rec* tr) {
+    int n = L->n, m = L->mb[0];
+    size_t mm = (size_t)m * m;
+    const int d = p->q + 1;
+    double eta;
+    orc_step_draws(p->seed, p->tag, chain, step, n, W->g, &eta);
+    double ell = p->L * eta; /* l = tau eta (Alg. 6 line 1) */
+    for (int i = 0; i < n; ++i) W->v[i] = W->g[i]; /* v ~ N(0, I) */
+    memcpy(W->xs, W->x, sizeof(double) * n);
+    memcpy(W->Fs, W->F, sizeof(double) * mm);
+    int64_t refl = 0;
+    int bound = -1;
+    st->steps += 1;
+    double* coef = W->coef;
+    for (;;) {
+        if (W->budget >= 0 && st->calls >= W->budget) return 5;
+        const int last = (ell <= p->h);
+        const double hs = last ? ell : p->h;
+        orc_colloc_poly(n, p, W->x, W->v, hs, coef);
+        for (int k = 1; k <= d; ++k) orc_dir_block(L, 0, coef + (size_t)k * n, W->Fk + (size_t)(k - 1) * mm);
+        orc_chord_res* r = W->res;
+        int rc = orc_colloc_chord(L, W->F, coef, d, hs, bound, W->u, r);
+        st->calls += 1;
+        if (rc) return rc;
+        if (r->outward) {
+            st->degenerates += 1;
+            goto reject;
+        }
+        double tp = r->t_plus;
+        const double th = (hs <= tp) ? hs : tp; /* reading R4: a tie ends the segment, no reflection */
+        poly_eval(n, d, coef, th, W->x);
+        poly_deriv(n, d, coef, th, W->g);
+        for (size_t e = 0; e < mm; ++e) {
+            double a = W->Fk[(size_t)(d - 1) * mm + e];
+            for (int k = d - 1; k >= 1; --k) a = a * th + W->Fk[(size_t)(k - 1) * mm + e];
+            W->F[e] += th * a;
+        }
+        if (hs <= tp) {
+            if (last) return 0;
+            ell -= hs;
+            memcpy(W->v, W->g, sizeof(double) * n);
+            bound = -1;
+            continue;
+        }
+        ell -= tp;
+        refl += 1;
+        st->reflections += 1;
+        if (refl > p->rho) {
+            st->rejects += 1;
+            goto reject;
+        }
+        if (r->degenerate || orc_normal(L, r->binding, r->y, r->ylen, W->w)) {
+            st->degenerates += 1;
+            goto reject;
+        }
+        orc_reflect(n, W->g, W->w, W->v);
+        {
+            double ny = 0.0;
+            for (int i = 0; i < r->ylen; ++i) ny += r->y[i] * r->y[i];
+            ny = sqrt(ny);
+            for (int i = 0; i < r->ylen; ++i) W->u[i] = r->y[i] / ny;
+        }
+        bound = r->binding;
+        if (tr && tr->nrec < tr->max_refl) {
+            int64_t k = tr->nrec;
+            memcpy(tr->hit_x + k * n, W->x, sizeof(double) * n);
+            tr->t[k] = tp;
+            memcpy(tr->w + k * n, W->w, sizeof(double) * n);
+            memcpy(tr->v_after + k * n, W->v, sizeof(double) * n);
+            tr->binding[k] = r->binding;
+            tr->nrec += 1;
+            if (tr->stop && tr->nrec >= tr->max_refl) return 6;
+        }
+    }
+reject:
+    memcpy(W->x, W->xs, sizeof(double) * n);
+    memcpy(W->F, W->Fs, sizeof(double) * mm);
+    return 0;
+}
+
 static int walk_step(const orc_lmi* L, const orc_walk_params* p, uint32_t chain, uint32_t step,
                      walk_ws* W, orc_stats* st, trace_rec* tr) {
     int n = L->n, m = L->mb[0];
     size_t mm = (size_t)m * m;
     double eta;
     if (p->kind == ORC_HNR || p->kind == ORC_CHNR) return hnr_step(L, p, chain, step, W, st);
+    if (p->kind == ORC_CHMC) return chmc_step(L, p, chain, step, W, st, tr);
     orc_step_draws(p->seed, p->tag, chain, step, n, W->g, &eta);
     double ell;
     if (p->kind == ORC_BILLIARD) {

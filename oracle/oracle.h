@@ -90,7 +90,9 @@ void orc_reflect(int n, const double* u, const double* w, double* s);
 int orc_membership(const orc_lmi* L, const double* x);
 
 /* ---- walks ---- */
-enum { ORC_BILLIARD = 0, ORC_HMC = 1, ORC_HNR = 2, ORC_CHNR = 3 }; /* HnR: Alg. 4; CHnR: P:985-996 */
+enum { ORC_BILLIARD = 0, ORC_HMC = 1, ORC_HNR = 2, ORC_CHNR = 3, ORC_CHMC = 4 }; /* HnR: Alg. 4; CHnR: P:985-996;
+                                                                    CHMC: HMC-r on collocation polynomials P:1146-1158 */
+enum { ORC_POT_LINEAR = 0, ORC_POT_GAUSS = 1, ORC_POT_LOGCOSH = 2 };
 typedef struct orc_stats {
     int64_t calls, reflections, rejects, degenerates, steps, failures;
 } orc_stats;
@@ -104,6 +106,13 @@ typedef struct orc_walk_params {
     int64_t rho;
     double T;      /* HMC temperature */
     const double* c; /* HMC objective (n) */
+    /* ORC_CHMC only (collocation HMC-r for exp(-f), sec:hmcr P:1116-1158): */
+    int pot;          /* ORC_POT_*: f = c^T x / T (LINEAR), |x - mu|^2 / (2 sigma^2) (GAUSS),
+                         sum_i log cosh((x_i - mu_i) / sigma) (LOGCOSH) */
+    const double* mu; /* n (GAUSS, LOGCOSH) */
+    double sigma;
+    int q;            /* collocation nodes (1..6): trajectory degree d = q + 1 */
+    double h;         /* ODE step: one polynomial covers at most [0, h] */
 } orc_walk_params;
 
 /* Run chains [chain_begin, chain_end) for p->steps steps from x0 (stride 0:
@@ -130,6 +139,32 @@ int orc_qep_root(int mb, const double* B0, const double* B1, const double* B2, i
                  const double* u, double* t_plus, double* y);
 int orc_hmc_chord(const orc_lmi* L, const double* x, const double* F0, const double* v,
                   const double* c, double T, int bound, const double* u, orc_chord_res* r);
+
+/* ---- collocation HMC-r (sec:hmcr P:1116-1158; Lemma 3 P:587-651 for degree d) ----
+ * Collocation ([Lee18]): on [0, h] the trajectory of p'' = -grad f(p),
+ * p(0) = x0, p'(0) = v0 is the degree-(q+1) polynomial whose second derivative
+ * interpolates -grad f(p(h s_j)) at the q Chebyshev nodes s_j = (1 - cos((2j+1) pi / 2q)) / 2
+ * of [0, 1]; the node values come from Picard (fixed-point) iteration.  DESIGN.md R33.
+ * orc_colloc_basis: nodes[q] and lcoef[q*q], lcoef[j*q + k] = coefficient of s^k in the
+ * Lagrange basis polynomial l_j (Vandermonde solve by Gaussian elimination).
+ * orc_colloc_poly: coef[(q+2)*n], coef[k*n + i] = coefficient of t^k of p_i(t); returns
+ * the Picard iterations used (stop when the node forces move by <= 1e-14 (1 + max|g|)),
+ * or -(ORC_COLLOC_MAXIT) if that never happened (the last iterate is returned). */
+#define ORC_COLLOC_MAXIT 64
+int orc_colloc_basis(int q, double* nodes, double* lcoef);
+int orc_colloc_poly(int n, const orc_walk_params* p, const double* x0, const double* v0, double h,
+                    double* coef);
+/* First root in (0, tmax] of det(B_0 + t B_1 + ... + t^d B_d) for one block (Lemma 3 with a
+ * degree-d curve; PEP by the mu = 1/t companion linearisation of P:320-354 + Francis QR).
+ * B: (d+1) row-major mb x mb matrices.  Boundary start (bound != 0, B_0 u = 0): Householder
+ * basis of u and the first row of the pencil divided by t (as orc_qep_root).  t_plus = +inf
+ * if no root in (0, tmax].  Returns 0, 2 (B_0 not PD), 3 (outward: u^T B_1 u <= 0). */
+int orc_pep_root(int mb, int d, const double* B, int bound, const double* u, double tmax, double* t_plus,
+                 double* y);
+/* chord of the curve p(t) = sum_k coef_k t^k (coef as orc_colloc_poly, degree d) over every
+ * block, t in (0, tmax]; F0 = carried dense block F_0(coef_0) (NULL: evaluate). */
+int orc_colloc_chord(const orc_lmi* L, const double* F0, const double* coef, int d, double tmax, int bound,
+                     const double* u, orc_chord_res* r);
 
 #ifdef __cplusplus
 }
