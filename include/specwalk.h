@@ -76,6 +76,16 @@ int spec_destroy(spec_ctx* ctx);
  * HMC-r (eq:boltz_ode).  EINVAL if |c| = 0. */
 int spec_set_objective(spec_ctx* ctx, const double* c);
 
+/* Potential f of the density exp(-f) sampled by SPEC_WALK_CHMC / chmc_oracle (sec:hmcr
+ * P:1116-1124):
+ *   SPEC_POT_LINEAR  f = c^T x / scale        (c from spec_set_objective; the Boltzmann law)
+ *   SPEC_POT_GAUSS   f = |x - mu|^2 / (2 scale^2)
+ *   SPEC_POT_LOGCOSH f = sum_i log cosh((x_i - mu_i) / scale)
+ * mu: host n doubles (NULL = 0; ignored by LINEAR).  EINVAL: unknown pot, scale <= 0 or not
+ * finite, NaN in mu, LINEAR without an objective. */
+enum { SPEC_POT_LINEAR = 0, SPEC_POT_GAUSS = 1, SPEC_POT_LOGCOSH = 2 };
+int spec_set_potential(spec_ctx* ctx, int pot, const double* mu, double scale);
+
 /* Ball constraint |x - center| <= radius added to S (a volume phase S_i of
  * eq:mmc_vol).  radius <= 0 removes it.  center: host n doubles. */
 int spec_set_ball(spec_ctx* ctx, const double* center, double radius);
@@ -120,6 +130,17 @@ int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const dou
 int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, double T,
                double* t_plus, double* normal, double* kernel, int32_t* binding);
 
+/* chmc_oracle -- one collocation-HMC segment per line (sec:hmcr P:1116-1158, Lemma 3 for a
+ * degree-(q+1) curve): the polynomial p(t) of p'' = -grad f on [0, h] from (x, v) (f from
+ * spec_set_potential), and its first boundary hit in (0, h].  Arguments as hmc_oracle (host
+ * pointers; u: batch x m unit kernel vectors of F(x) for lines starting on the dense boundary,
+ * or NULL).  t_plus: the hit time, or +inf when p stays inside on (0, h]; binding, normal,
+ * kernel: as boundary_oracle.  A line whose start moves outward gets t_plus = 0 and the status
+ * text in spec_last_error; one that hits the Weyl iteration cap gets NaN.  EPRECOND: some x is
+ * not interior.  EINVAL: no potential, q not in 1..6, h <= 0. */
+int chmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, int q, double h,
+                double* t_plus, double* normal, double* kernel, int32_t* binding);
+
 /* ---- walks ---- */
 /* BILLIARD: Alg. 5; HMC: reflective HMC for exp(-c^T x / T), Alg. 6
  * (P:1079-1115); HNR: Hit-and-Run for the uniform law, Alg. 4 -- the next point
@@ -129,7 +150,14 @@ int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, c
  * step and never reflects (L and rho are ignored); with 0 < T < inf it samples the
  * Boltzmann law exp(-c^T x / T) (sec:optimization P:1408-1424; needs the objective): the
  * point on the chord is a truncated exponential; T <= 0 or T = inf: the uniform law. */
-enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1, SPEC_WALK_HNR = 2, SPEC_WALK_CHNR = 3 };
+enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1, SPEC_WALK_HNR = 2, SPEC_WALK_CHNR = 3, SPEC_WALK_CHMC = 4 };
+/* CHMC: reflective HMC for a log-concave density exp(-f) on collocation polynomials (sec:hmcr
+ * P:1116-1158; R33; f from spec_set_potential): l = L eta, v ~ N(0, I); the ODE
+ * p'' = -grad f(p) is followed in segments of length h' = min(h, l_left), each the degree-(q+1)
+ * polynomial through (x, v) whose second derivative matches -grad f at q Chebyshev nodes (Picard
+ * iteration); a segment's chord is the first root of det F(p(t)) in (0, h'] (Lemma 3 for a
+ * degree-d curve).  No root: x = p(h'), v = p'(h').  A root t+: p'(t+) is reflected (Alg. 3) and
+ * the reflection counts towards rho.  One segment = one boundary-oracle call. */
 
 typedef struct spec_walk_params {
     int kind;            /* SPEC_WALK_BILLIARD (Alg. 5), SPEC_WALK_HMC (Alg. 6, Boltzmann), SPEC_WALK_HNR, SPEC_WALK_CHNR */
@@ -142,6 +170,8 @@ typedef struct spec_walk_params {
     uint32_t tag;        /* counter word 3 (purpose << 28 | phase), 0 for plain walks */
     double T;            /* HMC temperature (>0); Hit-and-Run: 0 < T < inf Boltzmann, else uniform;
                             ignored for billiard */
+    int q;               /* CHMC: collocation nodes (1..6), trajectory degree q + 1 */
+    double h;            /* CHMC: ODE segment length (> 0) */
 } spec_walk_params;
 
 typedef struct spec_walk_stats {

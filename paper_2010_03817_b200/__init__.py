@@ -26,7 +26,9 @@ _lp = C.POINTER(C.c_int64)
 
 SPEC_OK = 0
 ERRORS = {1: "EINVAL", 2: "EPRECOND", 3: "ERUNTIME", 4: "ECUDA", 5: "ENOMEM", 6: "EUNBOUNDED"}
-BILLIARD, HMC, HNR, CHNR = 0, 1, 2, 3  # Alg. 5, Alg. 6, Alg. 4, W-CHnR
+BILLIARD, HMC, HNR, CHNR, CHMC = 0, 1, 2, 3, 4  # Alg. 5, Alg. 6, Alg. 4, W-CHnR,
+#                                                collocation HMC-r
+POT_LINEAR, POT_GAUSS, POT_LOGCOSH = 0, 1, 2
 BIND_DENSE, BIND_BALL, BIND_NONE = 0, -1, -2
 
 # the symbols include/specwalk.h declares (checked by tests/test_abi.py)
@@ -35,7 +37,7 @@ EXPORTS = (
     "boundary_oracle_dev", "walk_sample", "walk_sample_dev", "walk_trace", "spec_sync", "spec_stream",
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
     "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
-    "spec_lanczos_iterations", "sdp_anneal", "spec_k2_config",
+    "spec_lanczos_iterations", "sdp_anneal", "spec_k2_config", "spec_set_potential", "chmc_oracle",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -84,6 +86,7 @@ class WalkParams(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("chain_begin", C.c_int64), ("chains", C.c_int64), ("steps", C.c_int64),
         ("L", C.c_double), ("rho", C.c_int64), ("seed", C.c_uint64), ("tag", C.c_uint32), ("T", C.c_double),
+        ("q", C.c_int), ("h", C.c_double),
     ]
 
 
@@ -145,6 +148,8 @@ def load(build_if_missing: bool = True):
     l.spec_k2_config.restype = C.c_char_p
     l.sdp_anneal.argtypes = [C.c_void_p, C.POINTER(SdpParams), _dp, _dp, C.POINTER(SdpReport)]
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
+    l.chmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _ip]
+    l.spec_set_potential.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
     l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
                          C.POINTER(VolumeReport)]
@@ -195,6 +200,11 @@ class Spectrahedron:
 
     def set_objective(self, c):
         _check(_lib.spec_set_objective(self._h, _p(_f64(c))))
+
+    def set_potential(self, pot: int, mu=None, scale: float = 1.0):
+        """Potential f of exp(-f) for collocation HMC-r (POT_LINEAR: c^T x / scale with the
+        objective; POT_GAUSS: |x - mu|^2 / 2 scale^2; POT_LOGCOSH: sum log cosh((x - mu) / scale))."""
+        _check(_lib.spec_set_potential(self._h, int(pot), _p(_f64(mu)) if mu is not None else None, float(scale)))
 
     def set_ball(self, center, radius: float):
         _check(_lib.spec_set_ball(self._h, _p(_f64(center)) if center is not None else None, float(radius)))
@@ -301,6 +311,24 @@ class Spectrahedron:
             out["kernel"] = ker
         return out
 
+    def chmc_oracle(self, x, v, q: int, h: float, u=None, want_kernel: bool = False) -> dict:
+        """One collocation-HMC segment per line: first boundary hit in (0, h] (+inf: none)."""
+        x, v = _f64(x), _f64(v)
+        if x.ndim == 1:
+            x, v = x[None], v[None]
+        B = x.shape[0]
+        ua = _f64(u).reshape(B, self.m) if u is not None else None
+        tp = np.empty(B)
+        nrm = np.empty((B, self.n))
+        ker = np.empty((B, self.m)) if want_kernel else None
+        bind = np.empty(B, dtype=np.int32)
+        _check(_lib.chmc_oracle(self._h, B, _p(x), _p(v), _p(ua), int(q), float(h), _p(tp), _p(nrm), _p(ker),
+                                bind.ctypes.data_as(_ip)))
+        out = dict(t_plus=tp, normal=nrm, binding=bind)
+        if want_kernel:
+            out["kernel"] = ker
+        return out
+
     def boundary_oracle_dev(self, x, v, u, t_minus, t_plus, normal, kernel, binding):
         """Device-pointer variant: arguments are torch CUDA tensors (or None for u / kernel)."""
         ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
@@ -309,17 +337,19 @@ class Spectrahedron:
 
     # -------------------------------------------------------------- walks
     @staticmethod
-    def _params(kind, chains, steps, L, rho, seed, chain_begin=0, tag=0, T=None) -> WalkParams:
+    def _params(kind, chains, steps, L, rho, seed, chain_begin=0, tag=0, T=None, q=3, h=0.0) -> WalkParams:
         if T is None:  # HMC: T = 1; Hit-and-Run: the uniform law (T = inf); ignored by the billiard
             T = 1.0 if kind == HMC else float("inf")
         p = WalkParams()
         p.kind, p.chain_begin, p.chains, p.steps = kind, chain_begin, chains, steps
         p.L, p.rho, p.seed, p.tag, p.T = float(L), rho, seed, tag, float(T)
+        p.q, p.h = int(q), float(h)
         return p
 
     def walk_sample(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD,
-                    x0=None, chain_begin: int = 0, tag: int = 0, T: Optional[float] = None, final: bool = True) -> dict:
-        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
+                    x0=None, chain_begin: int = 0, tag: int = 0, T: Optional[float] = None, final: bool = True,
+                    q: int = 3, h: float = 0.0) -> dict:
+        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T, q, h)
         per_chain = 0
         x0a = None
         if x0 is not None:
@@ -334,8 +364,8 @@ class Spectrahedron:
 
     def walk_sample_dev(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD,
                         x0=None, sum_x=None, sum_xx=None, final_x=None, chain_begin: int = 0, tag: int = 0,
-                        T: Optional[float] = None) -> dict:
-        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
+                        T: Optional[float] = None, q: int = 3, h: float = 0.0) -> dict:
+        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T, q, h)
         ptr = lambda t: None if t is None else C.c_void_p(t.data_ptr())
         per_chain = 1 if (x0 is not None and x0.dim() == 2) else 0
         st = WalkStats()
@@ -345,8 +375,8 @@ class Spectrahedron:
 
     # resumable walk: begin / rounds / end (device buffers are torch CUDA tensors)
     def walk_begin(self, chains: int, steps: int, L: float, rho: int, seed: int, kind: int = BILLIARD, x0=None,
-                   chain_begin: int = 0, tag: int = 0, T: Optional[float] = None):
-        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T)
+                   chain_begin: int = 0, tag: int = 0, T: Optional[float] = None, q: int = 3, h: float = 0.0):
+        p = self._params(kind, chains, steps, L, rho, seed, chain_begin, tag, T, q, h)
         ptr = None if x0 is None else C.c_void_p(x0.data_ptr())
         per_chain = 1 if (x0 is not None and x0.dim() == 2) else 0
         _check(_lib.walk_begin(self._h, C.byref(p), ptr, per_chain))
@@ -389,11 +419,11 @@ class Spectrahedron:
         return dict(mean_j=mj.value, solves=ns.value)
 
     def walk_trace(self, chain_ids, steps: int, L: float, rho: int, seed: int, max_refl: int,
-                   kind: int = BILLIARD, T: Optional[float] = None) -> list:
+                   kind: int = BILLIARD, T: Optional[float] = None, q: int = 3, h: float = 0.0) -> list:
         """First max_refl reflections of the given global chain ids (parity entry)."""
         ids = np.ascontiguousarray(np.asarray(chain_ids, dtype=np.int64))
         k = len(ids)
-        p = self._params(kind, k, steps, L, rho, seed, 0, 0, T)
+        p = self._params(kind, k, steps, L, rho, seed, 0, 0, T, q, h)
         n = self.n
         hit = np.zeros((k, max_refl, n))
         t = np.zeros((k, max_refl))

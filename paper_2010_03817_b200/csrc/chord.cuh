@@ -298,9 +298,9 @@ __device__ void step_start(const Team& T, int slot, long long gidv, int step, in
     const double* ax = AX + (size_t)slot * mtp;
     double* axs = AXs + (size_t)slot * mtp;
     for (int i = T.tid; i < mt; i += T.nthr) axs[i] = ax[i];
-    // ell: billiard -L ln eta, HMC L eta (Alg. 5 / Alg. 6 line 1); Hit-and-Run keeps eta (the
+    // ell: billiard -L ln eta, HMC / collocation HMC L eta (Alg. 5 / Alg. 6 line 1); Hit-and-Run keeps eta (the
     // position of the next point on the chord)
-    if (T.tid == 0) ell[slot] = (kind == 0) ? -Lpar * log(eta) : (kind == 1 ? Lpar * eta : eta);
+    if (T.tid == 0) ell[slot] = (kind == 0) ? -Lpar * log(eta) : ((kind == 1 || kind == 4) ? Lpar * eta : eta);
     if (CTA) __syncthreads(); else __syncwarp();
 }
 

@@ -24,6 +24,7 @@
 #include "lanczos_cl.cuh"
 #include "hmc.cuh"
 #include "hmc2.cuh"
+#include "colloc.cuh"
 #include "estimators.cuh"
 #include <algorithm>
 
@@ -89,6 +90,20 @@ struct HmcBuf {
     int *il0 = nullptr, *il1 = nullptr, *cnt = nullptr;
 };
 
+// K7 (collocation HMC-r, colloc.cuh) per-slot buffers, grown with the chain capacity and d
+struct ChmcBuf {
+    long long cap = 0;
+    int d = 0;
+    double *CF = nullptr, *CB = nullptr, *GW = nullptr, *hseg = nullptr;
+    int* elist = nullptr;
+};
+static void free_chmc_bufs(ChmcBuf& h) {
+    void* ps[] = {h.CF, h.CB, h.GW, h.hseg, h.elist};
+    for (void* p : ps)
+        if (p) cudaFree(p);
+    h = ChmcBuf();
+}
+
 struct spec_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -143,6 +158,17 @@ struct spec_ctx {
     spec_comm comm{nullptr, 0, 1, nullptr};
     int has_comm = 0;
     void* obuf = nullptr;  // OracleBuf*
+    // collocation HMC-r (K7): potential f of exp(-f) (spec_set_potential) and its buffers
+    int pot = -1;
+    double pot_scale = 1.0;
+    double* pot_mu = nullptr;
+    int has_mu = 0;
+    ChmcBuf chb;
+    double* chmc_scratch = nullptr;
+    long long chmc_stride = 0;
+    int chmc_grid = 0, chmc_d = 0;
+    size_t chmc_smem = 0;
+    unsigned long long* picard = nullptr;  // Picard iterations, segments, unconverged
 };
 
 static void free_chains(ChainBuf& b) {
@@ -446,11 +472,12 @@ extern "C" int spec_destroy(spec_ctx* ctx) {
     cudaSetDevice(ctx->dev);
     free_chains(ctx->cb);
     free_hmc_bufs(ctx->hb);
+    free_chmc_bufs(ctx->chb);
     if (ctx->obuf) {
         free_obuf(*(OracleBuf*)ctx->obuf);
         delete (OracleBuf*)ctx->obuf;
     }
-    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->c0, ctx->scratch, ctx->dstats, ctx->jsum, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch};
+    void* ps[] = {ctx->Ahat, ctx->a0, ctx->lo, ctx->hi, ctx->c, ctx->ball_c, ctx->c0, ctx->scratch, ctx->dstats, ctx->jsum, ctx->prof, ctx->lsave, ctx->Ac, ctx->hmc_scratch, ctx->pot_mu, ctx->chmc_scratch, ctx->picard};
     for (void* p : ps)
         if (p) cudaFree(p);
     if (ctx->e0) cudaEventDestroy(ctx->e0);
@@ -753,6 +780,136 @@ static int launch_hmc(spec_ctx* ctx, ChordParams P, int count_host) {
     return SPEC_OK;
 }
 
+// ---------------------------------------------------------------- K7: collocation HMC-r
+extern "C" int spec_set_potential(spec_ctx* ctx, int pot, const double* mu, double scale) {
+    if (!ctx) return fail(SPEC_EINVAL, "null ctx");
+    SW_NOT_DURING_WALK(ctx);
+    if (pot != SPEC_POT_LINEAR && pot != SPEC_POT_GAUSS && pot != SPEC_POT_LOGCOSH)
+        return fail(SPEC_EINVAL, "unknown potential");
+    if (!(scale > 0.0) || !std::isfinite(scale)) return fail(SPEC_EINVAL, "scale must be finite and > 0");
+    if (pot == SPEC_POT_LINEAR && !ctx->has_obj) return fail(SPEC_EINVAL, "SPEC_POT_LINEAR needs spec_set_objective");
+    CK(cudaSetDevice(ctx->dev));
+    if (!ctx->pot_mu) CK(zalloc(&ctx->pot_mu, ctx->n));
+    if (mu) {
+        for (int i = 0; i < ctx->n; ++i)
+            if (!std::isfinite(mu[i])) return fail(SPEC_EINVAL, "mu has NaN/Inf");
+        CK(cudaMemcpyAsync(ctx->pot_mu, mu, sizeof(double) * ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+    } else {
+        CK(cudaMemsetAsync(ctx->pot_mu, 0, sizeof(double) * ctx->n, ctx->stream));
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->pot = pot;
+    ctx->pot_scale = scale;
+    return SPEC_OK;
+}
+
+// Chebyshev nodes of [0, 1] and the monomial coefficients of the Lagrange basis, by expanding
+// l_j(s) = prod_{i != j} (s - s_i) / (s_j - s_i) (R33)
+static void chmc_basis(int q, double* nodes, double* lcoef) {
+    const double pi = 3.14159265358979323846;
+    for (int j = 0; j < q; ++j) nodes[j] = 0.5 * (1.0 - std::cos((2.0 * j + 1.0) * pi / (2.0 * q)));
+    for (int j = 0; j < q; ++j) {
+        double poly[CH_MAXQ + 1] = {1.0};
+        int deg = 0;
+        for (int i = 0; i < q; ++i) {
+            if (i == j) continue;
+            const double den = nodes[j] - nodes[i];
+            double nxt[CH_MAXQ + 1] = {0.0};
+            for (int k = 0; k <= deg; ++k) {
+                nxt[k + 1] += poly[k] / den;
+                nxt[k] -= poly[k] * nodes[i] / den;
+            }
+            ++deg;
+            for (int k = 0; k <= deg; ++k) poly[k] = nxt[k];
+        }
+        for (int k = 0; k < q; ++k) lcoef[j * q + k] = poly[k];
+    }
+}
+
+static int check_chmc(spec_ctx* ctx, int q, double h) {
+    if (ctx->pot < 0) return fail(SPEC_EINVAL, "collocation HMC needs spec_set_potential");
+    if (q < 1 || q > CH_MAXQ) return fail(SPEC_EINVAL, "collocation nodes q must be in 1..6");
+    if (!(h > 0.0) || !std::isfinite(h)) return fail(SPEC_EINVAL, "collocation step h must be finite and > 0");
+    if (ctx->has_ball) return fail(SPEC_EINVAL, "collocation HMC with a ball constraint is not supported");
+    return SPEC_OK;
+}
+
+// per-CTA scratch for the degree d and per-slot buffers for C chains
+static int ensure_chmc(spec_ctx* ctx, int q, long long C) {
+    const int d = q + 1;
+    const int mp = roundup(ctx->m, 8);
+    if (d > ctx->chmc_d) {
+        if (ctx->chmc_scratch) cudaFree(ctx->chmc_scratch);
+        ctx->chmc_scratch = nullptr;
+        ctx->chmc_smem = sizeof(double) * (size_t)16 * (mp + 8);
+        CK(cudaFuncSetAttribute(chmc_chord_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)ctx->chmc_smem));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chmc_chord_kernel<512>, 512, ctx->chmc_smem));
+        if (occ < 1) return fail(SPEC_ECUDA, "collocation chord kernel cannot be resident");
+        ctx->chmc_grid = occ * ctx->num_sms;
+        ctx->chmc_stride = (long long)chmc_nmat(d) * mp * ctx->ld;
+        cudaError_t e = zalloc(&ctx->chmc_scratch, (size_t)ctx->chmc_stride * ctx->chmc_grid);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            ctx->chmc_scratch = nullptr;
+            return fail(SPEC_ENOMEM, std::string("collocation scratch: ") + cudaGetErrorString(e));
+        }
+        ctx->chmc_d = d;
+    }
+    if (!ctx->picard) CK(zalloc(&ctx->picard, 4));
+    ChmcBuf& b = ctx->chb;
+    if (C <= b.cap && d <= b.d) return SPEC_OK;
+    free_chmc_bufs(b);
+    const long long cap = std::max(C, ctx->cb.cap);
+    const int dd = std::max(d, ctx->chmc_d);
+    cudaError_t e = cudaSuccess;
+#define ZA(ptr, cnt) \
+    if (e == cudaSuccess) e = zalloc(&b.ptr, (size_t)(cnt));
+    ZA(CF, cap * dd * ctx->np) ZA(CB, cap * dd * ctx->mtp) ZA(GW, cap * (dd - 1) * ctx->np) ZA(hseg, cap)
+    ZA(elist, cap * dd)
+#undef ZA
+    if (e != cudaSuccess) {
+        free_chmc_bufs(b);
+        cudaGetLastError();
+        return fail(SPEC_ENOMEM, std::string("collocation buffers: ") + cudaGetErrorString(e));
+    }
+    b.cap = cap;
+    b.d = dd;
+    return SPEC_OK;
+}
+
+static ChmcParams chmc_params(spec_ctx* ctx, int q, double h) {
+    ChmcParams H;
+    memset(&H, 0, sizeof(H));
+    H.CF = ctx->chb.CF; H.CB = ctx->chb.CB; H.GW = ctx->chb.GW; H.hseg = ctx->chb.hseg; H.elist = ctx->chb.elist;
+    H.q = q;
+    H.d = q + 1;
+    H.h = h;
+    H.pot = ctx->pot;
+    H.mu = ctx->pot_mu;
+    H.scale = ctx->pot_scale;
+    H.cvec = ctx->c;
+    chmc_basis(q, H.nodes, H.lcoef);
+    H.picard = ctx->picard;
+    return H;
+}
+
+// One collocation-HMC boundary-oracle call (one segment) for every slot of the list:
+// K7a (polynomial), the B_k = A(c_k) contraction over d rows per chain, K7b (chord + advance).
+static int launch_chmc(spec_ctx* ctx, ChordParams P, const ChmcParams& H, int count_host) {
+    const int wblocks = std::min((count_host + 7) / 8, 65535 * 4);
+    chmc_poly_kernel<<<std::max(wblocks, 1), 256, 0, ctx->stream>>>(P, H);
+    launch_gemm_av(ctx, H.CF, H.elist, nullptr, count_host * H.d, H.CB, nullptr);
+    P.scratch = ctx->chmc_scratch;
+    P.scratch_stride = ctx->chmc_stride;
+    const int grid = std::min(count_host, ctx->chmc_grid);
+    chmc_chord_kernel<512><<<std::max(grid, 1), 512, ctx->chmc_smem, ctx->stream>>>(P, H);
+    ctx->launches += 2;
+    CK(cudaGetLastError());
+    return SPEC_OK;
+}
+
 static NormalParams normal_params(spec_ctx* ctx, int mode) {
     NormalParams Q;
     memset(&Q, 0, sizeof(Q));
@@ -791,7 +948,8 @@ static int ensure_obuf(spec_ctx* ctx, long long B) {
 
 static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const double* dv, const double* du,
                        double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
-                       bool host_out, int* status_out, int* capped_out, double hmcT = 0.0) {
+                       bool host_out, int* status_out, int* capped_out, double hmcT = 0.0,
+                       const ChmcParams* chmc = nullptr, int* outward_out = nullptr) {
     ChainBuf& b = ctx->cb;
     OracleBuf& o = *(OracleBuf*)ctx->obuf;
     const int B = (int)batch;
@@ -806,13 +964,16 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     if (du) CK(cudaMemcpyAsync(b.U, du, sizeof(double) * (size_t)B * m, cudaMemcpyDeviceToDevice, ctx->stream));
     // A(x) = a0 + X Ahat ; A(v) = V Ahat  (K0, K1)
     launch_gemm_av(ctx, b.X, nullptr, nullptr, B, b.AX, ctx->a0);
-    launch_gemm_av(ctx, b.V, nullptr, nullptr, B, b.AV, nullptr);
+    if (!chmc) launch_gemm_av(ctx, b.V, nullptr, nullptr, B, b.AV, nullptr);
     // K2 in oracle mode
     ChordParams P = chord_params(ctx, 1);
     P.count_host = B;
     P.o_tminus = o.tm; P.o_tplus = o.tp; P.o_kernel = kernel ? o.ker : nullptr; P.o_binding = o.bind;
     P.o_status = o.stat;
-    if (hmcT > 0.0) {
+    if (chmc) {
+        int rc = launch_chmc(ctx, P, *chmc, B);
+        if (rc) return rc;
+    } else if (hmcT > 0.0) {
         P.Temp = hmcT;
         int rc = launch_hmc(ctx, P, B);
         if (rc) return rc;
@@ -837,19 +998,21 @@ static int oracle_impl(spec_ctx* ctx, int64_t batch, const double* dx, const dou
     CK(cudaMemcpyAsync(st.data(), o.stat, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     int worst = 0;
-    int ncapped = 0;
+    int ncapped = 0, nout = 0;
     for (int i = 0; i < B; ++i) {
         worst = std::max(worst, st[i] == 2 ? 2 : 0);
         ncapped += st[i] == 3;
+        nout += st[i] == 4;
     }
     if (status_out) *status_out = worst;
     if (capped_out) *capped_out = ncapped;
+    if (outward_out) *outward_out = nout;
     return SPEC_OK;
 }
 
 static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u,
                         double* t_minus, double* t_plus, double* normal, double* kernel, int32_t* binding,
-                        bool host, double hmcT = 0.0) {
+                        bool host, double hmcT = 0.0, int chmc_q = 0, double chmc_h = 0.0) {
     if (!ctx) return fail(SPEC_EINVAL, "null ctx");
     if (walk_is_active(ctx)) return fail(SPEC_EINVAL, "a resumable walk is in progress (call walk_end first)");
     if (batch < 0 || batch > (1LL << 30)) return fail(SPEC_EINVAL, "bad batch");
@@ -865,6 +1028,14 @@ static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const dou
         rc = ensure_hmc(ctx);
         if (rc) return rc;
     }
+    ChmcParams H;
+    if (chmc_q > 0) {
+        rc = check_chmc(ctx, chmc_q, chmc_h);
+        if (rc) return rc;
+        rc = ensure_chmc(ctx, chmc_q, batch);
+        if (rc) return rc;
+        H = chmc_params(ctx, chmc_q, chmc_h);
+    }
     OracleBuf& o = *(OracleBuf*)ctx->obuf;
     const int n = ctx->n, m = ctx->m;
     const double *dx = x, *dv = v, *du = u;
@@ -874,11 +1045,13 @@ static int oracle_entry(spec_ctx* ctx, int64_t batch, const double* x, const dou
         if (u) CK(cudaMemcpyAsync(o.u, u, sizeof(double) * batch * m, cudaMemcpyHostToDevice, ctx->stream));
         dx = o.x; dv = o.v; du = u ? o.u : nullptr;
     }
-    int status = 0, capped = 0;
-    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status, &capped, hmcT);
+    int status = 0, capped = 0, outward = 0;
+    rc = oracle_impl(ctx, batch, dx, dv, du, t_minus, t_plus, normal, kernel, binding, host, &status, &capped, hmcT,
+                     chmc_q > 0 ? &H : nullptr, &outward);
     if (rc) return rc;
     if (status == 2) return fail(SPEC_EPRECOND, "some x is not interior (Cholesky of F(x) failed)");
     if (capped) g_err = std::to_string(capped) + " line(s): Weyl iteration cap reached (t_plus = NaN)";
+    if (outward) g_err = std::to_string(outward) + " line(s): boundary start moving outward (t_plus = 0)";
     return SPEC_OK;
 }
 
@@ -891,6 +1064,12 @@ extern "C" int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const d
     if (!(T > 0.0)) return fail(SPEC_EINVAL, "T must be > 0");
     std::vector<double> tm((size_t)(batch > 0 ? batch : 1));
     return oracle_entry(ctx, batch, x, v, u, tm.data(), t_plus, normal, kernel, binding, true, T);
+}
+extern "C" int chmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, int q,
+                           double h, double* t_plus, double* normal, double* kernel, int32_t* binding) {
+    if (q < 1) return fail(SPEC_EINVAL, "collocation nodes q must be in 1..6");
+    std::vector<double> tm((size_t)(batch > 0 ? batch : 1));
+    return oracle_entry(ctx, batch, x, v, u, tm.data(), t_plus, normal, kernel, binding, true, 0.0, q, h);
 }
 extern "C" int boundary_oracle_dev(spec_ctx* ctx, int64_t batch, const double* x, const double* v,
                                    const double* u, double* t_minus, double* t_plus, double* normal,
@@ -921,6 +1100,7 @@ struct WalkRun {
     double k2ms[3] = {0, 0, 0};    // K2 split phases: factor, Lanczos, tail
     long long kcount[4] = {0, 0, 0, 0};
     long long k2_items = 0;        // chain-calls processed by K2 launches (upper bound incl. done)
+    ChmcParams H;                  // collocation HMC-r (kind SPEC_WALK_CHMC)
 };
 static WalkRun& walk_run(spec_ctx* ctx);
 
@@ -959,6 +1139,11 @@ static int walk_setup(spec_ctx* ctx, const spec_walk_params* p, const double* dx
                                                             b.AXs, b.ell, p->L, p->seed, p->tag, p->kind,
                                                             p->chain_begin, dgid);
     ctx->launches++;
+    if (p->kind == SPEC_WALK_CHMC) {
+        int rc = ensure_chmc(ctx, p->q, C);
+        if (rc) return rc;
+        W.H = chmc_params(ctx, p->q, p->h);
+    }
     W.p = *p;
     W.count = C;
     W.cur = 0;
@@ -1027,7 +1212,9 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             cudaEvent_t* e = W.timing ? &ev[7 * k] : nullptr;
             CK(cudaMemsetAsync(b.counters + 2, 0, sizeof(int), ctx->stream));
             if (e) CK(cudaEventRecord(e[0], ctx->stream));
-            if (W.p.kind == SPEC_WALK_CHNR) {  // A(e_j) = A_j: a row copy
+            if (W.p.kind == SPEC_WALK_CHMC) {
+                // no K1: the direction is part of the segment polynomial (K7a + its contraction)
+            } else if (W.p.kind == SPEC_WALK_CHNR) {  // A(e_j) = A_j: a row copy
                 coord_dir_kernel<<<std::min(count, ctx->num_sms * 8), 256, 0, ctx->stream>>>(
                     list, b.counters, count, b.V, ctx->np, ctx->n, ctx->Ahat, ctx->mtp, b.AV);
                 ctx->launches++;
@@ -1041,9 +1228,13 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
             if (W.p.kind == SPEC_WALK_HMC) {  // K5
                 int rc = launch_hmc(ctx, P, count);
                 if (rc) return rc;
+            } else if (W.p.kind == SPEC_WALK_CHMC) {  // K7
+                int rc = launch_chmc(ctx, P, W.H, count);
+                if (rc) return rc;
             } else launch_chord(ctx, P, count, (e && (ctx->k2_split || ctx->g_split)) ? &e[5] : nullptr);  // K2
             if (e) CK(cudaEventRecord(e[2], ctx->stream));
-            if (W.p.kind == SPEC_WALK_BILLIARD || W.p.kind == SPEC_WALK_HMC) {  // Hit-and-Run never reflects
+            if (W.p.kind == SPEC_WALK_BILLIARD || W.p.kind == SPEC_WALK_HMC || W.p.kind == SPEC_WALK_CHMC) {
+                // (Hit-and-Run never reflects)
                 launch_gemm_normal(ctx, b.nlist, b.counters + 2, count);  // K3
                 if (e) CK(cudaEventRecord(e[3], ctx->stream));
                 Q.nlist = b.nlist;
@@ -1175,8 +1366,12 @@ static int gather_f64(spec_ctx* ctx, int rc_local, const std::vector<double>& lo
 static int check_walk_params(spec_ctx* ctx, const spec_walk_params* p) {
     if (!ctx || !p) return fail(SPEC_EINVAL, "null argument");
     if (p->kind != SPEC_WALK_BILLIARD && p->kind != SPEC_WALK_HMC && p->kind != SPEC_WALK_HNR &&
-        p->kind != SPEC_WALK_CHNR)
+        p->kind != SPEC_WALK_CHNR && p->kind != SPEC_WALK_CHMC)
         return fail(SPEC_EINVAL, "unknown walk kind");
+    if (p->kind == SPEC_WALK_CHMC) {
+        int rc = check_chmc(ctx, p->q, p->h);
+        if (rc) return rc;
+    }
     if ((p->kind == SPEC_WALK_HNR || p->kind == SPEC_WALK_CHNR) && p->T > 0.0 && std::isfinite(p->T) && !ctx->has_obj)
         return fail(SPEC_EINVAL, "Hit-and-Run for exp(-c^T x / T) needs spec_set_objective (T = inf: uniform)");
     if (p->kind == SPEC_WALK_HMC) {

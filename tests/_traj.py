@@ -56,12 +56,14 @@ def traj_errors(g, o, H):
 
 
 
-def traj_parity(g, lmi, kind, seed, chains, steps, L, rho, R, n, pool, T=1.0, c=None):
-    a_max = A_MAX_HMC if kind == oracle.HMC else A_MAX
-    """Compare GPU traces g (walk_trace output for `chains`) with the oracle; returns (report, failures)."""
+def traj_parity(g, lmi, kind, seed, chains, steps, L, rho, R, n, pool, T=1.0, c=None, colloc=None):
+    """Compare GPU traces g (walk_trace output for `chains`) with the oracle; returns (report, failures).
+    colloc: the collocation HMC-r parameters (kind CHMC), whose chord budget is HMC-r's."""
+    a_max = A_MAX_HMC if kind in (oracle.HMC, oracle.CHMC) else A_MAX
     pert = specgen.unit_vectors(len(chains), n, 99) * DELTA
-    fo = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, None, T, c, 0, True) for ch in chains]
-    fp = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, pert[i], T, c, 0, True)
+    kw = dict(T=T, c=c, tag=0, stop=True, colloc=colloc)
+    fo = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, None, **kw) for ch in chains]
+    fp = [pool.submit(oracle.trace, lmi, kind, seed, ch, steps, L, rho, R, pert[i], **kw)
           for i, ch in enumerate(chains)]
     horizons, avail, worst, fails = [], [], [], []
     for i, ch in enumerate(chains):
