@@ -44,6 +44,7 @@ INSTANCE_SEED = 3  # BASELINE.json configs[3] instance (SURVEY 8(d).1 "M100")
 L_TAU = 2.0 * math.sqrt(N_DIM)
 RHO = 10 * N_DIM
 HMC_L = 1.09  # configs[3] HMC trajectory length: the diameter estimate
+CHMC_L, CHMC_Q, CHMC_H = 2.0, 3, 0.25  # collocation HMC-r side line (R33)
 LANCZOS_K = 55  # SURVEY V9 prior; the bench uses the device-measured mean J of its timed rounds
 
 WORKLOAD = (f"M100: billiard walk (Alg. 5) on the BASELINE.json configs[3] instance (rand-cube n=m={N_DIM}, "
@@ -481,6 +482,68 @@ def run_ours(args):
                                 "flop_model": "SURVEY 8(d).2: m^3/3 + m^3 + 2 J m^2, J measured on the device"},
                 "kernel_share": {k: v / max(sum(kt4["ms"].values()), 1e-9) for k, v in kt4["ms"].items()}}
 
+    # ---- collocation HMC-r (sec:hmcr P:1116-1158) on the configs[2] instance (n = m = 40),
+    # truncated Gaussian exp(-|x|^2 / 2), q = 3 Chebyshev nodes (degree-4 segments), h = 0.25, 65536 chains
+    chmc = None
+    if args.chmc_rounds > 0:
+        inst2c = specgen.config_instance(2)
+        Sc = sw.Spectrahedron.from_instance(inst2c, device=dev)
+        streamc = torch.cuda.ExternalStream(Sc.stream(), device=dev)
+        Sc.set_potential(sw.POT_GAUSS, np.zeros(inst2c.n), 1.0)
+        Sc.walk_begin(local_chains, 1000, CHMC_L, 100 * inst2c.n, SEED, chain_begin=begin, kind=sw.CHMC,
+                      q=CHMC_Q, h=CHMC_H)
+        Sc.walk_rounds(3)
+        c0s = Sc.walk_stats_now()
+        Sc.lanczos_iterations(reset=True)
+        Sc.chmc_counters(reset=True)
+        cl0 = Sc.kernel_launches()
+        barrier()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(streamc)
+        Sc.walk_rounds(args.chmc_rounds)
+        q1.record(streamc)
+        q1.synchronize()
+        barrier()
+        cms = q0.elapsed_time(q1)
+        c1s = Sc.walk_stats_now()
+        clz = Sc.lanczos_iterations(reset=True)
+        ccn = Sc.chmc_counters(reset=True)
+        claunch = int(Sc.kernel_launches() - cl0)
+        Sc.walk_end()
+        del Sc
+        ct = torch.tensor([cms, float(c1s["calls"] - c0s["calls"])], dtype=torch.float64, device=coll_dev)
+        if dist is not None:
+            cmax_ = ct.clone()
+            dist.all_reduce(cmax_[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(ct[1:], op=dist.ReduceOp.SUM)
+            cms, ccalls = float(cmax_[0]), float(ct[1])
+        else:
+            ccalls = float(ct[1])
+        lcalls = float(c1s["calls"] - c0s["calls"])
+        nn, mm_ = inst2c.n, inst2c.m
+        dq = CHMC_Q + 1
+        iwc = clz["solves"] / max(lcalls, 1.0)
+        cong = ccn["congruences"] / max(lcalls, 1.0)
+        cflops = (2 * dq * nn * mm_ * (mm_ + 1) / 2 + iwc * (mm_ ** 3 / 3 + 2 * clz["mean_j"] * mm_ * mm_)
+                  + cong * 2 * mm_ ** 3)
+        c_ach = cflops * ccalls / (cms * 1e-3) / 1e12
+        chmc = {"metric": "collocation HMC-r boundary-oracle calls/s (configs[2] instance n=m=40, "
+                          "exp(-|x|^2/2), q=3, h=0.25)",
+                "value": ccalls / (cms * 1e-3), "unit": "calls/s", "chains": chains, "rounds": args.chmc_rounds,
+                "ms": cms, "calls": ccalls, "L": CHMC_L, "gpu_launches": claunch,
+                "roofline": {"bound": "alu", "achieved": c_ach, "peak": peak, "unit": "TFLOP/s",
+                             "frac": c_ach / peak,
+                             "kernel": "whole collocation round (K7a + the d-row DMMA contraction + K7b + K3 + K4)",
+                             "flops_per_call": cflops, "weyl_iterations_per_call": iwc,
+                             "congruences_per_call": cong, "lanczos_j": clz["mean_j"],
+                             "picard_per_segment": ccn["picard"] / max(ccn["segments"], 1),
+                             "picard_unconverged": ccn["unconverged"],
+                             "flop_model": "2 d n m(m+1)/2 (contraction) + I_w (m^3/3 + 2 J m^2) + C 2 m^3 "
+                                           "(C = congruences K^-1 D_j K^-T), I_w, J, C device-counted"},
+                "note": "one segment (degree-4 collocation polynomial, its first boundary root in (0, h']) per "
+                        "chain per round; device events on the library stream, max over ranks"}
+
     # ---- BASELINE metric, second half: volume time at n = m = 40 (configs[2], eps 0.1, 4096 chains/phase)
     vol = None
     if args.volume_seeds > 0:
@@ -559,6 +622,7 @@ def run_ours(args):
         "volume_n40": vol,
         "hmc_configs3": hmc,
         "m200_configs4": m200,
+        "chmc_configs2": chmc,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -580,6 +644,7 @@ def main():
     ap.add_argument("--volume-seeds", type=int, default=10)
     ap.add_argument("--hmc-rounds", type=int, default=4)
     ap.add_argument("--m200-rounds", type=int, default=3)
+    ap.add_argument("--chmc-rounds", type=int, default=3)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

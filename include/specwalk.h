@@ -140,6 +140,10 @@ int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, c
  * not interior.  EINVAL: no potential, q not in 1..6, h <= 0. */
 int chmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, int q, double h,
                 double* t_plus, double* normal, double* kernel, int32_t* binding);
+/* Collocation HMC-r device counters since the last reset (out4, host): Picard iterations,
+ * segments, segments whose Picard iteration hit its cap (64) without converging, and the
+ * congruences K^-1 D_j K^-T of all Weyl iterations (the measured flop model of bench.py). */
+int spec_chmc_counters(spec_ctx* ctx, int reset, int64_t* out4);
 
 /* ---- walks ---- */
 /* BILLIARD: Alg. 5; HMC: reflective HMC for exp(-c^T x / T), Alg. 6

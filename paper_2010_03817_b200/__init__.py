@@ -38,6 +38,7 @@ EXPORTS = (
     "spec_kernel_launches", "walk_begin", "walk_rounds", "walk_end", "spec_walk_stats_now", "spec_kernel_timing",
     "spec_kernel_times", "hmc_oracle", "spec_set_comm", "volume", "expectation", "spec_k2_phase_times",
     "spec_lanczos_iterations", "sdp_anneal", "spec_k2_config", "spec_set_potential", "chmc_oracle",
+    "spec_chmc_counters",
 )
 F_LINEAR_C, F_SQNORM, F_HALFSPACE_UNION = 0, 1, 2
 MAX_PHASES = 64
@@ -150,6 +151,7 @@ def load(build_if_missing: bool = True):
     l.hmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_double, _dp, _dp, _dp, _ip]
     l.chmc_oracle.argtypes = [C.c_void_p, C.c_int64, _dp, _dp, _dp, C.c_int, C.c_double, _dp, _dp, _dp, _ip]
     l.spec_set_potential.argtypes = [C.c_void_p, C.c_int, _dp, C.c_double]
+    l.spec_chmc_counters.argtypes = [C.c_void_p, C.c_int, _lp]
     l.spec_set_comm.argtypes = [C.c_void_p, C.POINTER(Comm)]
     l.volume.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_int64, C.POINTER(VolumeOpts),
                          C.POINTER(VolumeReport)]
@@ -411,6 +413,12 @@ class Spectrahedron:
         return dict(ms={k: ms[i] for i, k in enumerate(names)}, launches={k: cnt[i] for i, k in enumerate(names)},
                     k2_items=items.value,
                     k2_phases_ms=dict(K2a_factor=k2[0], K2b_lanczos=k2[1], K2c_tail=k2[2]))
+
+    def chmc_counters(self, reset: bool = True) -> dict:
+        """Collocation HMC-r device counters since the last reset."""
+        out = np.zeros(4, dtype=np.int64)
+        _check(_lib.spec_chmc_counters(self._h, 1 if reset else 0, out.ctypes.data_as(_lp)))
+        return dict(picard=int(out[0]), segments=int(out[1]), unconverged=int(out[2]), congruences=int(out[3]))
 
     def lanczos_iterations(self, reset: bool = True) -> dict:
         """Device-counted Lanczos iterations per extreme-eigenvalue solve since the last reset."""

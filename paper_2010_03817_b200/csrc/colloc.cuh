@@ -49,7 +49,8 @@ struct ChmcParams {
     const double* cvec;
     double nodes[CH_MAXQ];
     double lcoef[CH_MAXQ * CH_MAXQ];  // lcoef[j*q + k]: s^k coefficient of the Lagrange polynomial l_j
-    unsigned long long* picard;       // optional [0] sum of Picard iterations, [1] segments, [2] unconverged
+    unsigned long long* picard;       // optional [0] sum of Picard iterations, [1] segments, [2] unconverged,
+                                      // [3] congruences N_j = K^-1 D_j K^-T of the Weyl iterations
 };
 
 __device__ __forceinline__ double pot_grad(const ChmcParams& H, int i, double x) {
@@ -389,7 +390,10 @@ __global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcPa
                         cj[j] = sqrt(fro);
                     }
                 }
-                if (T.tid == 0) sh_d[6] = weyl_step_n(a_min, cj, D);
+                if (T.tid == 0) {
+                    sh_d[6] = weyl_step_n(a_min, cj, D);
+                    if (H.picard) atomicAdd(&H.picard[3], (unsigned long long)D);  // congruences (flop model)
+                }
                 __syncthreads();
                 const double h = sh_d[6];
                 for (int i = T.tid; i < m; i += T.nthr) yy[i] = yk[i];

@@ -138,6 +138,8 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    int f2 = 0, f2_grid = 0;   // K2a as factor2_kernel (two chains per SM, one matrix in shared memory)
+    size_t f2_smem = 0;
     int g_split = 0, cl_grid = 0;  // m > 112: factor (global scratch) | lanczos_cl_kernel (2-CTA cluster) | tail
     size_t cl_smem = 0;
     size_t l2_smem = 0;
@@ -445,6 +447,18 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->f_grid = of * ctx->num_sms;
         ctx->l_grid = ol * ctx->num_sms;
         ctx->t_grid = ot * ctx->num_sms;
+        // K2a with two chains per SM (factor2_kernel) where one matrix fits half an SM's shared
+        // memory; opt-in (SPECWALK_FACTOR2=1) until measured
+        if (ctx->k2_variant == 1 && getenv("SPECWALK_FACTOR2")) {
+            ctx->f2_smem = sizeof(double) * f2_smem_doubles(mp, ctx->ld);
+            int o2 = 0;
+            CK(cudaFuncSetAttribute(factor2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->f2_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, factor2_kernel, F2_NT, ctx->f2_smem));
+            if (o2 >= 2) {
+                ctx->f2 = 1;
+                ctx->f2_grid = o2 * ctx->num_sms;
+            }
+        }
         // billiard / oracle K2b with two chains per SM (lanczos2.cuh) where M fits half an SM's
         // shared memory; SPECWALK_LZ_OLD=1 keeps the register-resident lanczos_kernel (A/B)
         if (ctx->k2_variant == 1 && !getenv("SPECWALK_LZ_OLD")) {
@@ -598,7 +612,10 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<256, 8><<<g(ctx->l_grid), 256, ctx->l_smem, ctx->stream>>>(P);
         } else if (ctx->k2_variant == 1) {
-            factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            if (ctx->f2)
+                factor2_kernel<<<g(ctx->f2_grid), F2_NT, ctx->f2_smem, ctx->stream>>>(P);
+            else
+                factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             if (ctx->lz2)
                 lanczos2_kernel<<<g(ctx->l2_grid), LZ2_NT, ctx->l2_smem, ctx->stream>>>(P);
@@ -1065,6 +1082,22 @@ extern "C" int hmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const d
     std::vector<double> tm((size_t)(batch > 0 ? batch : 1));
     return oracle_entry(ctx, batch, x, v, u, tm.data(), t_plus, normal, kernel, binding, true, T);
 }
+// Collocation HMC-r device counters since the last reset: Picard iterations, segments, segments
+// whose Picard iteration did not converge, congruences of the Weyl iterations.
+extern "C" int spec_chmc_counters(spec_ctx* ctx, int reset, int64_t* out4) {
+    if (!ctx || !out4) return fail(SPEC_EINVAL, "null argument");
+    CK(cudaSetDevice(ctx->dev));
+    if (!ctx->picard) {
+        for (int i = 0; i < 4; ++i) out4[i] = 0;
+        return SPEC_OK;
+    }
+    unsigned long long h[4];
+    CK(cudaMemcpyAsync(h, ctx->picard, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < 4; ++i) out4[i] = (int64_t)h[i];
+    if (reset) CK(cudaMemsetAsync(ctx->picard, 0, sizeof(h), ctx->stream));
+    return SPEC_OK;
+}
 extern "C" int chmc_oracle(spec_ctx* ctx, int64_t batch, const double* x, const double* v, const double* u, int q,
                            double h, double* t_plus, double* normal, double* kernel, int32_t* binding) {
     if (q < 1) return fail(SPEC_EINVAL, "collocation nodes q must be in 1..6");
@@ -1269,7 +1302,7 @@ static int walk_do_rounds(spec_ctx* ctx, long long max_rounds) {
                     W.kms[i] += t;
                     W.kcount[i] += 1;
                 }
-                if ((ctx->k2_split || ctx->g_split) && W.p.kind != SPEC_WALK_HMC) {
+                if ((ctx->k2_split || ctx->g_split) && W.p.kind != SPEC_WALK_HMC && W.p.kind != SPEC_WALK_CHMC) {
                     float t0 = 0.f, t1 = 0.f, t2 = 0.f;
                     CK(cudaEventElapsedTime(&t0, ev[7 * k + 1], ev[7 * k + 5]));
                     CK(cudaEventElapsedTime(&t1, ev[7 * k + 5], ev[7 * k + 6]));
@@ -1622,8 +1655,9 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
                  "lanczos_cl_kernel (2-CTA clusters, %d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->chord_grid_max, ctx->cl_grid, ctx->t_grid);
     else if (ctx->k2_split)
-        snprintf(buf, sizeof(buf), "split: factor_kernel<512> (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
-                 ctx->f_grid, ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
+        snprintf(buf, sizeof(buf), "split: %s (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->f2 ? "factor2_kernel<256 thr, 2/SM>" : "factor_kernel<512>", ctx->f2 ? ctx->f2_grid : ctx->f_grid,
+                 ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
                  ctx->lz2 ? ctx->l2_grid : ctx->l_grid, ctx->t_grid);
     else
         snprintf(buf, sizeof(buf), "fused: chord_kernel2<%d, %s> (%d CTAs)", ctx->chord_threads,
