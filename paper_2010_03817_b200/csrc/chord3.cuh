@@ -208,180 +208,6 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
     }
 }
 
-// ---------------------------------------------------------------- K2a, two chains per SM
-// factor2_kernel: the mathematics of factor_kernel with ONE full matrix in shared memory
-// (~104 KB at m = 100, 256 threads: two CTAs per SM), so that one chain's dependent
-// latency chain (Cholesky diagonal factors, TRSM block steps, barriers) overlaps the other's:
-//   phase 1: A(x) -> shared, its deflation (boundary start), Cholesky with inverse diagonal
-//            blocks; L to the tail's packed buffer and, in full rows, to the slot's M buffer
-//   phase 2: A(v) -> the same shared matrix, its deflation (Schur complement), the two
-//            left-looking DMMA TRSMs with L read from the slot buffer (L2-resident, written
-//            just before) and the inverse diagonal blocks from shared memory; M overwrites L.
-// Same arithmetic as factor_kernel (the Householder rank-2 vectors of G and B are formed in
-// separate passes; the formulas are unchanged).
-
-// p = beta X h - (beta/2)(h.beta X h) h: the rank-2 vector of H X H = X - h p^T - p h^T (not applied)
-__device__ void householder_vec(const Team& T, const double* X, int m, int ld, const double* h, double beta,
-                                double* p, double* red) {
-    for (int i = T.warp; i < m; i += T.nwarps) {
-        double s = 0.0;
-        for (int j = T.lane; j < m; j += 32) s += X[i * ld + j] * h[j];
-        s = warp_sum(s);
-        if (T.lane == 0) p[i] = beta * s;
-    }
-    __syncthreads();
-    double hp = 0.0;
-    for (int i = T.tid; i < m; i += T.nthr) hp += h[i] * p[i];
-    const double K = 0.5 * beta * block_sum(T, hp, red);
-    for (int i = T.tid; i < m; i += T.nthr) p[i] -= K * h[i];
-    __syncthreads();
-}
-
-constexpr int F2_NT = 256;
-// shared-memory layout of factor2_kernel (doubles): the matrix (mp + 1 rows of ld), six vectors,
-// 64 slack, the inverse diagonal blocks (8 mp)
-__host__ __device__ inline size_t f2_smem_doubles(int mp, int ld) {
-    return (size_t)(mp + 1) * ld + 6 * (size_t)(mp + 8) + 64 + 8 * (size_t)mp;
-}
-
-__global__ void __launch_bounds__(F2_NT, 2) factor2_kernel(ChordParams P) {
-    extern __shared__ __align__(16) double smem_dyn[];
-    Team T;
-    T.tid = threadIdx.x;
-    T.nthr = F2_NT;
-    T.lane = T.tid & 31;
-    T.warp = T.tid >> 5;
-    T.nwarps = F2_NT >> 5;
-    __shared__ double red[64];
-    __shared__ int sh_i[8];
-    const int m = P.m, ld = P.ld;
-    const int mp = (m + 7) & ~7;
-    const int vl = mp + 8;
-    double* X = smem_dyn;  // A(x) -> L, then A(v) -> M
-    double* vec = X + (size_t)(mp + 1) * ld;
-    double* uu = vec + 0 * vl;
-    double* hh = vec + 1 * vl;
-    double* pw = vec + 2 * vl;
-    double* rdiag = vec + 3 * vl;
-    double* yy = vec + 4 * vl;
-    double* bv = vec + 5 * vl;
-    double* Lv = vec + 6 * vl + 64;
-
-    const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
-    for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
-        const int slot = P.list ? P.list[rr] : rr;
-        if (slot < 0) continue;
-        if (P.mode == 0 && (P.flags[slot] & CF_DONE)) continue;
-        const double* av = P.AV + (size_t)slot * P.mtp;
-        const double* ax = P.AX + (size_t)slot * P.mtp;
-        double* S = P.wS + (size_t)slot * P.w_sstride;
-        double* Mw = P.wM + (size_t)slot * P.w_mstride;
-        double* Lw = P.wL + (size_t)slot * P.w_mstride;
-        const int bnd = P.bound[slot];
-        const bool defl = (bnd == 0);
-        __syncthreads();
-        long long t_prof = clock64();
-        // ---- phase 1: G = A(x)
-        unpack_sym_async(T, ax, X, m, ld);
-        if (defl)
-            for (int i = T.tid; i < m; i += T.nthr) uu[i] = P.U[(size_t)slot * m + i];
-        asm volatile("cp.async.wait_all;\n" ::);
-        __syncthreads();
-        PROF_MARK(0);
-        int md = m;
-        double beta_h = 0.0;
-        double* Xd = X;
-        if (defl) {
-            double nu = 0.0;
-            for (int i = T.tid; i < m; i += T.nthr) nu += uu[i] * uu[i];
-            nu = sqrt(block_sum(T, nu, red));
-            for (int i = T.tid; i < m; i += T.nthr) hh[i] = uu[i] / nu;
-            __syncthreads();
-            if (T.tid == 0) hh[0] += (hh[0] >= 0.0 ? 1.0 : -1.0);
-            __syncthreads();
-            double h2 = 0.0;
-            for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
-            beta_h = 2.0 / block_sum(T, h2, red);
-            householder_vec(T, X, m, ld, hh, beta_h, pw, red);
-            md = m - 1;
-            for (int i = 1 + T.warp; i < m; i += T.nwarps) {
-                const double hi = hh[i], pxi = pw[i];
-                for (int jx = 1 + T.lane; jx < m; jx += 32) X[i * ld + jx] -= hi * pw[jx] + pxi * hh[jx];
-            }
-            Xd = X + ld + 1;
-        }
-        const int mdp = (md + 7) & ~7;
-        for (int i = md + T.warp; i < mdp; i += T.nwarps)
-            for (int j = T.lane; j < mdp; j += 32) {
-                Xd[i * ld + j] = (i == j) ? 1.0 : 0.0;
-                Xd[j * ld + i] = (i == j) ? 1.0 : 0.0;
-            }
-        __syncthreads();
-        PROF_MARK(1);
-        int status = defl ? ST_DEFL : 0;
-        const bool okc = (md >= 1) ? cholesky_inv_blocked_la(T, Xd, mdp, ld, rdiag, Lv, &sh_i[2]) : true;
-        PROF_MARK(2);
-        if (!okc) status |= ST_FAILED;
-        if (okc && md >= 1) {
-            // L: packed lower rows for the tail kernel, full rows (strictly lower blocks suffice) for
-            // phase 2's TRSMs in the slot's M buffer
-            for (int i = T.warp; i < mdp; i += T.nwarps)
-                for (int jx = T.lane; jx <= i; jx += 32) {
-                    const double l = Xd[i * ld + jx];
-                    Lw[pk(i, jx)] = l;
-                    Mw[i * ld + jx] = l;
-                }
-        }
-        __syncthreads();
-        // ---- phase 2: B = A(v)
-        double a_schur = 0.0;
-        bool outward = false;
-        unpack_sym_async(T, av, X, m, ld);
-        asm volatile("cp.async.wait_all;\n" ::);
-        __syncthreads();
-        if (defl) {
-            householder_vec(T, X, m, ld, hh, beta_h, yy, red);
-            a_schur = X[0] - (hh[0] * yy[0] + yy[0] * hh[0]);
-            outward = !(a_schur > 0.0);
-            for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = X[(i + 1) * ld] - (hh[i + 1] * yy[0] + yy[i + 1] * hh[0]);
-            __syncthreads();
-            for (int i = 1 + T.warp; i < m; i += T.nwarps) {
-                const double hi = hh[i], pyi = yy[i], bi = bv[i - 1];
-                for (int jx = 1 + T.lane; jx < m; jx += 32) {
-                    const double bij = X[i * ld + jx] - (hi * yy[jx] + pyi * hh[jx]);
-                    X[i * ld + jx] = outward ? 0.0 : bij - bi * bv[jx - 1] / a_schur;
-                }
-            }
-        }
-        if (outward) status = (status & ~ST_FAILED) | ST_OUTWARD;  // as factor_kernel: no Cholesky verdict
-        for (int i = md + T.warp; i < mdp; i += T.nwarps)
-            for (int j = T.lane; j < mdp; j += 32) {
-                Xd[i * ld + j] = 0.0;
-                Xd[j * ld + i] = 0.0;
-            }
-        __syncthreads();
-        PROF_MARK(3);
-        if (!outward && okc && md >= 1) {
-            congruence_inv(T, Mw, Lv, Xd, mdp, ld);  // L from the slot buffer (global, L2)
-            // M = -(B + B^T)/2 over L's copy
-            for (int i = T.warp; i < mdp; i += T.nwarps)
-                for (int jx = T.lane; jx < mdp; jx += 32) Mw[i * ld + jx] = -0.5 * (Xd[i * ld + jx] + Xd[jx * ld + i]);
-        }
-        if (T.tid == 0) {
-            S[S_A] = a_schur;
-            S[S_BH] = beta_h;
-            S[S_MD] = (double)md;
-            S[S_ST] = (double)status;
-        }
-        for (int i = T.tid; i < mp; i += T.nthr) {
-            S[S_VEC + i] = hh[i];
-            S[S_VEC + vl + i] = bv[i];
-            S[S_VEC + 2 * vl + i] = rdiag[i];
-        }
-        PROF_MARK(4);
-    }
-}
-
 // ---------------------------------------------------------------- K2b
 template <int NT, int KC>
 __global__ void __launch_bounds__(NT, 1) lanczos_kernel(ChordParams P) {

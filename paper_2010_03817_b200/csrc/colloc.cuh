@@ -30,10 +30,30 @@ constexpr int CH_MAXQ = 6;               // collocation nodes (trajectory degree
 constexpr int CH_MAXD = CH_MAXQ + 1;
 constexpr int CH_MAXIT = 64;              // Picard iterations (R33)
 constexpr int CH_SCALAR_MAXIT = 400;      // Weyl iterations of one cube-face polynomial
-// scratch matrices per CTA: B_0..B_d, the 2d+1 deflated coefficients, K, N, the Lanczos basis
-__host__ __device__ constexpr int chmc_nmat(int d) { return (d + 1) + (2 * d + 1) + 3; }
+// scratch matrices per CTA: B_0..B_d, the 2d+1 deflated coefficients, K, N, the Lanczos basis, the
+// (up to 2d) congruenced coefficients
+__host__ __device__ constexpr int chmc_nmat(int d) { return (d + 1) + (2 * d + 1) + 3 + 2 * d; }
 
 enum : int { POT_LINEAR = 0, POT_GAUSS = 1, POT_LOGCOSH = 2 };
+
+// binomial coefficients binom(k, j), k, j < 16 (Taylor coefficients of the shifted pencil)
+__device__ const double c_binom[16][16] = {
+    {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 2.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 3.0, 3.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 4.0, 6.0, 4.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 5.0, 10.0, 10.0, 5.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 6.0, 15.0, 20.0, 15.0, 6.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 7.0, 21.0, 35.0, 35.0, 21.0, 7.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 8.0, 28.0, 56.0, 70.0, 56.0, 28.0, 8.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 9.0, 36.0, 84.0, 126.0, 126.0, 84.0, 36.0, 9.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 10.0, 45.0, 120.0, 210.0, 252.0, 210.0, 120.0, 45.0, 10.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 11.0, 55.0, 165.0, 330.0, 462.0, 462.0, 330.0, 165.0, 55.0, 11.0, 1.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 12.0, 66.0, 220.0, 495.0, 792.0, 924.0, 792.0, 495.0, 220.0, 66.0, 12.0, 1.0, 0.0, 0.0, 0.0},
+    {1.0, 13.0, 78.0, 286.0, 715.0, 1287.0, 1716.0, 1716.0, 1287.0, 715.0, 286.0, 78.0, 13.0, 1.0, 0.0, 0.0},
+    {1.0, 14.0, 91.0, 364.0, 1001.0, 2002.0, 3003.0, 3432.0, 3003.0, 2002.0, 1001.0, 364.0, 91.0, 14.0, 1.0, 0.0},
+    {1.0, 15.0, 105.0, 455.0, 1365.0, 3003.0, 5005.0, 6435.0, 6435.0, 5005.0, 3003.0, 1365.0, 455.0, 105.0, 15.0, 1.0}};
 
 struct ChmcParams {
     double* CF;        // per slot d rows of np: c_1 .. c_d
@@ -183,11 +203,7 @@ __device__ double scalar_first_root(const double* g0, int D, double tmax, bool o
         double e[2 * CH_MAXD + 2];
         for (int j = 0; j <= De; ++j) {
             double acc = 0.0;
-            for (int k = De; k >= j; --k) {
-                double bin = 1.0;
-                for (int qq = 0; qq < j; ++qq) bin = bin * (double)(k - qq) / (double)(qq + 1);
-                acc = acc * s + bin * g[k];
-            }
+            for (int k = De; k >= j; --k) acc = acc * s + c_binom[k][j] * g[k];
             e[j] = acc;
         }
         if (!(e[0] > 0.0)) return s;  // rounding past the root: the last safe point
@@ -224,6 +240,7 @@ __global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcPa
     double* Kf = Ct + (size_t)(2 * d + 1) * MS;
     double* Nw = Kf + MS;
     double* Qb = Nw + MS;
+    double* NK = Qb + MS;  // D congruenced coefficients N~_k
     const int vl = mp + 8;
     double* vec = smem_dyn;
     double* hh = vec + 0 * vl;
@@ -240,6 +257,7 @@ __global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcPa
     double* yy = vec + 12 * vl;
     double* yk = vec + 13 * vl;
     double* wv = vec + 14 * vl;  // 2 slots (ping-pong)
+    double* pq = vec + 16 * vl;  // p = K^-1 e_0 and q_k = K^-1 b_k (d + 1 vectors)
 
     const int count = P.count_dev ? min(*P.count_dev, P.count_host) : P.count_host;
     for (int rr = blockIdx.x; rr < count; rr += gridDim.x) {
@@ -338,20 +356,54 @@ __global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcPa
                 double cj[2 * CH_MAXD + 2];
                 for (int j = 0; j <= D; ++j) cj[j] = 0.0;
                 double a_min = 0.0;
+                // each coefficient congruenced once: N~_k = K^-1 Cs_k K^-T (dense), or -- the border
+                // coefficients of a deflated start (odd k: e_0 b^T + b e_0^T) -- p q_k^T + q_k p^T with
+                // p = K^-1 e_0, q_k = K^-1 b_k (vector solves); then N_j = sum_k binom(k, j) s^(k-j) N~_k
+                int ncong = 0;
+                for (int k = 1; k <= D; ++k) {
+                    if (defl && (k & 1)) continue;
+                    double* Nk = NK + (size_t)(k - 1) * MS;
+                    for (int i = T.warp; i < mp; i += T.nwarps)
+                        for (int jx = T.lane; jx < mp; jx += 32) Nk[i * ld + jx] = Cs[k * MS + i * ld + jx];
+                    __syncthreads();
+                    trsm_blocked<false>(T, Kf, Nk, mp, ld, rdiag);
+                    trsm_blocked<true>(T, Kf, Nk, mp, ld, rdiag);
+                    ++ncong;
+                }
+                if (defl) {
+                    // warp w: vector w (0: e_0, k = 2w - 1: column 0 of Cs_k), forward substitution
+                    for (int w = T.warp; w <= d; w += T.nwarps) {
+                        double* xv = pq + (size_t)w * vl;
+                        for (int i = T.lane; i < mp; i += 32)
+                            xv[i] = (w == 0) ? (i == 0 ? 1.0 : 0.0) : (i == 0 ? 0.0 : Cs[(2 * w - 1) * MS + i * ld]);
+                        __syncwarp();
+                        for (int i = 0; i < mp; ++i) {
+                            double acc = 0.0;
+                            for (int k = T.lane; k < i; k += 32) acc += Kf[i * ld + k] * xv[k];
+                            acc = warp_sum(acc);
+                            if (T.lane == 0) xv[i] = (xv[i] - acc) * rdiag[i];
+                            __syncwarp();
+                        }
+                    }
+                    __syncthreads();
+                }
                 for (int j = 1; j <= D; ++j) {
                     for (int i = T.warp; i < mp; i += T.nwarps)
                         for (int jx = T.lane; jx < mp; jx += 32) {
                             double acc = 0.0;
                             for (int k = D; k >= j; --k) {
-                                double bin = 1.0;
-                                for (int qq = 0; qq < j; ++qq) bin = bin * (double)(k - qq) / (double)(qq + 1);
-                                acc = acc * s + bin * Cs[k * MS + i * ld + jx];
+                                double nk;
+                                if (defl && (k & 1)) {
+                                    const double* qk = pq + (size_t)((k + 1) >> 1) * vl;
+                                    nk = pq[i] * qk[jx] + qk[i] * pq[jx];
+                                } else {
+                                    nk = NK[(size_t)(k - 1) * MS + i * ld + jx];
+                                }
+                                acc = acc * s + c_binom[k][j] * nk;
                             }
                             Nw[i * ld + jx] = acc;
                         }
                     __syncthreads();
-                    trsm_blocked<false>(T, Kf, Nw, mp, ld, rdiag);
-                    trsm_blocked<true>(T, Kf, Nw, mp, ld, rdiag);
                     double fro = 0.0;
                     for (int i = T.warp; i < mp; i += T.nwarps)
                         for (int jx = T.lane; jx <= i; jx += 32) {
@@ -392,7 +444,7 @@ __global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcPa
                 }
                 if (T.tid == 0) {
                     sh_d[6] = weyl_step_n(a_min, cj, D);
-                    if (H.picard) atomicAdd(&H.picard[3], (unsigned long long)D);  // congruences (flop model)
+                    if (H.picard) atomicAdd(&H.picard[3], (unsigned long long)ncong);  // dense congruences (flop model)
                 }
                 __syncthreads();
                 const double h = sh_d[6];

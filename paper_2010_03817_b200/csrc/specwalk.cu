@@ -138,8 +138,6 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
-    int f2 = 0, f2_grid = 0;   // K2a as factor2_kernel (two chains per SM, one matrix in shared memory)
-    size_t f2_smem = 0;
     int g_split = 0, cl_grid = 0;  // m > 112: factor (global scratch) | lanczos_cl_kernel (2-CTA cluster) | tail
     size_t cl_smem = 0;
     size_t l2_smem = 0;
@@ -447,18 +445,6 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->f_grid = of * ctx->num_sms;
         ctx->l_grid = ol * ctx->num_sms;
         ctx->t_grid = ot * ctx->num_sms;
-        // K2a with two chains per SM (factor2_kernel) where one matrix fits half an SM's shared
-        // memory; opt-in (SPECWALK_FACTOR2=1) until measured
-        if (ctx->k2_variant == 1 && getenv("SPECWALK_FACTOR2")) {
-            ctx->f2_smem = sizeof(double) * f2_smem_doubles(mp, ctx->ld);
-            int o2 = 0;
-            CK(cudaFuncSetAttribute(factor2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->f2_smem));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, factor2_kernel, F2_NT, ctx->f2_smem));
-            if (o2 >= 2) {
-                ctx->f2 = 1;
-                ctx->f2_grid = o2 * ctx->num_sms;
-            }
-        }
         // billiard / oracle K2b with two chains per SM (lanczos2.cuh) where M fits half an SM's
         // shared memory; SPECWALK_LZ_OLD=1 keeps the register-resident lanczos_kernel (A/B)
         if (ctx->k2_variant == 1 && !getenv("SPECWALK_LZ_OLD")) {
@@ -612,10 +598,7 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<256, 8><<<g(ctx->l_grid), 256, ctx->l_smem, ctx->stream>>>(P);
         } else if (ctx->k2_variant == 1) {
-            if (ctx->f2)
-                factor2_kernel<<<g(ctx->f2_grid), F2_NT, ctx->f2_smem, ctx->stream>>>(P);
-            else
-                factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             if (ctx->lz2)
                 lanczos2_kernel<<<g(ctx->l2_grid), LZ2_NT, ctx->l2_smem, ctx->stream>>>(P);
@@ -858,7 +841,7 @@ static int ensure_chmc(spec_ctx* ctx, int q, long long C) {
     if (d > ctx->chmc_d) {
         if (ctx->chmc_scratch) cudaFree(ctx->chmc_scratch);
         ctx->chmc_scratch = nullptr;
-        ctx->chmc_smem = sizeof(double) * (size_t)16 * (mp + 8);
+        ctx->chmc_smem = sizeof(double) * (size_t)(16 + CH_MAXD + 1) * (mp + 8);
         CK(cudaFuncSetAttribute(chmc_chord_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)ctx->chmc_smem));
         int occ = 0;
@@ -1655,9 +1638,8 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
                  "lanczos_cl_kernel (2-CTA clusters, %d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->chord_grid_max, ctx->cl_grid, ctx->t_grid);
     else if (ctx->k2_split)
-        snprintf(buf, sizeof(buf), "split: %s (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
-                 ctx->f2 ? "factor2_kernel<256 thr, 2/SM>" : "factor_kernel<512>", ctx->f2 ? ctx->f2_grid : ctx->f_grid,
-                 ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
+        snprintf(buf, sizeof(buf), "split: factor_kernel<512> (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->f_grid, ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
                  ctx->lz2 ? ctx->l2_grid : ctx->l_grid, ctx->t_grid);
     else
         snprintf(buf, sizeof(buf), "fused: chord_kernel2<%d, %s> (%d CTAs)", ctx->chord_threads,
