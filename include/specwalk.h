@@ -161,7 +161,10 @@ enum { SPEC_WALK_BILLIARD = 0, SPEC_WALK_HMC = 1, SPEC_WALK_HNR = 2, SPEC_WALK_C
  * polynomial through (x, v) whose second derivative matches -grad f at q Chebyshev nodes (Picard
  * iteration); a segment's chord is the first root of det F(p(t)) in (0, h'] (Lemma 3 for a
  * degree-d curve).  No root: x = p(h'), v = p'(h').  A root t+: p'(t+) is reflected (Alg. 3) and
- * the reflection counts towards rho.  One segment = one boundary-oracle call. */
+ * the reflection counts towards rho.  One segment = one boundary-oracle call.  The Picard iteration
+ * contracts when h^2 times the largest curvature of f is below ~1 (Gaussian: h < sigma); a segment
+ * whose iteration did not converge in 64 steps uses the last iterate and is counted
+ * (spec_chmc_counters). */
 
 typedef struct spec_walk_params {
     int kind;            /* SPEC_WALK_BILLIARD (Alg. 5), SPEC_WALK_HMC (Alg. 6, Boltzmann), SPEC_WALK_HNR, SPEC_WALK_CHNR */
