@@ -219,7 +219,7 @@ __device__ double scalar_first_root(const double* g0, int D, double tmax, bool o
 
 // ---------------------------------------------------------------- K7b
 template <int NT>
-__global__ void __launch_bounds__(NT, 1) chmc_chord_kernel(ChordParams P, ChmcParams H) {
+__global__ void __launch_bounds__(NT, (NT <= 256) ? 2 : 1) chmc_chord_kernel(ChordParams P, ChmcParams H) {
     Team T;
     T.tid = threadIdx.x;
     T.nthr = NT;

@@ -166,7 +166,7 @@ struct spec_ctx {
     ChmcBuf chb;
     double* chmc_scratch = nullptr;
     long long chmc_stride = 0;
-    int chmc_grid = 0, chmc_d = 0;
+    int chmc_grid = 0, chmc_d = 0, chmc_nt = 512;
     size_t chmc_smem = 0;
     unsigned long long* picard = nullptr;  // Picard iterations, segments, unconverged
 };
@@ -842,10 +842,19 @@ static int ensure_chmc(spec_ctx* ctx, int q, long long C) {
         if (ctx->chmc_scratch) cudaFree(ctx->chmc_scratch);
         ctx->chmc_scratch = nullptr;
         ctx->chmc_smem = sizeof(double) * (size_t)(16 + CH_MAXD + 1) * (mp + 8);
-        CK(cudaFuncSetAttribute(chmc_chord_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)ctx->chmc_smem));
+        // m <= 64: 256 threads and two chains per SM (the per-chain latency chain is short of work
+        // for 16 warps); larger m: 512 threads, one chain per SM
+        ctx->chmc_nt = (mp <= 64 && !getenv("SPECWALK_CHMC_512")) ? 256 : 512;
         int occ = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chmc_chord_kernel<512>, 512, ctx->chmc_smem));
+        if (ctx->chmc_nt == 256) {
+            CK(cudaFuncSetAttribute(chmc_chord_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ctx->chmc_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chmc_chord_kernel<256>, 256, ctx->chmc_smem));
+        } else {
+            CK(cudaFuncSetAttribute(chmc_chord_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)ctx->chmc_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, chmc_chord_kernel<512>, 512, ctx->chmc_smem));
+        }
         if (occ < 1) return fail(SPEC_ECUDA, "collocation chord kernel cannot be resident");
         ctx->chmc_grid = occ * ctx->num_sms;
         ctx->chmc_stride = (long long)chmc_nmat(d) * mp * ctx->ld;
@@ -904,7 +913,10 @@ static int launch_chmc(spec_ctx* ctx, ChordParams P, const ChmcParams& H, int co
     P.scratch = ctx->chmc_scratch;
     P.scratch_stride = ctx->chmc_stride;
     const int grid = std::min(count_host, ctx->chmc_grid);
-    chmc_chord_kernel<512><<<std::max(grid, 1), 512, ctx->chmc_smem, ctx->stream>>>(P, H);
+    if (ctx->chmc_nt == 256)
+        chmc_chord_kernel<256><<<std::max(grid, 1), 256, ctx->chmc_smem, ctx->stream>>>(P, H);
+    else
+        chmc_chord_kernel<512><<<std::max(grid, 1), 512, ctx->chmc_smem, ctx->stream>>>(P, H);
     ctx->launches += 2;
     CK(cudaGetLastError());
     return SPEC_OK;
