@@ -844,7 +844,7 @@ static int ensure_chmc(spec_ctx* ctx, int q, long long C) {
         ctx->chmc_smem = sizeof(double) * (size_t)(16 + CH_MAXD + 1) * (mp + 8);
         // m <= 64: 256 threads and two chains per SM (the per-chain latency chain is short of work
         // for 16 warps); larger m: 512 threads, one chain per SM
-        ctx->chmc_nt = (mp <= 64 && !getenv("SPECWALK_CHMC_512")) ? 256 : 512;
+        ctx->chmc_nt = (mp <= 128 && !getenv("SPECWALK_CHMC_512")) ? 256 : 512;
         int occ = 0;
         if (ctx->chmc_nt == 256) {
             CK(cudaFuncSetAttribute(chmc_chord_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
