@@ -17,12 +17,35 @@
 
 namespace sw {
 
+// Inverse diagonal blocks (Lv, 64 doubles each) are stored row-major with the column index
+// XOR-swizzled by bit 1 of the row, so that the DMMA fragment loads W[r][q], W[r][4+q] of a
+// half-warp (rows 0..3 or 4..7) hit 16 distinct 8-byte bank slots (an unswizzled 8-wide row
+// puts rows r and r+2 on the same banks: 2-way conflicts, ncu r2fs).
+__device__ __forceinline__ int lv_idx(int r, int c) { return r * 8 + (c ^ ((r & 2) << 1)); }
+
+// Conflict-free access to the DMMA accumulator pair C[r][2q], C[r][2q+1] (rows of an even
+// leading dimension ld = 4 or 12 mod 16): odd rows touch their two elements in the opposite
+// order, so each of the two 8-byte accesses of a half-warp hits 16 distinct bank slots (in
+// order, rows r and r+1 collide: 2-way conflicts on every tile load / store, ncu r2fs).
+__device__ __forceinline__ void acc_ld(double (&acc)[2], const double* C, int ld, int r, int q) {
+    const int sw = r & 1;
+    const double v0 = C[r * ld + 2 * q + sw];
+    const double v1 = C[r * ld + 2 * q + 1 - sw];
+    acc[0] = sw ? v1 : v0;
+    acc[1] = sw ? v0 : v1;
+}
+__device__ __forceinline__ void acc_st(const double (&acc)[2], double* C, int ld, int r, int q) {
+    const int sw = r & 1;
+    C[r * ld + 2 * q + sw] = sw ? acc[1] : acc[0];
+    C[r * ld + 2 * q + 1 - sw] = sw ? acc[0] : acc[1];
+}
+
 // acc(8x8) = A(8x8, row-major lda) * W^T, W 8x8 row-major (ldw): C[r][c] = sum_k A[r][k] W[c][k]
 __device__ __forceinline__ void tile_mul_wt(double (&acc)[2], const double* A, int lda, const double* W, int ldw,
                                             int lane) {
     const int r = lane >> 2, q = lane & 3;
     const double a0 = A[r * lda + q], a1 = A[r * lda + 4 + q];
-    const double b0 = W[r * ldw + q], b1 = W[r * ldw + 4 + q];
+    const double b0 = W[lv_idx(r, q)], b1 = W[lv_idx(r, 4 + q)];  // W: an Lv block (ldw = 8, swizzled)
     acc[0] = 0.0;
     acc[1] = 0.0;
     dmma_t(acc, a0, b0);
@@ -33,7 +56,7 @@ __device__ __forceinline__ void tile_mul_wt(double (&acc)[2], const double* A, i
 __device__ __forceinline__ void tile_mul_w(double (&acc)[2], const double* W, int ldw, const double* Bp, int ldb,
                                            int lane) {
     const int r = lane >> 2, q = lane & 3;
-    const double a0 = W[r * ldw + q], a1 = W[r * ldw + 4 + q];
+    const double a0 = W[lv_idx(r, q)], a1 = W[lv_idx(r, 4 + q)];  // W: an Lv block (ldw = 8, swizzled)
     const double b0 = Bp[q * ldb + r], b1 = Bp[(4 + q) * ldb + r];
     acc[0] = 0.0;
     acc[1] = 0.0;
@@ -87,7 +110,7 @@ __device__ __forceinline__ bool diag_factor_inv(double* D, int ld, double* rd8, 
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
             if (c <= r) D[r * ld + c] = a[c];
-            V[r * 8 + c] = (c <= r) ? x[c] : 0.0;
+            V[lv_idx(r, c)] = (c <= r) ? x[c] : 0.0;
         }
         rd8[r] = rd;
     }
@@ -134,7 +157,7 @@ __device__ __forceinline__ bool diag_factor_inv_reg(double* D, int ld, double* r
     if (lane < 8) {
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            V[r * 8 + c] = (r >= c) ? x[r] : 0.0;
+            V[lv_idx(r, c)] = (r >= c) ? x[r] : 0.0;
             if (r == lane) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k)
@@ -179,8 +202,7 @@ __device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld,
             double acc[2];
             tile_mul_wt(acc, Ct, ld, Vk, 8, T.lane);
             __syncwarp();
-            Ct[rr * ld + 2 * q] = acc[0];
-            Ct[rr * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, Ct, ld, rr, q);
         }
         __syncthreads();
         const int Tr = TB - kb - 1;
@@ -188,10 +210,10 @@ __device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld,
         if (T.warp == 0) {
             // tile (kb+1, kb+1) of the trailing update, then its factor and inverse
             double* C = G + (kb + 1) * 8 * ld + (kb + 1) * 8;
-            double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
+            double acc[2];
+            acc_ld(acc, C, ld, rr, q);
             tile_msub<true>(acc, G + (kb + 1) * 8 * ld + k0, ld, G + (kb + 1) * 8 * ld + k0, ld, 8, T.lane);
-            C[rr * ld + 2 * q] = acc[0];
-            C[rr * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, rr, q);
             __syncwarp();
             const bool ok = SW_DIAG_FACTOR(C, ld, rdiag + (kb + 1) * 8, Lv + (kb + 1) * 64, T.lane);
             if (T.lane == 0) *flag = ok ? 0 : 1;
@@ -204,10 +226,10 @@ __device__ bool cholesky_inv_blocked_la(const Team& T, double* G, int n, int ld,
             while (ii < Tr) {
                 const int ib = kb + 1 + ii, jb = kb + 1 + jj;
                 double* C = G + ib * 8 * ld + jb * 8;
-                double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
+                double acc[2];
+            acc_ld(acc, C, ld, rr, q);
                 tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
-                C[rr * ld + 2 * q] = acc[0];
-                C[rr * ld + 2 * q + 1] = acc[1];
+                acc_st(acc, C, ld, rr, q);
                 jj += T.nwarps - 1;
                 while (ii < Tr && jj > ii) { jj -= ii + 1; ++ii; }
             }
@@ -267,7 +289,7 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     if (c <= r) D[r * ld + c] = a[c];
-                    Vk[r * 8 + c] = (c <= r) ? x[c] : 0.0;
+                    Vk[lv_idx(r, c)] = (c <= r) ? x[c] : 0.0;
                 }
                 rdiag[k0 + r] = rd;
             }
@@ -282,8 +304,7 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
             tile_mul_wt(acc, Ct, ld, Vk, 8, T.lane);
             __syncwarp();
             const int r = T.lane >> 2, q = T.lane & 3;
-            Ct[r * ld + 2 * q] = acc[0];
-            Ct[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, Ct, ld, r, q);
         }
         __syncthreads();
         // trailing SYRK on DMMA tiles: G_ij -= P_i P_j^T, kb < j <= i (tile index walked
@@ -295,10 +316,10 @@ __device__ bool cholesky_inv_blocked(const Team& T, double* G, int n, int ld, do
             const int ib = kb + 1 + ii, jb = kb + 1 + jj;
             double* C = G + ib * 8 * ld + jb * 8;
             const int rr = T.lane >> 2, q = T.lane & 3;
-            double acc[2] = {C[rr * ld + 2 * q], C[rr * ld + 2 * q + 1]};
+            double acc[2];
+            acc_ld(acc, C, ld, rr, q);
             tile_msub<true>(acc, G + ib * 8 * ld + k0, ld, G + jb * 8 * ld + k0, ld, 8, T.lane);
-            C[rr * ld + 2 * q] = acc[0];
-            C[rr * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, rr, q);
             jj += T.nwarps;
             while (ii < Tr && jj > ii) { jj -= ii + 1; ++ii; }
         }
@@ -323,14 +344,12 @@ __device__ void trsm_inv_blocked(const Team& T, const double* G, const double* L
                 double* Bt = B + k0 * ld + cb * 8;  // W tile (kb, cb) = B rows k0.., cols cb*8..
                 tile_mul_w(acc, Vk, 8, Bt, ld, T.lane);
                 __syncwarp();
-                Bt[r * ld + 2 * q] = acc[0];
-                Bt[r * ld + 2 * q + 1] = acc[1];
+                acc_st(acc, Bt, ld, r, q);
             } else {
                 double* Bt = B + cb * 8 * ld + k0;  // W tile (kb, cb) = (B rows cb*8.., cols k0..)^T
                 tile_mul_wt(acc, Bt, ld, Vk, 8, T.lane);
                 __syncwarp();
-                Bt[r * ld + 2 * q] = acc[0];
-                Bt[r * ld + 2 * q + 1] = acc[1];
+                acc_st(acc, Bt, ld, r, q);
             }
         }
         __syncthreads();
@@ -346,8 +365,7 @@ __device__ void trsm_inv_blocked(const Team& T, const double* G, const double* L
                 acc[0] = C[r * ld + 2 * q];
                 acc[1] = C[r * ld + 2 * q + 1];
                 tile_msub<false>(acc, A, ld, B + k0 * ld + cb * 8, ld, 8, T.lane);
-                C[r * ld + 2 * q] = acc[0];
-                C[r * ld + 2 * q + 1] = acc[1];
+                acc_st(acc, C, ld, r, q);
             } else {
                 double* Ct = B + cb * 8 * ld + ib * 8;
                 acc[0] = Ct[(2 * q) * ld + r];
@@ -375,14 +393,12 @@ __device__ void trsm_inv_blocked_la(const Team& T, const double* G, const double
             double* Bt = B + cb * 8;
             tile_mul_w(acc, Lv, 8, Bt, ld, T.lane);
             __syncwarp();
-            Bt[r * ld + 2 * q] = acc[0];
-            Bt[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, Bt, ld, r, q);
         } else {
             double* Bt = B + cb * 8 * ld;
             tile_mul_wt(acc, Bt, ld, Lv, 8, T.lane);
             __syncwarp();
-            Bt[r * ld + 2 * q] = acc[0];
-            Bt[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, Bt, ld, r, q);
         }
     }
     __syncthreads();
@@ -401,14 +417,12 @@ __device__ void trsm_inv_blocked_la(const Team& T, const double* G, const double
                 acc[0] = C[r * ld + 2 * q];
                 acc[1] = C[r * ld + 2 * q + 1];
                 tile_msub<false>(acc, A, ld, B + k0 * ld + cb * 8, ld, 8, T.lane);
-                C[r * ld + 2 * q] = acc[0];
-                C[r * ld + 2 * q + 1] = acc[1];
+                acc_st(acc, C, ld, r, q);
                 if (ib == kb + 1) {  // finish block row kb+1: W = L^{-1} W for this tile
                     __syncwarp();
                     tile_mul_w(acc, Vn, 8, C, ld, T.lane);
                     __syncwarp();
-                    C[r * ld + 2 * q] = acc[0];
-                    C[r * ld + 2 * q + 1] = acc[1];
+                    acc_st(acc, C, ld, r, q);
                 }
             } else {
                 double* Ct = B + cb * 8 * ld + ib * 8;
@@ -421,8 +435,7 @@ __device__ void trsm_inv_blocked_la(const Team& T, const double* G, const double
                     __syncwarp();
                     tile_mul_wt(acc, Ct, ld, Vn, 8, T.lane);
                     __syncwarp();
-                    Ct[r * ld + 2 * q] = acc[0];
-                    Ct[r * ld + 2 * q + 1] = acc[1];
+                    acc_st(acc, Ct, ld, r, q);
                 }
             }
         }
@@ -468,15 +481,14 @@ __device__ void trsm_ll_cols(const Team& T, const double* G, const double* Lv, d
         double* Bc = B + cb * 8;
         for (int ib = 0; ib < TB; ++ib) {
             double* C = Bc + ib * 8 * ld;
-            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            double acc[2];
+            acc_ld(acc, C, ld, r, q);
             if (ib > 0) tile_msub2<false>(acc, G + ib * 8 * ld, ld, Bc, ld, 8 * ib, T.lane);
-            C[r * ld + 2 * q] = acc[0];
-            C[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, r, q);
             __syncwarp();
             tile_mul_w(acc, Lv + ib * 64, 8, C, ld, T.lane);
             __syncwarp();
-            C[r * ld + 2 * q] = acc[0];
-            C[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, r, q);
             __syncwarp();
         }
     }
@@ -492,15 +504,14 @@ __device__ void trsm_ll_rows(const Team& T, const double* G, const double* Lv, d
         double* Br = B + rb * 8 * ld;
         for (int jb = 0; jb < TB; ++jb) {
             double* C = Br + jb * 8;
-            double acc[2] = {C[r * ld + 2 * q], C[r * ld + 2 * q + 1]};
+            double acc[2];
+            acc_ld(acc, C, ld, r, q);
             if (jb > 0) tile_msub2<true>(acc, Br, ld, G + jb * 8 * ld, ld, 8 * jb, T.lane);
-            C[r * ld + 2 * q] = acc[0];
-            C[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, r, q);
             __syncwarp();
             tile_mul_wt(acc, C, ld, Lv + jb * 64, 8, T.lane);
             __syncwarp();
-            C[r * ld + 2 * q] = acc[0];
-            C[r * ld + 2 * q + 1] = acc[1];
+            acc_st(acc, C, ld, r, q);
             __syncwarp();
         }
     }

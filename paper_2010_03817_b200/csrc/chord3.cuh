@@ -60,6 +60,33 @@ __device__ __forceinline__ void unpack_sym_async(const Team& T, const double* __
         }
     }
 }
+// the same copy per 8 x 8 tile of the lower triangle (one warp per tile): lane (r, q) copies
+// elements (r, q) and (r, q + 4) and their transposes, so that both the row-wise and the
+// transposed 8-byte writes of a half-warp hit distinct bank slots (ld = 4 or 12 mod 16); the
+// row-wise copy's transposed writes were 4-way conflicted (14% of K2a's excess shared-memory
+// wavefronts, ncu r2fs)
+__device__ __forceinline__ void unpack_sym_tiles_async(const Team& T, const double* __restrict__ P, double* M, int m,
+                                                       int ld) {
+    const int TB = (m + 7) >> 3;
+    const int ntile = TB * (TB + 1) / 2;
+    const int r = T.lane >> 2, q = T.lane & 3;
+    for (int t = T.warp; t < ntile; t += T.nwarps) {
+        int ib = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while ((ib + 1) * (ib + 2) / 2 <= t) ++ib;
+        while (ib * (ib + 1) / 2 > t) --ib;
+        const int jb = t - ib * (ib + 1) / 2;
+        const int i = ib * 8 + r;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int j = jb * 8 + q + 4 * h;
+            if (i < m && j <= i) {
+                const double* src = P + (size_t)i * (i + 1) / 2 + j;
+                cp_async8(M + i * ld + j, src);
+                if (j < i) cp_async8(M + j * ld + i, src);
+            }
+        }
+    }
+}
 __device__ __forceinline__ void mirror_upper(const Team& T, double* M, int m, int ld) {
     for (int i = T.warp; i < m; i += T.nwarps)
         for (int j = T.lane; j < i; j += 32) M[j * ld + i] = M[i * ld + j];
@@ -105,8 +132,8 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
         __syncthreads();
         long long t_prof = clock64();
 #if SW_UNPACK_BOTH
-        unpack_sym_async(T, ax, G, m, ld);
-        unpack_sym_async(T, av, B, m, ld);
+        unpack_sym_tiles_async(T, ax, G, m, ld);
+        unpack_sym_tiles_async(T, av, B, m, ld);
 #else
         unpack_lower_async(T, ax, G, m, ld);
         unpack_lower_async(T, av, B, m, ld);
@@ -178,18 +205,26 @@ __global__ void __launch_bounds__(NT, 1) factor_kernel(ChordParams P) {
             } else {
                 congruence_inv(T, Gd, Lv, Bd, mdp, ld);
                 PROF_MARK(3);
-                // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp)
+                // M = -(B + B^T)/2 and L to the work buffers (rows of length mdp), per 8 x 8 tile
+                // (lane (r, q): elements (r, q), (r, q + 4)) so that the transposed reads of B are
+                // conflict-free (the row-wise pass's column reads were 4-way conflicted, ncu r2fs)
                 double* Mw = P.wM + (size_t)slot * P.w_mstride;
                 double* Lw = P.wL + (size_t)slot * P.w_mstride;
-                for (int i = T.warp; i < mdp; i += T.nwarps)
-                    for (int jx = T.lane; jx < mdp; jx += 32) {
+                const int TBd = mdp >> 3;
+                const int tr = T.lane >> 2, tq = T.lane & 3;
+                for (int t = T.warp; t < TBd * TBd; t += T.nwarps) {
+                    const int i = (t / TBd) * 8 + tr;
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int jx = (t % TBd) * 8 + tq + 4 * h;
 #if SW_FACTOR_SYM
                         Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
 #else
-                        Mw[i * ld + jx] = -Bd[i * ld + jx];  // rows only: no column (bank-conflicted) reads
+                        Mw[i * ld + jx] = -Bd[i * ld + jx];
 #endif
                         if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];  // packed lower rows (tail_kernel)
                     }
+                }
             }
         }
         // scalars and vectors of the slot

@@ -58,8 +58,8 @@ __device__ void fwd_solve_vecs(const Team& T, const double* G, const double* Lv,
             const double ri = x[k0 + r] - acc;
             const double r0 = __shfl_sync(0xffffffffu, ri, 8 * q);
             const double r1 = __shfl_sync(0xffffffffu, ri, 8 * q + 4);
-            const double* V = Lv + kb * 64 + r * 8;
-            double part = fma(V[2 * q], r0, V[2 * q + 1] * r1);
+            const double* V = Lv + kb * 64;
+            double part = fma(V[lv_idx(r, 2 * q)], r0, V[lv_idx(r, 2 * q + 1)] * r1);
             part += __shfl_xor_sync(0xffffffffu, part, 1);
             part += __shfl_xor_sync(0xffffffffu, part, 2);
             __syncwarp();
