@@ -23,23 +23,6 @@ namespace sw {
 // puts rows r and r+2 on the same banks: 2-way conflicts, ncu r2fs).
 __device__ __forceinline__ int lv_idx(int r, int c) { return r * 8 + (c ^ ((r & 2) << 1)); }
 
-// Conflict-free access to the DMMA accumulator pair C[r][2q], C[r][2q+1] (rows of an even
-// leading dimension ld = 4 or 12 mod 16): odd rows touch their two elements in the opposite
-// order, so each of the two 8-byte accesses of a half-warp hits 16 distinct bank slots (in
-// order, rows r and r+1 collide: 2-way conflicts on every tile load / store, ncu r2fs).
-__device__ __forceinline__ void acc_ld(double (&acc)[2], const double* C, int ld, int r, int q) {
-    const int sw = r & 1;
-    const double v0 = C[r * ld + 2 * q + sw];
-    const double v1 = C[r * ld + 2 * q + 1 - sw];
-    acc[0] = sw ? v1 : v0;
-    acc[1] = sw ? v0 : v1;
-}
-__device__ __forceinline__ void acc_st(const double (&acc)[2], double* C, int ld, int r, int q) {
-    const int sw = r & 1;
-    C[r * ld + 2 * q + sw] = sw ? acc[1] : acc[0];
-    C[r * ld + 2 * q + 1 - sw] = sw ? acc[0] : acc[1];
-}
-
 // acc(8x8) = A(8x8, row-major lda) * W^T, W 8x8 row-major (ldw): C[r][c] = sum_k A[r][k] W[c][k]
 __device__ __forceinline__ void tile_mul_wt(double (&acc)[2], const double* A, int lda, const double* W, int ldw,
                                             int lane) {
