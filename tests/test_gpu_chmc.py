@@ -76,6 +76,8 @@ CASES = [
     ("rand_40_40_logcosh_q3", lambda: specgen.rand_cube(40, 40, 2), "logcosh", 0.4, 3, 0.2, 1.0),
     ("cube_only_6_gauss_q6", lambda: specgen.cube_only(6), "gauss", 0.6, 6, 0.5, 1.5),
     ("rand_20_100_gauss_q3", lambda: specgen.rand_cube(20, 100, 3), "gauss", 0.5, 3, 0.1, 1.0),
+    # m > 128: 512 threads, one chain per SM; the Lanczos matvec's general path (mdp > 128)
+    ("rand_8_136_logcosh_q2", lambda: specgen.rand_cube(8, 136, 8), "logcosh", 0.5, 2, 0.4, 1.0),
 ]
 
 
@@ -84,7 +86,7 @@ def test_chmc_oracle_interior_parity(name, make, pot, sigma, q, h, vscale):
     inst = make()
     lmi = oracle.Lmi(inst)
     S, c, mu, colloc = _setup(inst, POTS[pot], sigma)
-    count = 16 if inst.m >= 100 else 48
+    count = 8 if inst.m > 128 else (16 if inst.m >= 100 else 48)
     xs, vs = _interior(inst, lmi, count, 11, vscale)
     # h: most segments hit; h / 8: most end inside (t_plus = +inf on both sides)
     for hh, need in ((h, count // 8), (h / 8, 0)):
@@ -106,7 +108,7 @@ def test_chmc_oracle_boundary_start_parity(name, make, pot, sigma, q, h, vscale)
     inst = specgen.Instance(inst0.name, inst0.A)  # dense block only
     lmi = oracle.Lmi(inst)
     S, c, mu, colloc = _setup(inst, POTS[pot], sigma)
-    count = 12 if inst.m >= 100 else 40
+    count = 8 if inst.m > 128 else (12 if inst.m >= 100 else 40)
     xs, vs = _interior(inst, lmi, count, 13, vscale)
     hits, ss, us = [], [], []
     for k in range(count):
@@ -121,7 +123,7 @@ def test_chmc_oracle_boundary_start_parity(name, make, pot, sigma, q, h, vscale)
         hits.append(hit)
         ss.append(oracle.reflect(vel, w))
         us.append(r["y"] / np.linalg.norm(r["y"]))
-    assert len(hits) >= 6
+    assert len(hits) >= min(6, count // 2)
     hits, ss, us = map(np.array, (hits, ss, us))
     for hh in (h, 4 * h):
         refs = [_ref(lmi, hits[k], ss[k], q, hh, colloc, c, sigma, F0=lmi.eval_block(0, hits[k]), bound=0,
@@ -220,3 +222,18 @@ def test_chmc_invalid_arguments():
         S.set_potential(sw.POT_LINEAR, None, 1.0)  # no objective
     with pytest.raises(sw.SpecError):
         S.set_potential(sw.POT_GAUSS, None, -1.0)
+
+
+def test_chmc_oracle_empty_batch_and_counters():
+    """batch = 0 is a no-op; the device counters see the segments of a call and reset."""
+    import paper_2010_03817_b200 as sw
+    inst = specgen.rand_cube(6, 6, 1)
+    S, c, mu, colloc = _setup(inst, oracle.POT_GAUSS, 0.8)
+    res = S.chmc_oracle(np.zeros((0, 6)), np.zeros((0, 6)), 3, 0.2)
+    assert res["t_plus"].shape == (0,)
+    S.chmc_counters(reset=True)
+    xs, vs = _interior(inst, oracle.Lmi(inst), 10, 3)
+    S.chmc_oracle(xs, vs, 3, 0.2)
+    cnt = S.chmc_counters(reset=True)
+    assert cnt["segments"] == 10 and cnt["unconverged"] == 0 and cnt["picard"] >= 10
+    assert S.chmc_counters(reset=False)["segments"] == 0
