@@ -25,6 +25,7 @@
 #include "hmc.cuh"
 #include "hmc2.cuh"
 #include "colloc.cuh"
+#include "factor_t.cuh"
 #include "estimators.cuh"
 #include <algorithm>
 
@@ -138,6 +139,8 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    int ft = 0, ft_grid = 0;   // K2a as factor_t_kernel (lower-tile storage, two chains per SM, m <= 104)
+    size_t ft_smem = 0;
     int g_split = 0, cl_grid = 0;  // m > 112: factor (global scratch) | lanczos_cl_kernel (2-CTA cluster) | tail
     size_t cl_smem = 0;
     size_t l2_smem = 0;
@@ -445,6 +448,18 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->f_grid = of * ctx->num_sms;
         ctx->l_grid = ol * ctx->num_sms;
         ctx->t_grid = ot * ctx->num_sms;
+        // K2a with both matrices as lower 8 x 8 tiles, two chains per SM (factor_t.cuh);
+        // opt-in (SPECWALK_FACTOR_T=1) until measured
+        if (ctx->k2_variant == 1 && mp <= 8 * FT_TBMAX && getenv("SPECWALK_FACTOR_T")) {
+            ctx->ft_smem = sizeof(double) * ft_smem_doubles(mp);
+            int o2 = 0;
+            CK(cudaFuncSetAttribute(factor_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->ft_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, factor_t_kernel, FT_NT, ctx->ft_smem));
+            if (o2 >= 1) {
+                ctx->ft = 1;
+                ctx->ft_grid = o2 * ctx->num_sms;
+            }
+        }
         // billiard / oracle K2b with two chains per SM (lanczos2.cuh) where M fits half an SM's
         // shared memory; SPECWALK_LZ_OLD=1 keeps the register-resident lanczos_kernel (A/B)
         if (ctx->k2_variant == 1 && !getenv("SPECWALK_LZ_OLD")) {
@@ -598,7 +613,10 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             lanczos_kernel<256, 8><<<g(ctx->l_grid), 256, ctx->l_smem, ctx->stream>>>(P);
         } else if (ctx->k2_variant == 1) {
-            factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
+            if (ctx->ft)
+                factor_t_kernel<<<g(ctx->ft_grid), FT_NT, ctx->ft_smem, ctx->stream>>>(P);
+            else
+                factor_kernel<512><<<g(ctx->f_grid), 512, ctx->f_smem, ctx->stream>>>(P);
             if (sub) cudaEventRecord(sub[0], ctx->stream);
             if (ctx->lz2)
                 lanczos2_kernel<<<g(ctx->l2_grid), LZ2_NT, ctx->l2_smem, ctx->stream>>>(P);
@@ -1650,8 +1668,9 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
                  "lanczos_cl_kernel (2-CTA clusters, %d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->chord_grid_max, ctx->cl_grid, ctx->t_grid);
     else if (ctx->k2_split)
-        snprintf(buf, sizeof(buf), "split: factor_kernel<512> (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
-                 ctx->f_grid, ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
+        snprintf(buf, sizeof(buf), "split: %s (%d CTAs) | %s (%d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->ft ? "factor_t_kernel<256 thr, tiles>" : "factor_kernel<512>", ctx->ft ? ctx->ft_grid : ctx->f_grid,
+                 ctx->lz2 ? "lanczos2_kernel<256 thr, 2/SM>" : "lanczos_kernel<512>",
                  ctx->lz2 ? ctx->l2_grid : ctx->l_grid, ctx->t_grid);
     else
         snprintf(buf, sizeof(buf), "fused: chord_kernel2<%d, %s> (%d CTAs)", ctx->chord_threads,
