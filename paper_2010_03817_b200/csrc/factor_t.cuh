@@ -73,23 +73,100 @@ __device__ void ft_unpack(const Team& T, const double* __restrict__ P, double* T
         for (int j = T.tid; j < m; j += T.nthr) row0[j] = P[pk(j, 0)];
 }
 
-// p = beta X h - (beta/2)(h . beta X h) h for X = [[row0], [row0^T, tiles]] (m x m)
-__device__ void ft_householder_vec(const Team& T, const double* Xt, const double* row0, int m, const double* h,
-                                   double beta, double* p, double* red) {
-    for (int i = T.tid; i < m; i += T.nthr) {
-        double s = row0[i] * h[0];
-        if (i == 0) {
-            for (int j = 1; j < m; ++j) s = fma(row0[j], h[j], s);
-        } else {
-            for (int j = 1; j < m; ++j) s = fma(tsym(Xt, i - 1, j - 1), h[j], s);
+// p = beta X h - (beta/2)(h . beta X h) h for X = [[row0], [row0^T, tiles]] (m x m), for G and B
+// at once: (X h) of the trailing block as row sums (a warp per block row, tiles J <= I in order)
+// plus the transposed tiles' column sums (a warp per block column, tiles I > J in order) --
+// deterministic: every sum in a fixed order (lane (r, q): elements (r, q), (r, q + 4))
+__device__ void ft_householder_vecs(const Team& T, const double* Gt, const double* Bt, const double* g0,
+                                    const double* b0, int m, int md, int TB, const double* h, double beta,
+                                    double* pg, double* pb, double* cg, double* cb, double* red) {
+    const int r = T.lane >> 2, q = T.lane & 3;
+    const double* h1 = h + 1;  // trailing index i' = i - 1
+    for (int w = T.warp; w < 2 * TB; w += T.nwarps) {
+        if (w < TB) {  // block row I = w: sum_J X_IJ h_J
+            const int I = w;
+            double sg = 0.0, sb = 0.0;
+            for (int J = 0; J <= I; ++J) {
+                const double* Xg = Gt + tix(I, J);
+                const double* Xb = Bt + tix(I, J);
+                const int c0 = J * 8 + q, c1 = c0 + 4;
+                const double hc0 = (c0 < md) ? h1[c0] : 0.0, hc1 = (c1 < md) ? h1[c1] : 0.0;
+                sg = fma(Xg[tph(r, q)], hc0, sg);
+                sg = fma(Xg[tph(r, 4 + q)], hc1, sg);
+                sb = fma(Xb[tph(r, q)], hc0, sb);
+                sb = fma(Xb[tph(r, 4 + q)], hc1, sb);
+            }
+            sg += __shfl_xor_sync(0xffffffffu, sg, 1);
+            sb += __shfl_xor_sync(0xffffffffu, sb, 1);
+            sg += __shfl_xor_sync(0xffffffffu, sg, 2);
+            sb += __shfl_xor_sync(0xffffffffu, sb, 2);
+            if (q == 0) {
+                pg[I * 8 + r] = sg;
+                pb[I * 8 + r] = sb;
+            }
+        } else {  // block column J = w - TB: sum_{I > J} X_IJ^T h_I
+            const int J = w - TB;
+            double tg0 = 0.0, tg1 = 0.0, tb0 = 0.0, tb1 = 0.0;
+            for (int I = J + 1; I < TB; ++I) {
+                const double* Xg = Gt + tix(I, J);
+                const double* Xb = Bt + tix(I, J);
+                const int ri = I * 8 + r;
+                const double hr = (ri < md) ? h1[ri] : 0.0;
+                tg0 = fma(Xg[tph(r, q)], hr, tg0);
+                tg1 = fma(Xg[tph(r, 4 + q)], hr, tg1);
+                tb0 = fma(Xb[tph(r, q)], hr, tb0);
+                tb1 = fma(Xb[tph(r, 4 + q)], hr, tb1);
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                tg0 += __shfl_xor_sync(0xffffffffu, tg0, o);
+                tg1 += __shfl_xor_sync(0xffffffffu, tg1, o);
+                tb0 += __shfl_xor_sync(0xffffffffu, tb0, o);
+                tb1 += __shfl_xor_sync(0xffffffffu, tb1, o);
+            }
+            if (r == 0) {
+                cg[J * 8 + q] = tg0;
+                cg[J * 8 + q + 4] = tg1;
+                cb[J * 8 + q] = tb0;
+                cb[J * 8 + q + 4] = tb1;
+            }
         }
-        p[i] = beta * s;
     }
     __syncthreads();
-    double hp = 0.0;
-    for (int i = T.tid; i < m; i += T.nthr) hp += h[i] * p[i];
-    const double K = 0.5 * beta * block_sum(T, hp, red);
-    for (int i = T.tid; i < m; i += T.nthr) p[i] -= K * h[i];
+    // shift to full indices (i = i' + 1) and add the column part: trailing (X h)_i
+    for (int ip = T.tid; ip < md; ip += T.nthr) {
+        cg[ip] += pg[ip];
+        cb[ip] += pb[ip];
+    }
+    __syncthreads();
+    for (int i = T.tid; i < m; i += T.nthr) {
+        pg[i] = (i == 0) ? 0.0 : cg[i - 1];
+        pb[i] = (i == 0) ? 0.0 : cb[i - 1];
+    }
+    __syncthreads();
+    // row / column 0 and the scaling: p = beta (X h) - K h
+    double s0g = 0.0, s0b = 0.0;
+    for (int j = T.tid; j < m; j += T.nthr) {
+        s0g = fma(g0[j], h[j], s0g);
+        s0b = fma(b0[j], h[j], s0b);
+    }
+    s0g = block_sum(T, s0g, red);
+    s0b = block_sum(T, s0b, red);
+    double hpg = 0.0, hpb = 0.0;
+    for (int i = T.tid; i < m; i += T.nthr) {
+        const double yg = (i == 0) ? s0g : fma(g0[i], h[0], pg[i]);
+        const double yb = (i == 0) ? s0b : fma(b0[i], h[0], pb[i]);
+        pg[i] = beta * yg;
+        pb[i] = beta * yb;
+        hpg += h[i] * pg[i];
+        hpb += h[i] * pb[i];
+    }
+    const double Kg = 0.5 * beta * block_sum(T, hpg, red);
+    const double Kb = 0.5 * beta * block_sum(T, hpb, red);
+    for (int i = T.tid; i < m; i += T.nthr) {
+        pg[i] -= Kg * h[i];
+        pb[i] -= Kb * h[i];
+    }
     __syncthreads();
 }
 
@@ -255,12 +332,14 @@ __device__ void ft_congruence(const Team& T, const double* Wt, const double* Bt,
     for (int J = T.warp; J < TB; J += T.nwarps) {
         double yt[FT_TBMAX][2];
 #pragma unroll
-        for (int K = 0; K < FT_TBMAX; ++K) {
-            yt[K][0] = 0.0;
-            yt[K][1] = 0.0;
-            if (K < TB) {
-                for (int L = 0; L <= J; ++L) {
-                    const double* Wl = Wt + tix(J, L);
+        for (int K = 0; K < FT_TBMAX; ++K) yt[K][0] = yt[K][1] = 0.0;
+        // Y^T_JK = sum_{L <= J} W_JL B_LK: one W fragment feeds 13 independent accumulators
+        for (int L = 0; L <= J; ++L) {
+            const double* Wl = Wt + tix(J, L);
+            const double a0 = Wl[tph(r, q)], a1 = Wl[tph(r, 4 + q)];
+#pragma unroll
+            for (int K = 0; K < FT_TBMAX; ++K) {
+                if (K < TB) {
                     double b0, b1;
                     if (L >= K) {  // B_LK stored: element (q, r) / (4+q, r)
                         const double* Bl = Bt + tix(L, K);
@@ -271,21 +350,33 @@ __device__ void ft_congruence(const Team& T, const double* Wt, const double* Bt,
                         b0 = Bl[tph(r, q)];
                         b1 = Bl[tph(r, 4 + q)];
                     }
-                    dmma_t(yt[K], Wl[tph(r, q)], b0);
-                    dmma_t(yt[K], Wl[tph(r, 4 + q)], b1);
+                    dmma_t(yt[K], a0, b0);
+                    dmma_t(yt[K], a1, b1);
                 }
             }
         }
-        for (int I = J; I < TB; ++I) {
-            double acc[2] = {0.0, 0.0};
+        // M_IJ = -sum_{K <= I} W_IK Y_KJ, two output tiles at a time (independent chains)
+        for (int I0 = J; I0 < TB; I0 += 2) {
+            double accs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+            const bool two = (I0 + 1 < TB);
 #pragma unroll
             for (int K = 0; K < FT_TBMAX; ++K) {
-                if (K <= I) {
-                    const double* Wk = Wt + tix(I, K);
-                    dmma_t(acc, -Wk[tph(r, 2 * q)], yt[K][0]);
-                    dmma_t(acc, -Wk[tph(r, 2 * q + 1)], yt[K][1]);
+                if (K <= I0) {
+                    const double* Wk = Wt + tix(I0, K);
+                    dmma_t(accs[0], -Wk[tph(r, 2 * q)], yt[K][0]);
+                    dmma_t(accs[0], -Wk[tph(r, 2 * q + 1)], yt[K][1]);
+                }
+                if (two && K <= I0 + 1) {
+                    const double* Wk = Wt + tix(I0 + 1, K);
+                    dmma_t(accs[1], -Wk[tph(r, 2 * q)], yt[K][0]);
+                    dmma_t(accs[1], -Wk[tph(r, 2 * q + 1)], yt[K][1]);
                 }
             }
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+            const int I = I0 + u;
+            if (I >= TB) break;
+            const double* acc = accs[u];
             double* row = Mw + (size_t)(I * 8 + r) * ld + J * 8 + 2 * q;
             if (I > J) {
                 *reinterpret_cast<double2*>(row) = make_double2(acc[0], acc[1]);
@@ -299,6 +390,7 @@ __device__ void ft_congruence(const Team& T, const double* Wt, const double* Bt,
                 const double m1 = 0.5 * (acc[1] + sc[(2 * q + 1) * 8 + r]);
                 __syncwarp();
                 *reinterpret_cast<double2*>(row) = make_double2(m0, m1);
+            }
             }
         }
     }
@@ -373,25 +465,33 @@ __global__ void __launch_bounds__(FT_NT, 2) factor_t_kernel(ChordParams P) {
             double h2 = 0.0;
             for (int i = T.tid; i < m; i += T.nthr) h2 += hh[i] * hh[i];
             beta_h = 2.0 / block_sum(T, h2, red);
-            ft_householder_vec(T, Gt, g0, m, hh, beta_h, pw, red);
-            ft_householder_vec(T, Bt, b0, m, hh, beta_h, yy, red);
+            ft_householder_vecs(T, Gt, Bt, g0, b0, m, md, TB, hh, beta_h, pw, yy, rdiag, bv, red);
             a_schur = b0[0] - (hh[0] * yy[0] + yy[0] * hh[0]);
             outward = !(a_schur > 0.0);
             for (int i = T.tid; i + 1 < m; i += T.nthr) bv[i] = b0[i + 1] - (hh[i + 1] * yy[0] + yy[i + 1] * hh[0]);
             __syncthreads();
-            // trailing blocks (index i' = i - 1): G' = G - h p^T - p h^T; B'' = B' - b b^T / a
-            const int ntile = TB * (TB + 1) / 2;
-            for (int e = T.tid; e < ntile * 64; e += T.nthr) {
-                int ib, jb;
-                tile_of(e >> 6, ib, jb);
-                const int rr2 = (e >> 3) & 7, cc = e & 7;
-                const int ip = ib * 8 + rr2, jp = jb * 8 + cc;
-                if (ip >= md || jp >= md) continue;  // diagonal tiles hold both triangles
-                const int i = ip + 1, j = jp + 1;
-                const int x = tix(ib, jb) + tph(rr2, cc);
-                Gt[x] -= hh[i] * pw[j] + pw[i] * hh[j];
-                const double bij = Bt[x] - (hh[i] * yy[j] + yy[i] * hh[j]);
-                Bt[x] = outward ? 0.0 : bij - bv[ip] * bv[jp] / a_schur;
+            // trailing blocks (index i' = i - 1): G' = G - h p^T - p h^T; B'' = B' - b b^T / a (warp per
+            // tile; diagonal tiles hold both triangles)
+            {
+                const int r = T.lane >> 2, q = T.lane & 3;
+                const int ntile = TB * (TB + 1) / 2;
+                for (int t = T.warp; t < ntile; t += T.nwarps) {
+                    int ib, jb;
+                    tile_of(t, ib, jb);
+                    const int ip = ib * 8 + r;
+                    if (ip >= md) continue;
+                    const double hi = hh[ip + 1], pgi = pw[ip + 1], pbi = yy[ip + 1], bvi = bv[ip];
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        const int c = q + 4 * hf, jp = jb * 8 + c;
+                        if (jp >= md) continue;
+                        const int x = tix(ib, jb) + tph(r, c);
+                        const double hj = hh[jp + 1];
+                        Gt[x] -= hi * pw[jp + 1] + pgi * hj;
+                        const double bij = Bt[x] - (hi * yy[jp + 1] + pbi * hj);
+                        Bt[x] = outward ? 0.0 : bij - bvi * bv[jp] / a_schur;
+                    }
+                }
             }
             __syncthreads();
         }

@@ -448,9 +448,11 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         ctx->f_grid = of * ctx->num_sms;
         ctx->l_grid = ol * ctx->num_sms;
         ctx->t_grid = ot * ctx->num_sms;
-        // K2a with both matrices as lower 8 x 8 tiles, two chains per SM (factor_t.cuh);
-        // opt-in (SPECWALK_FACTOR_T=1) until measured
-        if (ctx->k2_variant == 1 && mp <= 8 * FT_TBMAX && getenv("SPECWALK_FACTOR_T")) {
+        // K2a with both matrices as lower 8 x 8 tiles, two chains per SM (factor_t.cuh): K2a
+        // 25.24 -> 20.61 ms per 65536-chain M100 round (profiles/r2ft1); SPECWALK_FACTOR_T=0 keeps
+        // factor_kernel<512> (A/B)
+        const char* ftenv = getenv("SPECWALK_FACTOR_T");
+        if (ctx->k2_variant == 1 && mp <= 8 * FT_TBMAX && !(ftenv && ftenv[0] == '0')) {
             ctx->ft_smem = sizeof(double) * ft_smem_doubles(mp);
             int o2 = 0;
             CK(cudaFuncSetAttribute(factor_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->ft_smem));

@@ -27,7 +27,7 @@ import pytest
 
 import oracle
 import specgen
-from _traj import PER_CALL_BUDGET, PER_CALL_BUDGET_HMC, traj_parity
+from _traj import PER_CALL_ASSERT, PER_CALL_BUDGET_HMC, traj_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -190,5 +190,5 @@ def test_per_call_parity_256_interior_and_boundary(kind, name):
     assert not bad_i, bad_i[:8]
     assert not bad_b, bad_b[:8]
     # the per-call budget the trajectory horizon assumes (tests/_traj.py, R27)
-    budget = PER_CALL_BUDGET_HMC if hmc else PER_CALL_BUDGET
+    budget = PER_CALL_BUDGET_HMC if hmc else PER_CALL_ASSERT
     assert max(dw_i + dw_b) <= budget, (max(dw_i + dw_b), budget)
