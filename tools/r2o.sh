@@ -6,7 +6,7 @@ $B > $O/bench_short.json 2>&1 && timeout 900 ncu --metrics gpu__time_duration.su
 python tools/summarize_launches.py $O/launches.csv 3 > $O/launches_timed.txt 2>&1
 F="ncu --set full --clock-control none --import-source on"
 S=/tmp/ncu_$T; mkdir -p $S
-python tools/prof_target.py m100 3 1 > $O/pt_m100.log 2>&1 && timeout 1200 $F -k regex:"gemm_f64_dmma|factor_kernel|lanczos2_kernel|tail_kernel" -s 16 -c 5 -o $S/m100_full python tools/prof_target.py m100 3 1 > $O/ncu_m100.log 2>&1
+python tools/prof_target.py m100 3 1 > $O/pt_m100.log 2>&1 && timeout 1200 $F -k regex:"gemm_f64_dmma|factor_t_kernel|factor_kernel|lanczos2_kernel|tail_kernel" -s 16 -c 5 -o $S/m100_full python tools/prof_target.py m100 3 1 > $O/ncu_m100.log 2>&1
 python tools/summarize_ncu.py full $S/m100_full.ncu-rep $O/m100_full.txt "M100 round 4: K1, factor, lanczos2, tail, K3" >> $O/summ.log 2>&1
 ncu -i $S/m100_full.ncu-rep --page source --csv --print-source sass -k regex:lanczos2_kernel > $S/lz2_sass.csv 2>> $O/summ.log; gzip -c $S/lz2_sass.csv > $O/lanczos2_sass.csv.gz
 ncu -i $S/m100_full.ncu-rep --page source --csv --print-source sass -k regex:factor_kernel > $S/factor_sass.csv 2>> $O/summ.log; gzip -c $S/factor_sass.csv > $O/factor_sass.csv.gz
