@@ -77,6 +77,11 @@ VARIANTS = [
     ("v5_rand_12_44", lambda: specgen.rand_cube(12, 44, 12)),
     ("v0_rand_16_60", lambda: specgen.rand_cube(16, 60, 13)),
     ("v1_rand_20_72", lambda: specgen.rand_cube(20, 72, 14)),
+    # factor_t_kernel's tile-count edges: m = 65 (a deflated start has md = 64: no padding),
+    # m = 97 (md = 96, 12 tiles), m = 104 (mp = 104, 13 tiles, md = 103)
+    ("v1_rand_10_65", lambda: specgen.rand_cube(10, 65, 18)),
+    ("v1_rand_12_97", lambda: specgen.rand_cube(12, 97, 19)),
+    ("v1_rand_14_104", lambda: specgen.rand_cube(14, 104, 20)),
     ("v3_rand_16_110", lambda: specgen.rand_cube(16, 110, 17)),  # fused <512, smem, KC 16> (104 < mp <= 112)
     ("v2_rand_24_120", lambda: specgen.rand_cube(24, 120, 15)),  # mp = 120: matrices no longer fit shared memory
     ("v2_rand_10_136", lambda: specgen.rand_cube(10, 136, 16)),

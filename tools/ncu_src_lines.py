@@ -48,7 +48,8 @@ for a, s, r in samp:
         except ValueError:
             pass
 srcs = {}
-for f in ['lanczos2.cuh', 'chord2.cuh', 'chord.cuh', 'chord3.cuh', 'chol_inv.cuh', 'chord_tail.inc', 'common.cuh', 'hmc.cuh', 'walk.cuh']:
+for f in ['lanczos2.cuh', 'chord2.cuh', 'chord.cuh', 'chord3.cuh', 'chol_inv.cuh', 'chord_tail.inc', 'common.cuh', 'hmc.cuh', 'walk.cuh',
+          'factor_t.cuh', 'colloc.cuh', 'hmc2.cuh']:
     try:
         srcs[f] = open('paper_2010_03817_b200/csrc/' + f).read().split('\n')
     except OSError:
