@@ -436,12 +436,14 @@ def run_ours(args):
                        "iterations per call); device events on the library stream, max over ranks"}
 
     # ---- north_star's second size: configs[4] (n = m = 200, 65536 billiard chains, seed 4), calls/s
-    # over scheduler rounds on the global-scratch K2 variant, with the K2 roofline fraction
+    # over scheduler rounds on the m > 112 K2 variant (split: global-scratch factor phase | lanczos_t | tail),
+    # with the K2 roofline fraction
     m200 = None
     if args.m200_rounds > 0:
         inst4 = specgen.config_instance(4)
         S4 = sw.Spectrahedron.from_instance(inst4, device=dev)
         stream4 = torch.cuda.ExternalStream(S4.stream(), device=dev)
+        k2cfg4 = S4.k2_config()
         S4.walk_begin(local_chains, 100, 2.0 * math.sqrt(200), 2000, SEED, chain_begin=begin)
         S4.walk_rounds(2)
         g0 = S4.walk_stats_now()
@@ -480,7 +482,8 @@ def run_ours(args):
                                 "frac": k2_ach4 / fp64_peak_tflops(), "flops_per_chain_call": f4["k2"],
                                 "lanczos_j": J4,
                                 "flop_model": "SURVEY 8(d).2: m^3/3 + m^3 + 2 J m^2, J measured on the device"},
-                "kernel_share": {k: v / max(sum(kt4["ms"].values()), 1e-9) for k, v in kt4["ms"].items()}}
+                "kernel_share": {k: v / max(sum(kt4["ms"].values()), 1e-9) for k, v in kt4["ms"].items()},
+                "k2_phases_ms": kt4.get("k2_phases_ms"), "k2_config": k2cfg4}
 
     # ---- collocation HMC-r (sec:hmcr P:1116-1158) on the configs[2] instance (n = m = 40),
     # truncated Gaussian exp(-|x|^2 / 2), q = 3 Chebyshev nodes (degree-4 segments), h = 0.25, 65536 chains

@@ -86,7 +86,8 @@ struct ChordParams {
     int wkind;      // walk kind (SPEC_WALK_*): 2 = Hit-and-Run, 3 = coordinate Hit-and-Run
     int need_tmin;  // the chord must return t- as well (oracle mode, Hit-and-Run walks)
     int hnr_boltz;  // Hit-and-Run for exp(-c^T x / Temp) instead of the uniform law
-    int gsplit;     // global-scratch chord_kernel2 as the factor phase only (m > 112 split, lanczos_cl.cuh)
+    int gsplit;     // global-scratch chord_kernel2 as the factor phase only (m > 112 split): 1 = M as full rows
+                    // (lanczos_cl.cuh), 2 = M as lower 8 x 8 tiles (lanczos_t.cuh)
     // K2 split into factor / Lanczos / tail kernels: per-slot work buffers
     double* wM;     // M = -L^{-1} A(v) L^{-T} (mdp x mdp rows, leading dimension ld)
     double* wL;     // L (lower incl. diagonal, rows of leading dimension ld)

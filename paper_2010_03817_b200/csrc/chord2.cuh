@@ -1508,11 +1508,28 @@ __global__ void __launch_bounds__(NT, (NT <= 128) ? SW_MINB128 : (NT <= 192) ? S
                     PROF_MARK(3);
                     double* Mw = P.wM + (size_t)slot * P.w_mstride;
                     double* Lw = P.wL + (size_t)slot * P.w_mstride;
-                    for (int i = T.warp; i < mdp; i += T.nwarps)
-                        for (int jx = T.lane; jx < mdp; jx += 32) {
-                            Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
-                            if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];
-                        }
+                    if (P.gsplit == 2) {
+                        // M as the lower 8 x 8 tiles lanczos_t_kernel holds: tile (I, J), I >= J, at
+                        // 64 (I (I + 1) / 2 + J), row-major; L packed by rows
+                        const int nbk = mdp >> 3;
+                        for (int I = T.warp; I < nbk; I += T.nwarps)
+                            for (int J = 0; J <= I; ++J) {
+                                double* Mt = Mw + 64 * (I * (I + 1) / 2 + J);
+#pragma unroll
+                                for (int h2 = 0; h2 < 2; ++h2) {
+                                    const int e = T.lane + 32 * h2, gi = 8 * I + (e >> 3), gj = 8 * J + (e & 7);
+                                    Mt[e] = -0.5 * (Bd[gi * ld + gj] + Bd[gj * ld + gi]);
+                                }
+                            }
+                        for (int i = T.warp; i < mdp; i += T.nwarps)
+                            for (int jx = T.lane; jx <= i; jx += 32) Lw[pk(i, jx)] = Gd[i * ld + jx];
+                    } else {
+                        for (int i = T.warp; i < mdp; i += T.nwarps)
+                            for (int jx = T.lane; jx < mdp; jx += 32) {
+                                Mw[i * ld + jx] = -0.5 * (Bd[i * ld + jx] + Bd[jx * ld + i]);
+                                if (jx <= i) Lw[pk(i, jx)] = Gd[i * ld + jx];
+                            }
+                    }
                 }
             }
             double* S = P.wS + (size_t)slot * P.w_sstride;

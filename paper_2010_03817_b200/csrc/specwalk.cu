@@ -22,6 +22,7 @@
 #include "chord3.cuh"
 #include "lanczos2.cuh"
 #include "lanczos_cl.cuh"
+#include "lanczos_t.cuh"
 #include "hmc.cuh"
 #include "hmc2.cuh"
 #include "colloc.cuh"
@@ -141,8 +142,10 @@ struct spec_ctx {
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
     int ft = 0, ft_grid = 0;   // K2a as factor_t_kernel (lower-tile storage, two chains per SM, m <= 104)
     size_t ft_smem = 0;
-    int g_split = 0, cl_grid = 0;  // m > 112: factor (global scratch) | lanczos_cl_kernel (2-CTA cluster) | tail
-    size_t cl_smem = 0;
+    // m > 112: factor (global scratch) | lanczos_t_kernel (g_split = 2) or lanczos_cl_kernel (2-CTA
+    // cluster, g_split = 1) | tail
+    int g_split = 0, cl_grid = 0, lt_grid = 0;
+    size_t cl_smem = 0, lt_smem = 0;
     size_t l2_smem = 0;
     size_t f_smem = 0, l_smem = 0, t_smem = 0;
     size_t smem_bytes = 0;
@@ -388,8 +391,30 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
         const LclLayout lcl(mp, ctx->ld);
         const size_t t_smem =
             sizeof(double) * ((((size_t)mp * (mp + 1) / 2 + 1) & ~(size_t)1) + 5 * (size_t)(mp + 8) + 64);
-        if (mp <= 2 * LCL_ROWS && sizeof(double) * (size_t)lcl.total <= 227 * 1024 && t_smem <= 227 * 1024 &&
-            getenv("SPECWALK_G_SPLIT")) {
+        // default for mp <= 208 (SPECWALK_G_SPLIT=0: the fused kernel, =cl: the cluster variant): the
+        // same factor phase and tail around lanczos_t_kernel (M as lower 8 x 8 tiles in one CTA's
+        // shared memory, lanczos_t.cuh)
+        const char* gsenv = getenv("SPECWALK_G_SPLIT");
+        const bool gs_off = gsenv && gsenv[0] == '0';
+        const bool gs_cl = gsenv && gsenv[0] == 'c';
+        const LztLayout lzt(mp);
+        if (!gs_off && !gs_cl && mp <= 8 * LZT_NBMAX && sizeof(double) * (size_t)lzt.total <= 227 * 1024 &&
+            t_smem <= 227 * 1024) {
+            ctx->lt_smem = sizeof(double) * (size_t)lzt.total;
+            ctx->t_smem = t_smem;
+            CK(cudaFuncSetAttribute(lanczos_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->lt_smem));
+            CK(cudaFuncSetAttribute(tail_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->t_smem));
+            int ol = 0, ot = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ol, lanczos_t_kernel, LZT_NT, ctx->lt_smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ot, tail_kernel<256>, 256, ctx->t_smem));
+            if (ol >= 1 && ot >= 1) {
+                ctx->g_split = 2;
+                ctx->lt_grid = ol * ctx->num_sms;
+                ctx->t_grid = ot * ctx->num_sms;
+            }
+        }
+        if (!ctx->g_split && mp <= 2 * LCL_ROWS && sizeof(double) * (size_t)lcl.total <= 227 * 1024 &&
+            t_smem <= 227 * 1024 && gs_cl) {
             ctx->cl_smem = sizeof(double) * (size_t)lcl.total;
             ctx->t_smem = t_smem;
             CK(cudaFuncSetAttribute(lanczos_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->cl_smem));
@@ -596,13 +621,17 @@ static ChordParams chord_params(spec_ctx* ctx, int mode) {
 static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cudaEvent_t* sub = nullptr) {
     if (ctx->g_split) {
         ChordParams Pf = P;
-        Pf.gsplit = 1;
+        Pf.gsplit = ctx->g_split;
         int grid = std::max(1, std::min(count_host, ctx->chord_grid_max));
         chord_kernel2<512, false, 16><<<grid, 512, ctx->g_smem, ctx->stream>>>(Pf);
         if (sub) cudaEventRecord(sub[0], ctx->stream);
         // clusters: one per chain (grid rounded to whole clusters)
-        const int cg2 = std::max(2, std::min(2 * count_host, ctx->cl_grid));
-        lanczos_cl_kernel<<<cg2, LCL_NT, ctx->cl_smem, ctx->stream>>>(P);
+        if (ctx->g_split == 2) {
+            lanczos_t_kernel<<<std::max(1, std::min(count_host, ctx->lt_grid)), LZT_NT, ctx->lt_smem, ctx->stream>>>(P);
+        } else {
+            const int cg2 = std::max(2, std::min(2 * count_host, ctx->cl_grid));
+            lanczos_cl_kernel<<<cg2, LCL_NT, ctx->cl_smem, ctx->stream>>>(P);
+        }
         if (sub) cudaEventRecord(sub[1], ctx->stream);
         tail_kernel<256><<<std::max(1, std::min(count_host, ctx->t_grid)), 256, ctx->t_smem, ctx->stream>>>(P);
         ctx->launches += 3;
@@ -1665,7 +1694,11 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
     static thread_local std::string s;
     if (!ctx) return "";
     char buf[256];
-    if (ctx->g_split)
+    if (ctx->g_split == 2)
+        snprintf(buf, sizeof(buf), "split (m > 112): chord_kernel2<512, global scratch> factor phase (%d CTAs) | "
+                 "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->chord_grid_max, ctx->lt_grid, ctx->t_grid);
+    else if (ctx->g_split)
         snprintf(buf, sizeof(buf), "split (m > 112): chord_kernel2<512, global scratch> factor phase (%d CTAs) | "
                  "lanczos_cl_kernel (2-CTA clusters, %d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->chord_grid_max, ctx->cl_grid, ctx->t_grid);
