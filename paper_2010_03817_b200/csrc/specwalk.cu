@@ -27,6 +27,7 @@
 #include "hmc2.cuh"
 #include "colloc.cuh"
 #include "factor_t.cuh"
+#include "factor_g.cuh"
 #include "estimators.cuh"
 #include <algorithm>
 
@@ -140,6 +141,8 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    int fg = 0, fg_grid = 0;   // m > 112 factor phase as factor_g_kernel<fg> (G/L/W tiles in shared memory, B tiles in L2)
+    size_t fg_smem = 0;
     int ft = 0, ft_grid = 0;   // K2a as factor_t_kernel (lower-tile storage, two chains per SM, m <= 104)
     size_t ft_smem = 0;
     // m > 112: factor (global scratch) | lanczos_t_kernel (g_split = 2) or lanczos_cl_kernel (2-CTA
@@ -411,6 +414,27 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
                 ctx->g_split = 2;
                 ctx->lt_grid = ol * ctx->num_sms;
                 ctx->t_grid = ot * ctx->num_sms;
+                // factor phase as factor_g_kernel (factor_g.cuh; SPECWALK_G_FACTOR=0: the global-scratch
+                // chord kernel, =256: 256 threads instead of 384)
+                const char* fge = getenv("SPECWALK_G_FACTOR");
+                const int fnt = (fge && atoi(fge) == 256) ? 256 : 384;
+                const size_t fgs = sizeof(double) * fg_smem_doubles(mp, fnt / 32);
+                if (!(fge && fge[0] == '0') && mp <= 8 * FG_TBMAX && fgs <= 227 * 1024 &&
+                    (long long)fg_scratch_doubles(mp) <= ctx->scratch_stride) {
+                    int og = 0;
+                    if (fnt == 256) {
+                        CK(cudaFuncSetAttribute(factor_g_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fgs));
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&og, factor_g_kernel<256>, 256, fgs));
+                    } else {
+                        CK(cudaFuncSetAttribute(factor_g_kernel<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fgs));
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&og, factor_g_kernel<384>, 384, fgs));
+                    }
+                    if (og >= 1) {
+                        ctx->fg = fnt;
+                        ctx->fg_smem = fgs;
+                        ctx->fg_grid = std::min(ctx->num_sms, ctx->scratch_ctas);
+                    }
+                }
             }
         }
         if (!ctx->g_split && mp <= 2 * LCL_ROWS && sizeof(double) * (size_t)lcl.total <= 227 * 1024 &&
@@ -623,7 +647,12 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
         ChordParams Pf = P;
         Pf.gsplit = ctx->g_split;
         int grid = std::max(1, std::min(count_host, ctx->chord_grid_max));
-        chord_kernel2<512, false, 16><<<grid, 512, ctx->g_smem, ctx->stream>>>(Pf);
+        if (ctx->g_split == 2 && ctx->fg == 384)
+            factor_g_kernel<384><<<std::max(1, std::min(count_host, ctx->fg_grid)), 384, ctx->fg_smem, ctx->stream>>>(P);
+        else if (ctx->g_split == 2 && ctx->fg == 256)
+            factor_g_kernel<256><<<std::max(1, std::min(count_host, ctx->fg_grid)), 256, ctx->fg_smem, ctx->stream>>>(P);
+        else
+            chord_kernel2<512, false, 16><<<grid, 512, ctx->g_smem, ctx->stream>>>(Pf);
         if (sub) cudaEventRecord(sub[0], ctx->stream);
         // clusters: one per chain (grid rounded to whole clusters)
         if (ctx->g_split == 2) {
@@ -1694,7 +1723,11 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
     static thread_local std::string s;
     if (!ctx) return "";
     char buf[256];
-    if (ctx->g_split == 2)
+    if (ctx->g_split == 2 && ctx->fg)
+        snprintf(buf, sizeof(buf), "split (m > 112): factor_g_kernel<%d> (G/L/W tiles in shared memory, B tiles in L2, %d CTAs) | "
+                 "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<256> (%d CTAs)",
+                 ctx->fg, ctx->fg_grid, ctx->lt_grid, ctx->t_grid);
+    else if (ctx->g_split == 2)
         snprintf(buf, sizeof(buf), "split (m > 112): chord_kernel2<512, global scratch> factor phase (%d CTAs) | "
                  "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<256> (%d CTAs)",
                  ctx->chord_grid_max, ctx->lt_grid, ctx->t_grid);

@@ -85,6 +85,11 @@ VARIANTS = [
     ("v3_rand_16_110", lambda: specgen.rand_cube(16, 110, 17)),  # fused <512, smem, KC 16> (104 < mp <= 112)
     ("v2_rand_24_120", lambda: specgen.rand_cube(24, 120, 15)),  # mp = 120: matrices no longer fit shared memory
     ("v2_rand_10_136", lambda: specgen.rand_cube(10, 136, 16)),
+    # factor_g_kernel's tile-count edges: m = 113 (mp = 120; a deflated start has md = 112: 14 tiles,
+    # no padding), m = 201 (mp = 208, 26 tiles; md = 200: 25 tiles), m = 208 (26 tiles, md = 207)
+    ("v2_rand_8_113", lambda: specgen.rand_cube(8, 113, 21)),
+    ("v2_rand_6_201", lambda: specgen.rand_cube(6, 201, 22)),
+    ("v2_rand_6_208", lambda: specgen.rand_cube(6, 208, 23)),
 ]
 
 
