@@ -18,6 +18,10 @@
 namespace sw {
 
 constexpr int FG_TBMAX = 26;  // mdp <= 208
+#ifndef SW_FG_KCH
+#define SW_FG_KCH 9
+#endif
+constexpr int FG_KCH = SW_FG_KCH;  // B tiles per load batch of the congruence (7: K2a 116.2 ms, 9: 114.0 ms per m = 200 round)
 
 __host__ __device__ inline size_t fg_smem_doubles(int mp, int nwarps) {
     const int TB = mp >> 3;
@@ -151,26 +155,37 @@ __device__ void fg_congruence(const Team& T, const double* Wt, const double* Bt,
         double yt[FG_TBMAX][2];
 #pragma unroll
         for (int K = 0; K < FG_TBMAX; ++K) yt[K][0] = yt[K][1] = 0.0;
-        // Y^T_JK = sum_{L <= J} W_JL B_LK: one W fragment feeds TB independent accumulators
+        // Y^T_JK = sum_{L <= J} W_JL B_LK: one W fragment feeds TB independent accumulators.  The B
+        // fragments come from L2 in branch-free batches of FG_KCH tiles (all loads of a batch in
+        // flight before its DMMAs): B_LK is the stored tile (L, K), element (q, r) / (4+q, r), for
+        // K <= L and the transpose of tile (K, L), element (r, q) / (r, 4+q), for K > L; K >= TB
+        // reads tile (TB - 1, .) again and feeds accumulators that are never used
+        const int os0 = tph(q, r), os1 = tph(4 + q, r), ot0 = tph(r, q), ot1 = tph(r, 4 + q);
         for (int L = 0; L <= J; ++L) {
             const double* Wl = Wt + tix(J, L);
             const double a0 = Wl[tph(r, q)], a1 = Wl[tph(r, 4 + q)];
             const double* Brow = Bt + tix(L, 0);  // tiles (L, K), K <= L
 #pragma unroll
-            for (int K = 0; K < FG_TBMAX; ++K) {
-                if (K < TB) {
-                    double b0, b1;
-                    if (L >= K) {  // B_LK stored: element (q, r) / (4+q, r)
-                        const double* Bl = Brow + K * 64;
-                        b0 = Bl[tph(q, r)];
-                        b1 = Bl[tph(4 + q, r)];
-                    } else {  // B_LK = B_KL^T: element (r, q) / (r, 4+q) of B_KL
-                        const double* Bl = Bt + tix(K, L);
-                        b0 = Bl[tph(r, q)];
-                        b1 = Bl[tph(r, 4 + q)];
+            for (int K0 = 0; K0 < FG_TBMAX; K0 += FG_KCH) {
+                double b[FG_KCH][2];
+#pragma unroll
+                for (int u = 0; u < FG_KCH; ++u) {
+                    const int K = K0 + u;
+                    if (K < FG_TBMAX) {
+                        const bool st = (L >= K);
+                        const int Kc = (K < TB) ? K : TB - 1;
+                        const double* Bl = st ? Brow + K * 64 : Bt + tix(Kc, L);
+                        b[u][0] = Bl[st ? os0 : ot0];
+                        b[u][1] = Bl[st ? os1 : ot1];
                     }
-                    dmma_t(yt[K], a0, b0);
-                    dmma_t(yt[K], a1, b1);
+                }
+#pragma unroll
+                for (int u = 0; u < FG_KCH; ++u) {
+                    const int K = K0 + u;
+                    if (K < FG_TBMAX) {
+                        dmma_t(yt[K], a0, b[u][0]);
+                        dmma_t(yt[K], a1, b[u][1]);
+                    }
                 }
             }
         }

@@ -14,8 +14,8 @@ F="ncu --set full --clock-control none --import-source on"
 S=/tmp/ncu_$T; mkdir -p $S
 python tools/prof_target.py m100 3 1 > $O/pt_m100.log 2>&1 && timeout 1200 $F -k regex:"gemm_f64_dmma|factor_t_kernel|factor_kernel|lanczos2_kernel|tail_kernel" -s 16 -c 5 -o $S/m100_full python tools/prof_target.py m100 3 1 > $O/ncu_m100.log 2>&1
 python tools/summarize_ncu.py full $S/m100_full.ncu-rep $O/m100_full.txt "M100 round 4: K1, factor_t, lanczos2, tail, K3" >> $O/summ.log 2>&1
-python tools/prof_target.py m200 2 1 > $O/pt_m200.log 2>&1 && timeout 1500 $F -k regex:"chord_kernel2|lanczos_t_kernel|tail_kernel" -s 6 -c 3 -o $S/m200_full python tools/prof_target.py m200 2 1 > $O/ncu_m200.log 2>&1
-python tools/summarize_ncu.py full $S/m200_full.ncu-rep $O/m200_full.txt "configs[4] round 3: factor phase chord_kernel2<512,false,16>, lanczos_t_kernel, tail" >> $O/summ.log 2>&1
-ncu -i $S/m200_full.ncu-rep --page source --csv --print-source sass -k regex:chord_kernel2 > $S/ck2_sass.csv 2>> $O/summ.log; gzip -c $S/ck2_sass.csv > $O/m200_factor_sass.csv.gz
+python tools/prof_target.py m200 2 1 > $O/pt_m200.log 2>&1 && timeout 1500 $F -k regex:"factor_g_kernel|lanczos_t_kernel|tail_kernel" -s 6 -c 3 -o $S/m200_full python tools/prof_target.py m200 2 1 > $O/ncu_m200.log 2>&1
+python tools/summarize_ncu.py full $S/m200_full.ncu-rep $O/m200_full.txt "configs[4] round 3: factor_g_kernel<384>, lanczos_t_kernel, tail_kernel" >> $O/summ.log 2>&1
+ncu -i $S/m200_full.ncu-rep --page source --csv --print-source sass -k regex:factor_g_kernel > $S/ck2_sass.csv 2>> $O/summ.log; gzip -c $S/ck2_sass.csv > $O/m200_factor_sass.csv.gz
 du -sh $O >> $O/summ.log
 echo done > $O/DONE
