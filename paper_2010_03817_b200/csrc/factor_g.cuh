@@ -7,7 +7,8 @@
 // M = -L^{-1} A(v) L^{-T}; the Schur deflation of a boundary start, R6): the Cholesky and
 // the triangular inverse never leave shared memory, and the congruence M = -W B W^T reads every
 // B tile from L2 straight into DMMA B fragments (Y^T_J = W_J: B in 2 x TBM register accumulators per
-// 8-column panel J, then M_IJ = -sum_K W_IK Y_KJ with the accumulators as the B operands).
+// 8-column panel J, then M_IJ = -sum_K W_IK Y_KJ with the accumulators as the B operands); the
+// fragment loads run one batch of FG_KCH tiles ahead of the DMMAs (two register buffers).
 // Panels are handed to the warps from a shared counter in order of decreasing cost (each panel's
 // arithmetic is self-contained and ordered, so the result does not depend on the assignment).
 // Outputs as the gsplit-2 factor phase: M as row-major lower 8 x 8 tiles (lanczos_t_kernel's
@@ -18,10 +19,13 @@
 namespace sw {
 
 constexpr int FG_TBMAX = 26;  // mdp <= 208
-#ifndef SW_FG_KCH
-#define SW_FG_KCH 9
+#ifndef SW_FG_PIPE
+#define SW_FG_PIPE 1  // software-pipelined B-fragment loads in the congruence (0: one batch at a time)
 #endif
-constexpr int FG_KCH = SW_FG_KCH;  // B tiles per load batch of the congruence (7: K2a 116.2 ms, 9: 114.0 ms per m = 200 round)
+#ifndef SW_FG_KCH
+#define SW_FG_KCH 5
+#endif
+constexpr int FG_KCH = SW_FG_KCH;  // B tiles per load batch of the congruence (unpipelined 7: K2a 116.2 ms, 9: 114.0 ms per m = 200 round; pipelined 5: 104.4 ms)
 
 __host__ __device__ inline size_t fg_smem_doubles(int mp, int nwarps) {
     const int TB = mp >> 3;
@@ -161,6 +165,48 @@ __device__ void fg_congruence(const Team& T, const double* Wt, const double* Bt,
         // K <= L and the transpose of tile (K, L), element (r, q) / (r, 4+q), for K > L; K >= TB
         // reads tile (TB - 1, .) again and feeds accumulators that are never used
         const int os0 = tph(q, r), os1 = tph(4 + q, r), ot0 = tph(r, q), ot1 = tph(r, 4 + q);
+#if SW_FG_PIPE
+        // software pipeline over the (L, batch) sequence: the loads of the next batch are issued
+        // before the DMMAs of the current one (two register buffers; FG_NCH is even, so the buffer
+        // of batch c is c & 1 for every L)
+        constexpr int FG_NCH = (FG_TBMAX + FG_KCH - 1) / FG_KCH;
+        static_assert(FG_NCH % 2 == 0, "FG_NCH must be even");
+        double b[2][FG_KCH][2];
+        auto load_batch = [&](int L, int c, double (&bb)[FG_KCH][2]) {
+            const double* Brow = Bt + tix(L, 0);
+#pragma unroll
+            for (int u = 0; u < FG_KCH; ++u) {
+                const int K = c * FG_KCH + u;
+                if (K < FG_TBMAX) {
+                    const bool st = (L >= K);
+                    const int Kc = (K < TB) ? K : TB - 1;
+                    const double* Bl = st ? Brow + K * 64 : Bt + tix(Kc, L);
+                    bb[u][0] = Bl[st ? os0 : ot0];
+                    bb[u][1] = Bl[st ? os1 : ot1];
+                }
+            }
+        };
+        load_batch(0, 0, b[0]);
+        for (int L = 0; L <= J; ++L) {
+            const double* Wl = Wt + tix(J, L);
+            const double a0 = Wl[tph(r, q)], a1 = Wl[tph(r, 4 + q)];
+#pragma unroll
+            for (int c = 0; c < FG_NCH; ++c) {
+                if (c + 1 < FG_NCH)
+                    load_batch(L, c + 1, b[(c + 1) & 1]);
+                else if (L < J)
+                    load_batch(L + 1, 0, b[0]);
+#pragma unroll
+                for (int u = 0; u < FG_KCH; ++u) {
+                    const int K = c * FG_KCH + u;
+                    if (K < FG_TBMAX) {
+                        dmma_t(yt[K], a0, b[c & 1][u][0]);
+                        dmma_t(yt[K], a1, b[c & 1][u][1]);
+                    }
+                }
+            }
+        }
+#else
         for (int L = 0; L <= J; ++L) {
             const double* Wl = Wt + tix(J, L);
             const double a0 = Wl[tph(r, q)], a1 = Wl[tph(r, 4 + q)];
@@ -189,6 +235,7 @@ __device__ void fg_congruence(const Team& T, const double* Wt, const double* Bt,
                 }
             }
         }
+#endif
         // M_IJ = -sum_{K <= I} W_IK Y_KJ, two output tiles at a time (independent chains)
         for (int I0 = J; I0 < TB; I0 += 2) {
             double accs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
