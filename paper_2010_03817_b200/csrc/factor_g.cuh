@@ -22,9 +22,13 @@ constexpr int FG_TBMAX = 26;  // mdp <= 208
 #ifndef SW_FG_PIPE
 #define SW_FG_PIPE 1  // software-pipelined B-fragment loads in the congruence (0: one batch at a time)
 #endif
+#ifndef SW_FG_S2W
+#define SW_FG_S2W 2
+#endif
 #ifndef SW_FG_KCH
 #define SW_FG_KCH 5
 #endif
+constexpr int FG_S2W = SW_FG_S2W;  // output tiles per step of the congruence's second stage
 constexpr int FG_KCH = SW_FG_KCH;  // B tiles per load batch of the congruence (unpipelined 7: K2a 116.2 ms, 9: 114.0 ms per m = 200 round; pipelined 5: 104.4 ms)
 
 __host__ __device__ inline size_t fg_smem_doubles(int mp, int nwarps) {
@@ -236,27 +240,28 @@ __device__ void fg_congruence(const Team& T, const double* Wt, const double* Bt,
             }
         }
 #endif
-        // M_IJ = -sum_{K <= I} W_IK Y_KJ, two output tiles at a time (independent chains)
-        for (int I0 = J; I0 < TB; I0 += 2) {
-            double accs[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-            const bool two = (I0 + 1 < TB);
-            const double* W0 = Wt + tix(I0, 0);
-            const double* W1 = Wt + tix(two ? I0 + 1 : I0, 0);
+        // M_IJ = -sum_{K <= I} W_IK Y_KJ, FG_S2W output tiles at a time (independent chains)
+        for (int I0 = J; I0 < TB; I0 += FG_S2W) {
+            double accs[FG_S2W][2];
+            const double* Wr[FG_S2W];
+#pragma unroll
+            for (int u = 0; u < FG_S2W; ++u) {
+                accs[u][0] = accs[u][1] = 0.0;
+                Wr[u] = Wt + tix((I0 + u < TB) ? I0 + u : I0, 0);
+            }
 #pragma unroll
             for (int K = 0; K < FG_TBMAX; ++K) {
-                if (K <= I0) {
-                    const double* Wk = W0 + K * 64;
-                    dmma_t(accs[0], -Wk[tph(r, 2 * q)], yt[K][0]);
-                    dmma_t(accs[0], -Wk[tph(r, 2 * q + 1)], yt[K][1]);
-                }
-                if (two && K <= I0 + 1) {
-                    const double* Wk = W1 + K * 64;
-                    dmma_t(accs[1], -Wk[tph(r, 2 * q)], yt[K][0]);
-                    dmma_t(accs[1], -Wk[tph(r, 2 * q + 1)], yt[K][1]);
+#pragma unroll
+                for (int u = 0; u < FG_S2W; ++u) {
+                    if (I0 + u < TB && K <= I0 + u) {
+                        const double* Wk = Wr[u] + K * 64;
+                        dmma_t(accs[u], -Wk[tph(r, 2 * q)], yt[K][0]);
+                        dmma_t(accs[u], -Wk[tph(r, 2 * q + 1)], yt[K][1]);
+                    }
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < FG_S2W; ++u) {
                 const int I = I0 + u;
                 if (I >= TB) break;
                 const double* acc = accs[u];
