@@ -439,7 +439,7 @@ __device__ __forceinline__ void back_solve_lt_packed(const Team& T, const double
 
 // ---------------------------------------------------------------- K2c
 template <int NT>
-__global__ void __launch_bounds__(NT, SW_TAIL_CTAS) tail_kernel(ChordParams P) {
+__global__ void __launch_bounds__(NT, (NT > 256) ? 1 : SW_TAIL_CTAS) tail_kernel(ChordParams P) {
     extern __shared__ __align__(16) double smem_dyn[];
     Team T;
     T.tid = threadIdx.x;

@@ -141,6 +141,7 @@ struct spec_ctx {
     int k2_split = 0;  // K2 as factor / Lanczos / tail kernels (chord3.cuh)
     int f_grid = 0, l_grid = 0, t_grid = 0;
     int lz2 = 0, l2_grid = 0;  // K2b as lanczos2_kernel (two chains per SM, m <= 104)
+    int t512 = 0;              // m > 112 split tail with 512 threads (one CTA per SM)
     int fg = 0, fg_grid = 0;   // m > 112 factor phase as factor_g_kernel<fg> (G/L/W tiles in shared memory, B tiles in L2)
     size_t fg_smem = 0;
     int ft = 0, ft_grid = 0;   // K2a as factor_t_kernel (lower-tile storage, two chains per SM, m <= 104)
@@ -414,6 +415,13 @@ static int create_impl(spec_ctx* ctx, int n, int m, const double* A, const doubl
                 ctx->g_split = 2;
                 ctx->lt_grid = ol * ctx->num_sms;
                 ctx->t_grid = ot * ctx->num_sms;
+                // one tail CTA per SM (L no longer fits twice, mp > 152): 512 threads (SPECWALK_T512=0: 256)
+                if (ot == 1 && !(getenv("SPECWALK_T512") && getenv("SPECWALK_T512")[0] == '0')) {
+                    int o5 = 0;
+                    CK(cudaFuncSetAttribute(tail_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->t_smem));
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o5, tail_kernel<512>, 512, ctx->t_smem));
+                    if (o5 >= 1) ctx->t512 = 1;
+                }
                 // factor phase as factor_g_kernel (factor_g.cuh; SPECWALK_G_FACTOR=0: the global-scratch
                 // chord kernel, =256: 256 threads instead of 384)
                 const char* fge = getenv("SPECWALK_G_FACTOR");
@@ -662,7 +670,10 @@ static void launch_chord(spec_ctx* ctx, const ChordParams& P, int count_host, cu
             lanczos_cl_kernel<<<cg2, LCL_NT, ctx->cl_smem, ctx->stream>>>(P);
         }
         if (sub) cudaEventRecord(sub[1], ctx->stream);
-        tail_kernel<256><<<std::max(1, std::min(count_host, ctx->t_grid)), 256, ctx->t_smem, ctx->stream>>>(P);
+        if (ctx->t512)
+            tail_kernel<512><<<std::max(1, std::min(count_host, ctx->t_grid)), 512, ctx->t_smem, ctx->stream>>>(P);
+        else
+            tail_kernel<256><<<std::max(1, std::min(count_host, ctx->t_grid)), 256, ctx->t_smem, ctx->stream>>>(P);
         ctx->launches += 3;
         return;
     }
