@@ -1736,8 +1736,8 @@ extern "C" const char* spec_k2_config(spec_ctx* ctx) {
     char buf[256];
     if (ctx->g_split == 2 && ctx->fg)
         snprintf(buf, sizeof(buf), "split (m > 112): factor_g_kernel<%d> (G/L/W tiles in shared memory, B tiles in L2, %d CTAs) | "
-                 "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<256> (%d CTAs)",
-                 ctx->fg, ctx->fg_grid, ctx->lt_grid, ctx->t_grid);
+                 "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<%d> (%d CTAs)",
+                 ctx->fg, ctx->fg_grid, ctx->lt_grid, ctx->t512 ? 512 : 256, ctx->t_grid);
     else if (ctx->g_split == 2)
         snprintf(buf, sizeof(buf), "split (m > 112): chord_kernel2<512, global scratch> factor phase (%d CTAs) | "
                  "lanczos_t_kernel (M as lower tiles in shared memory, %d CTAs) | tail_kernel<256> (%d CTAs)",
